@@ -1,0 +1,152 @@
+"""fp64 CPU oracle for the TDBP hot path (arXiv 2101.05888) -- TEST INFRASTRUCTURE.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` /
+``--impl reference`` legs may import this package.  The product path
+(``paper_2101_05888_b200``) never imports it; the two share no code.
+
+What is computed is documented in ``oracle/oracle.c`` (the definition of
+SURVEY §8(c), PAPER.md Eq. (eqn:backprojection) P:89-92).  This module is only
+ctypes marshalling plus the gcc build of ``liboracle.so``.
+
+Parity status: every function here is pinned (tests/test_oracle_pins.py):
+``tdbp_points`` / ``tdbp_grid`` by closed forms, hand-computed mono/bistatic
+delays, zero-extension values, point-target physics and invariants;
+``rangecompress`` by the autocorrelation-peak, shift and mainlobe pins.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so with gcc (-O2, OpenMP, no fast-math)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-std=c11",
+                               "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        build()
+        lib = ctypes.CDLL(_LIB)
+        f64p = ctypes.POINTER(ctypes.c_double)
+        f32p = ctypes.POINTER(ctypes.c_float)
+        i64p = ctypes.POINTER(ctypes.c_int64)
+        lib.oracle_tdbp_points.argtypes = [f32p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                           f64p, f64p, f64p, ctypes.c_double, ctypes.c_double,
+                                           ctypes.c_double, f64p, ctypes.c_int64, f64p, i64p]
+        lib.oracle_tdbp_points.restype = ctypes.c_int
+        lib.oracle_tdbp_grid_pixels.argtypes = [f32p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                                f64p, f64p, f64p, ctypes.c_double, ctypes.c_double,
+                                                ctypes.c_double, f64p, f64p, f64p, f64p, i64p,
+                                                ctypes.c_int64, f64p, i64p]
+        lib.oracle_tdbp_grid_pixels.restype = ctypes.c_int
+        lib.oracle_rangecompress.argtypes = [f32p, ctypes.c_int64, ctypes.c_int32, f32p,
+                                             ctypes.c_int32, f64p]
+        lib.oracle_rangecompress.restype = ctypes.c_int
+        lib.oracle_num_threads.restype = ctypes.c_int
+        _lib = lib
+    return _lib
+
+
+def _p(a, ct):
+    return a.ctypes.data_as(ctypes.POINTER(ct)) if a is not None else None
+
+
+def _echo_arrays(echoes, tx, rx, t0):
+    echoes = np.ascontiguousarray(echoes)
+    if echoes.dtype == np.complex64:
+        echoes = echoes.view(np.float32).reshape(echoes.shape + (2,))
+    if echoes.dtype != np.float32 or echoes.ndim != 4 or echoes.shape[-1] != 2:
+        raise ValueError("echoes must be complex64 [P][E][Ns] or float32 [P][E][Ns][2]")
+    P, E, Ns = echoes.shape[:3]
+    tx = np.ascontiguousarray(tx, dtype=np.float64).reshape(P, 3)
+    rx = np.ascontiguousarray(rx, dtype=np.float64).reshape(P, E, 3)
+    t0 = None if t0 is None else np.ascontiguousarray(t0, dtype=np.float64).reshape(P)
+    return echoes, P, E, Ns, tx, rx, t0
+
+
+def tdbp_points(echoes, tx, rx, t0, fc, fs, c, pts, with_count=False):
+    """I(x) at explicit fp64 points ``pts[N][3]``; returns complex128 [N] (and N_u counts)."""
+    lib = _load()
+    echoes, P, E, Ns, tx, rx, t0 = _echo_arrays(echoes, tx, rx, t0)
+    pts = np.ascontiguousarray(pts, dtype=np.float64).reshape(-1, 3)
+    N = pts.shape[0]
+    out = np.zeros((N, 2), dtype=np.float64)
+    cnt = np.zeros(N, dtype=np.int64) if with_count else None
+    rc = lib.oracle_tdbp_points(_p(echoes, ctypes.c_float), P, E, Ns, _p(tx, ctypes.c_double),
+                                _p(rx, ctypes.c_double), _p(t0, ctypes.c_double), float(fc),
+                                float(fs), float(c), _p(pts, ctypes.c_double), N,
+                                _p(out, ctypes.c_double), _p(cnt, ctypes.c_int64))
+    if rc != 0:
+        raise ValueError("oracle_tdbp_points: invalid arguments")
+    res = out[:, 0] + 1j * out[:, 1]
+    return (res, cnt) if with_count else res
+
+
+def tdbp_grid(echoes, tx, rx, t0, fc, fs, c, grid, idx=None, with_count=False):
+    """I at grid pixels.  ``grid`` is a dict with origin, step_x, step_y, step_z (3-vectors)
+    and nx, ny, nz.  ``idx`` is an int64 [N][3] array of (ix, iy, iz); None = full grid,
+    returned as [nz][ny][nx]."""
+    lib = _load()
+    echoes, P, E, Ns, tx, rx, t0 = _echo_arrays(echoes, tx, rx, t0)
+    full = idx is None
+    if full:
+        iz, iy, ix = np.meshgrid(np.arange(grid["nz"]), np.arange(grid["ny"]), np.arange(grid["nx"]),
+                                 indexing="ij")
+        idx = np.stack([ix.ravel(), iy.ravel(), iz.ravel()], axis=1)
+    idx = np.ascontiguousarray(idx, dtype=np.int64).reshape(-1, 3)
+    N = idx.shape[0]
+    vec = {k: np.ascontiguousarray(grid[k], dtype=np.float64).reshape(3)
+           for k in ("origin", "step_x", "step_y", "step_z")}
+    out = np.zeros((N, 2), dtype=np.float64)
+    cnt = np.zeros(N, dtype=np.int64) if with_count else None
+    rc = lib.oracle_tdbp_grid_pixels(_p(echoes, ctypes.c_float), P, E, Ns, _p(tx, ctypes.c_double),
+                                     _p(rx, ctypes.c_double), _p(t0, ctypes.c_double), float(fc),
+                                     float(fs), float(c), _p(vec["origin"], ctypes.c_double),
+                                     _p(vec["step_x"], ctypes.c_double),
+                                     _p(vec["step_y"], ctypes.c_double),
+                                     _p(vec["step_z"], ctypes.c_double), _p(idx, ctypes.c_int64), N,
+                                     _p(out, ctypes.c_double), _p(cnt, ctypes.c_int64))
+    if rc != 0:
+        raise ValueError("oracle_tdbp_grid_pixels: invalid arguments")
+    res = out[:, 0] + 1j * out[:, 1]
+    if full:
+        res = res.reshape(grid["nz"], grid["ny"], grid["nx"])
+        if cnt is not None:
+            cnt = cnt.reshape(grid["nz"], grid["ny"], grid["nx"])
+    return (res, cnt) if with_count else res
+
+
+def rangecompress(raw, replica):
+    """Direct fp64 correlation y[n] = sum_m x[n+m] conj(r[m]) per channel; raw complex64 [..., Ns]."""
+    lib = _load()
+    raw = np.ascontiguousarray(raw, dtype=np.complex64)
+    replica = np.ascontiguousarray(replica, dtype=np.complex64).ravel()
+    shape = raw.shape
+    Ns = shape[-1]
+    nch = int(np.prod(shape[:-1])) if len(shape) > 1 else 1
+    out = np.zeros((nch, Ns, 2), dtype=np.float64)
+    rc = lib.oracle_rangecompress(_p(raw.view(np.float32), ctypes.c_float), nch, Ns,
+                                  _p(replica.view(np.float32), ctypes.c_float), replica.size,
+                                  _p(out, ctypes.c_double))
+    if rc != 0:
+        raise ValueError("oracle_rangecompress: invalid arguments")
+    return (out[..., 0] + 1j * out[..., 1]).reshape(shape)
+
+
+def num_threads() -> int:
+    return int(_load().oracle_num_threads())

@@ -1,0 +1,182 @@
+/*
+ * oracle/oracle.c -- plain, slow, obviously-correct fp64 CPU oracle for the
+ * time-domain backprojection (TDBP) hot path of Gerg et al., "GPU Acceleration
+ * for Synthetic Aperture Sonar Image Reconstruction" (arXiv 2101.05888).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load this library.
+ * The product path (paper_2101_05888_b200/) never links, imports or calls it,
+ * and this file shares no code, header, table or constant with the CUDA path.
+ *
+ * Citation key: P:n = /root/reference/PAPER.md line n (sections / equations as
+ * labelled there); readings R1..R13 are listed in DESIGN.md ("Readings").
+ *
+ * What it computes:
+ *
+ *   I(x) = sum_{p=0}^{P-1} sum_{e=0}^{E-1}  ehat_{p,e}(u_{p,e}(x)) * exp(+j 2 pi fc tau_{p,e}(x))
+ *
+ *   tau_{p,e}(x) = (|x - tx_p| + |x - rx_{p,e}|) / c      -- delay argument of
+ *                  Eq. (eqn:backprojection), tx stationary during
+ *                  transmit; stop-and-hop per element (R5)
+ *   u_{p,e}(x)   = (tau - t0_p) * fs                      -- sample n is taken
+ *                  t0_p + n/fs after ping p's transmit (R4)
+ *   ehat(u)      = (1-a) d[k] + a d[k+1],  k = floor(u), a = u - k,
+ *                  d[n] = 0 for n outside 0..Ns-1         -- linear, zero-extended (R1, R2)
+ *   exp(+j...)   -- re-modulation of basebanded echoes (R3)
+ *   weight 1, no FOV gate, no normalisation (R6, R7, R10), pixel centre =
+ *   origin + ix*step_x + iy*step_y + iz*step_z (R8), single sound speed (R9).
+ *
+ * Every quantity is fp64 (positions, tau, u, phase, std sin/cos, accumulator);
+ * only the echoes are complex64, because that is what the caller provides.
+ * Loop order per pixel: ping-major, then element (R11).
+ *
+ * Range compression (the paper presumes compressed data,
+ * S:195):  y[n] = sum_{m=0}^{Nr-1} x[n+m] * conj(r[m]),  x[k] = 0 for k >= Ns,
+ * the direct O(Ns*Nr) correlation in fp64.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define ORACLE_TWO_PI 6.283185307179586476925286766559
+
+/* d[n] with zero extension outside 0..Ns-1 (reading R2). */
+static inline void sample_at(const float* ch, int32_t Ns, int64_t n, double* re, double* im) {
+  if (n < 0 || n >= (int64_t)Ns) { *re = 0.0; *im = 0.0; return; }
+  *re = (double)ch[2 * n];
+  *im = (double)ch[2 * n + 1];
+}
+
+/* Euclidean distance |a - b| in fp64. */
+static inline double dist3(const double* a, const double* b) {
+  double dx = a[0] - b[0], dy = a[1] - b[1], dz = a[2] - b[2];
+  return sqrt(dx * dx + dy * dy + dz * dz);
+}
+
+/* Pixel centre (reading R8): origin + ix*step_x + iy*step_y + iz*step_z. */
+void oracle_pixel_centre(const double* origin, const double* step_x, const double* step_y,
+                         const double* step_z, int64_t ix, int64_t iy, int64_t iz, double* out) {
+  for (int a = 0; a < 3; ++a)
+    out[a] = origin[a] + (double)ix * step_x[a] + (double)iy * step_y[a] + (double)iz * step_z[a];
+}
+
+/*
+ * One term of the sum for one pixel x, ping p, element e (the whole method for
+ * one (pixel, ping, element) triple).  Returns 1 if the interpolation support
+ * meets the recorded window, i.e. u in (-1, Ns), else 0 (the term is then 0).
+ */
+static int one_term(const double* x, const float* ch, int32_t Ns, const double* tx, const double* rx,
+                    double t0, double fc, double fs, double c, double* acc_re, double* acc_im) {
+  double tau = (dist3(x, tx) + dist3(x, rx)) / c;           /* Eq. 1 delay */
+  double u = (tau - t0) * fs;                                /* R4 */
+  double kf = floor(u);
+  double a = u - kf;
+  int64_t k = (int64_t)kf;
+  double d0r, d0i, d1r, d1i;
+  sample_at(ch, Ns, k, &d0r, &d0i);
+  sample_at(ch, Ns, k + 1, &d1r, &d1i);
+  double er = (1.0 - a) * d0r + a * d1r;                     /* R1 linear */
+  double ei = (1.0 - a) * d0i + a * d1i;
+  double ph = ORACLE_TWO_PI * fc * tau;                      /* R3 exp(+j 2 pi fc tau) */
+  double cs = cos(ph), sn = sin(ph);
+  *acc_re += er * cs - ei * sn;
+  *acc_im += er * sn + ei * cs;
+  return (u > -1.0 && u < (double)Ns) ? 1 : 0;
+}
+
+/*
+ * TDBP at an explicit list of N points (fp64 NED metres).
+ *   echoes : complex64 [P][E][Ns] interleaved (re, im)
+ *   tx     : [P][3], rx : [P][E][3], t0 : [P] or NULL (= 0)
+ *   out    : complex128 [N] interleaved; n_in : [N] or NULL, count of terms
+ *            with u in (-1, Ns) (SURVEY §8(d) N_u)
+ * Returns 0, or -1 on invalid sizes.
+ */
+int oracle_tdbp_points(const float* echoes, int32_t P, int32_t E, int32_t Ns, const double* tx,
+                       const double* rx, const double* t0, double fc, double fs, double c,
+                       const double* pts, int64_t N, double* out, int64_t* n_in) {
+  if (P < 1 || E < 1 || Ns < 1 || N < 0 || !(c > 0) || !(fs > 0)) return -1;
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int64_t i = 0; i < N; ++i) {
+    const double* x = pts + 3 * i;
+    double ar = 0.0, ai = 0.0;
+    int64_t cnt = 0;
+    for (int32_t p = 0; p < P; ++p) {            /* ping-major (R11) */
+      double t0p = t0 ? t0[p] : 0.0;
+      for (int32_t e = 0; e < E; ++e) {
+        const float* ch = echoes + 2 * ((int64_t)p * E + e) * (int64_t)Ns;
+        cnt += one_term(x, ch, Ns, tx + 3 * p, rx + 3 * ((int64_t)p * E + e), t0p, fc, fs, c, &ar, &ai);
+      }
+    }
+    out[2 * i] = ar;
+    out[2 * i + 1] = ai;
+    if (n_in) n_in[i] = cnt;
+  }
+  return 0;
+}
+
+/*
+ * TDBP at grid pixels given by index triples idx[N][3] = (ix, iy, iz) of the
+ * grid (origin, step_x, step_y, step_z), reading R8.
+ */
+int oracle_tdbp_grid_pixels(const float* echoes, int32_t P, int32_t E, int32_t Ns, const double* tx,
+                            const double* rx, const double* t0, double fc, double fs, double c,
+                            const double* origin, const double* step_x, const double* step_y,
+                            const double* step_z, const int64_t* idx, int64_t N, double* out,
+                            int64_t* n_in) {
+  if (N < 0) return -1;
+  int rc = 0;
+  /* chunked so the point list stays small */
+  const int64_t CHUNK = 4096;
+  double pts[3 * 4096];
+  for (int64_t s = 0; s < N && rc == 0; s += CHUNK) {
+    int64_t n = (N - s) < CHUNK ? (N - s) : CHUNK;
+    for (int64_t i = 0; i < n; ++i) {
+      const int64_t* q = idx + 3 * (s + i);
+      oracle_pixel_centre(origin, step_x, step_y, step_z, q[0], q[1], q[2], pts + 3 * i);
+    }
+    rc = oracle_tdbp_points(echoes, P, E, Ns, tx, rx, t0, fc, fs, c, pts, n, out + 2 * s,
+                            n_in ? n_in + s : NULL);
+  }
+  return rc;
+}
+
+/*
+ * Direct matched-filter correlation (row a1):
+ *   y[n] = sum_{m=0}^{Nr-1} x[n+m] * conj(r[m]),  n = 0..Ns-1,  x[k] = 0 for k >= Ns.
+ *   raw : complex64 [nch][Ns], replica : complex64 [Nr], out : complex128 [nch][Ns].
+ */
+int oracle_rangecompress(const float* raw, int64_t nch, int32_t Ns, const float* replica, int32_t Nr,
+                         double* out) {
+  if (nch < 0 || Ns < 1 || Nr < 1) return -1;
+#pragma omp parallel for schedule(static)
+  for (int64_t ch = 0; ch < nch; ++ch) {
+    const float* x = raw + 2 * ch * (int64_t)Ns;
+    double* y = out + 2 * ch * (int64_t)Ns;
+    for (int32_t n = 0; n < Ns; ++n) {
+      double yr = 0.0, yi = 0.0;
+      for (int32_t m = 0; m < Nr && n + m < Ns; ++m) {
+        double xr = x[2 * (n + m)], xi = x[2 * (n + m) + 1];
+        double rr = replica[2 * m], ri = -(double)replica[2 * m + 1];  /* conj(r[m]) */
+        yr += xr * rr - xi * ri;
+        yi += xr * ri + xi * rr;
+      }
+      y[2 * n] = yr;
+      y[2 * n + 1] = yi;
+    }
+  }
+  return 0;
+}
+
+/* Number of OpenMP threads the oracle will use (for the cpu_baseline "cores"). */
+int oracle_num_threads(void) {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}

@@ -1,0 +1,161 @@
+// Pipe-throughput microbenchmarks for the TDBP roofline.
+// Measures, on the B200 it runs on, per-SM per-clock throughput of the
+// instruction classes the backprojection inner loop is made of:
+//   FFMA (3-register form), FFMA with an immediate, MUFU.SIN+MUFU.COS (__sinf/__cosf),
+//   MUFU.RSQ (rsqrtf), LDS.128 (conflict-free), and a mixed "issue" probe.
+// Output: one JSON line per probe on stdout.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o pipes pipes.cu
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { \
+  fprintf(stderr, "CUDA %s at %s:%d\n", cudaGetErrorString(e_), __FILE__, __LINE__); return 1; } } while (0)
+
+constexpr int CH = 8;        // independent chains per thread
+constexpr int ITERS = 4096;
+
+__device__ unsigned long long g_cycles[4096];
+
+__global__ void k_ffma(float* out, float a, float b) {
+  float x[CH];
+#pragma unroll
+  for (int i = 0; i < CH; ++i) x[i] = threadIdx.x * 1e-3f + i;
+  float y = a * 0.5f, z = b * 0.25f;
+  unsigned long long t0 = clock64();
+  for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+    for (int i = 0; i < CH; ++i) x[i] = fmaf(x[i], y, z);
+  }
+  unsigned long long t1 = clock64();
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < CH; ++i) s += x[i];
+  if (s == 1234.5f) out[0] = s;
+  if (threadIdx.x == 0) g_cycles[blockIdx.x] = t1 - t0;
+}
+
+__global__ void k_ffma_imm(float* out, float a) {
+  float x[CH];
+#pragma unroll
+  for (int i = 0; i < CH; ++i) x[i] = threadIdx.x * 1e-3f + i;
+  float y = a * 0.5f;
+  unsigned long long t0 = clock64();
+  for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+    for (int i = 0; i < CH; ++i) x[i] = fmaf(x[i], y, 0.7071f);
+  }
+  unsigned long long t1 = clock64();
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < CH; ++i) s += x[i];
+  if (s == 1234.5f) out[0] = s;
+  if (threadIdx.x == 0) g_cycles[blockIdx.x] = t1 - t0;
+}
+
+// sin + cos of the same argument: 2 MUFU per chain step (+ FMUL.RZ + FADD)
+__global__ void k_sincos(float* out, float a) {
+  float x[CH];
+#pragma unroll
+  for (int i = 0; i < CH; ++i) x[i] = threadIdx.x * 1e-3f + i;
+  unsigned long long t0 = clock64();
+  for (int it = 0; it < ITERS / 4; ++it) {
+#pragma unroll
+    for (int i = 0; i < CH; ++i) x[i] = __sinf(x[i]) + __cosf(x[i]);
+  }
+  unsigned long long t1 = clock64();
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < CH; ++i) s += x[i];
+  if (s == 1234.5f) out[0] = s;
+  if (threadIdx.x == 0) g_cycles[blockIdx.x] = t1 - t0;
+}
+
+__global__ void k_rsqrt(float* out, float a) {
+  float x[CH];
+#pragma unroll
+  for (int i = 0; i < CH; ++i) x[i] = threadIdx.x * 1e-3f + i + 1.f;
+  unsigned long long t0 = clock64();
+  for (int it = 0; it < ITERS / 4; ++it) {
+#pragma unroll
+    for (int i = 0; i < CH; ++i) x[i] = rsqrtf(x[i]);
+  }
+  unsigned long long t1 = clock64();
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < CH; ++i) s += x[i];
+  if (s == 1234.5f) out[0] = s;
+  if (threadIdx.x == 0) g_cycles[blockIdx.x] = t1 - t0;
+}
+
+__global__ void k_lds128(float* out, int stride) {
+  __shared__ float4 buf[1024];
+  for (int i = threadIdx.x; i < 1024; i += blockDim.x) buf[i] = make_float4(i, i + 1, i + 2, i + 3);
+  __syncthreads();
+  float4 acc = make_float4(0, 0, 0, 0);
+  int idx[CH];
+#pragma unroll
+  for (int i = 0; i < CH; ++i) idx[i] = (threadIdx.x * stride + i * 37) & 1023;
+  unsigned long long t0 = clock64();
+  for (int it = 0; it < ITERS / 4; ++it) {
+#pragma unroll
+    for (int i = 0; i < CH; ++i) {
+      float4 v = buf[idx[i]];
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+      idx[i] = (idx[i] + (int)v.x) & 1023;  // dependent address chain
+    }
+  }
+  unsigned long long t1 = clock64();
+  if (acc.x + acc.y + acc.z + acc.w == 1234.5f) out[0] = acc.x;
+  if (threadIdx.x == 0) g_cycles[blockIdx.x] = t1 - t0;
+}
+
+template <typename F>
+static int run(const char* name, F launch, int blocks, int threads, double ops_per_thread, int sms,
+               int clk_khz) {
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0)); CK(cudaEventCreate(&e1));
+  launch();  // warm
+  CK(cudaDeviceSynchronize());
+  CK(cudaEventRecord(e0));
+  launch();
+  CK(cudaEventRecord(e1));
+  CK(cudaEventSynchronize(e1));
+  float ms = 0; CK(cudaEventElapsedTime(&ms, e0, e1));
+  unsigned long long cyc[4096];
+  CK(cudaMemcpyFromSymbol(cyc, g_cycles, sizeof(unsigned long long) * blocks));
+  double cmax = 0, csum = 0;
+  for (int i = 0; i < blocks; ++i) { cmax = cyc[i] > cmax ? cyc[i] : cmax; csum += cyc[i]; }
+  double total_ops = ops_per_thread * threads * (double)blocks;
+  double blocks_per_sm = (double)blocks / sms;
+  // per-SM per-clock from in-kernel cycle counts (all blocks co-resident: blocks <= sms*occ)
+  double per_sm_clk = ops_per_thread * threads * blocks_per_sm / (csum / blocks);
+  double eff_ghz = (csum / blocks) / (ms * 1e-3) / 1e9;
+  printf("{\"probe\":\"%s\",\"blocks\":%d,\"threads\":%d,\"ms\":%.4f,\"Gops_per_s\":%.1f,"
+         "\"ops_per_sm_per_clk\":%.2f,\"kernel_clock_ghz_est\":%.3f,\"sms\":%d,\"max_clk_mhz\":%.0f}\n",
+         name, blocks, threads, ms, total_ops / (ms * 1e-3) / 1e9, per_sm_clk, eff_ghz, sms,
+         clk_khz / 1e3);
+  return 0;
+}
+
+int main() {
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, 0));
+  int sms = prop.multiProcessorCount;
+  int clk_khz = 0;
+  CK(cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, 0));
+  printf("{\"device\":\"%s\",\"sms\":%d,\"cc\":\"%d.%d\",\"clock_khz\":%d,\"smem_per_sm\":%zu,\"regs_per_sm\":%d}\n",
+         prop.name, sms, prop.major, prop.minor, clk_khz, prop.sharedMemPerMultiprocessor,
+         prop.regsPerMultiprocessor);
+  float* out; CK(cudaMalloc(&out, 16));
+  const int T = 256, B = sms * 4;  // 32 warps/SM, all co-resident
+  if (run("ffma_3reg", [&] { k_ffma<<<B, T>>>(out, 1.0001f, 0.999f); }, B, T, (double)ITERS * CH, sms, clk_khz)) return 1;
+  if (run("ffma_imm", [&] { k_ffma_imm<<<B, T>>>(out, 1.0001f); }, B, T, (double)ITERS * CH, sms, clk_khz)) return 1;
+  // sincos: count MUFU ops (2 per step)
+  if (run("mufu_sin_cos", [&] { k_sincos<<<B, T>>>(out, 1.f); }, B, T, (double)(ITERS / 4) * CH * 2, sms, clk_khz)) return 1;
+  if (run("mufu_rsq", [&] { k_rsqrt<<<B, T>>>(out, 1.f); }, B, T, (double)(ITERS / 4) * CH, sms, clk_khz)) return 1;
+  // LDS.128: count 16-byte loads
+  if (run("lds128", [&] { k_lds128<<<B, T>>>(out, 1); }, B, T, (double)(ITERS / 4) * CH, sms, clk_khz)) return 1;
+  CK(cudaGetLastError());
+  return 0;
+}
