@@ -1,0 +1,350 @@
+#!/usr/bin/env python
+"""Benchmark of the TDBP hot path (BASELINE.json metric: giga pixel.ping.element backprojections/s).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl sasbp|reference] [--config 2]
+
+A step = one whole TDBP image formation (all §8(a) rows: reference geometry, delays,
+interpolation, phase ramp, accumulation, image write) over config 2 of BASELINE.json
+(2D stripmap, 1000 pings x 32 elements x 10240 samples, 4096 x 4096 pixels; synthetic,
+seeded inputs from synth/).  N = 1 times one GPU; under torchrun (N > 1) the image is
+sharded across ranks (image-shard, strong scaling; echoes broadcast once over NVLink).
+
+value  : dense terms (pixels x pings x elements; = N_u for this config) / device time of the
+         timed steps (CUDA events on the launching stream, max over ranks), inputs resident.
+e2e    : the same metric through the C ABI with HOST buffers (pinned echoes -> H2D ->
+         form -> D2H image), wall time per step, max over ranks.
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "giga pixel·ping·element backprojections/s"
+UNIT = "Gterm/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="sasbp", choices=["sasbp", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ roofline
+
+def roof_terms_per_s(E: int, sms: int, f_hz: float) -> float:
+    """FP32/SFU roofline of the canonical per-term instruction mix:
+    F = 20 + 6/E FP32-pipe ops, S = 3 + 1/E MUFU ops per term; 128 FP32 lanes and 16 MUFU per SM
+    per clock (B200, measured in profiles/ubench_r01.jsonl)."""
+    F = 20.0 + 6.0 / E
+    S = 3.0 + 1.0 / E
+    return sms * f_hz * min(128.0 / F, 16.0 / S)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 3 + i and r[3 + i] == "Active"})
+        pw = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows), "power_w_max": max(pw) if pw else None}
+
+
+# ------------------------------------------------------------------ CPU oracle baseline
+
+def cpu_oracle_rate(s, echoes, seconds: float, seed: int = 123):
+    """Time the fp64 oracle (as it stands) on a bounded random-pixel sample of the workload."""
+    import oracle
+    rng = np.random.default_rng(seed)
+    g = s.grid
+
+    def sample(n):
+        return np.stack([rng.integers(0, g["nx"], n), rng.integers(0, g["ny"], n), rng.integers(0, g["nz"], n)], 1)
+
+    probe = sample(64)
+    t = time.perf_counter()
+    oracle.tdbp_grid(echoes, s.tx, s.rx, s.t0, s.fc, s.fs, s.c, g, idx=probe)
+    dt = max(time.perf_counter() - t, 1e-6)
+    n = int(max(64, min(1 << 20, 64 * seconds / dt)))
+    idx = sample(n)
+    t = time.perf_counter()
+    oracle.tdbp_grid(echoes, s.tx, s.rx, s.t0, s.fc, s.fs, s.c, g, idx=idx)
+    dt = time.perf_counter() - t
+    terms = n * s.P * s.E
+    return {"value": terms / dt / 1e9, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": f"{n} seeded-random pixels of config {s.name} x all {s.P} pings x {s.E} elements "
+                      f"({terms:.3e} terms, {dt:.1f} s, fp64 C + OpenMP)"}
+
+
+def host_cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+# ------------------------------------------------------------------ arms
+
+def run_reference(args):
+    """Reference arm: the fp64 CPU oracle (this tier has no reference implementation)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import synth
+    s = synth.scenario(args.config)
+    echoes = s.echoes()
+    per_step = max(2.0, 60.0 / max(1, args.steps + args.warmup))
+    rates = []
+    last = None
+    for i in range(args.warmup + args.steps):
+        last = cpu_oracle_rate(s, echoes, per_step, seed=1000 + i)
+        if i >= args.warmup:
+            rates.append(last["value"])
+    v = float(np.mean(rates))
+    terms_per_step = s.dense_terms
+    out = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": 0, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": terms_per_step / (v * 1e9) * 1e3, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": f"BASELINE config {args.config}: {s.name} {s.grid['nx']}x{s.grid['ny']}x{s.grid['nz']} "
+                                  f"P={s.P} E={s.E} Ns={s.Ns}", "sampled": True},
+           "cpu_baseline": {"value": v, "unit": UNIT, "cores": last["cores"], "kind": "oracle",
+                            "sample": "per step: " + last["sample"], "cpu_model": host_cpu_model()},
+           "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+           "note": "reference arm = the fp64 C oracle on the host cores, timed on bounded random-pixel samples; "
+                   "ms_per_step is extrapolated to the full image"}
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+def run_sasbp(args):
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    import paper_2101_05888_b200 as pkg
+    from paper_2101_05888_b200 import distributed as pdist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    pkg.load_library()
+
+    s = synth.scenario(args.config)
+    g = s.grid
+    echoes_h = s.echoes() if (rank == 0 or world == 1) else None
+    P, E, Ns = s.P, s.E, s.Ns
+    dense = s.dense_terms
+
+    # device-resident inputs
+    echoes_d = torch.empty((P, E, Ns), dtype=torch.complex64, device=dev)
+    if echoes_h is not None:
+        echoes_d.copy_(torch.from_numpy(echoes_h))
+    if world > 1:
+        pdist.broadcast_echoes(echoes_d, dist)
+        torch.cuda.synchronize()
+
+    # this rank's band (image-shard); one plan per rank
+    bands = pdist.row_bands(pdist.band_axis_len(g), world, 32 if g["nz"] == 1 else 8)
+    lo, hi = bands[rank]
+    sg = pdist.sub_grid(g, lo, hi) if world > 1 else g
+    bp = pkg.Backprojector(s.fc, s.bandwidth, s.fs, s.c, sg)
+    bp.set_pings_device(echoes_d, s.tx, s.rx, s.t0)
+    img = torch.empty(bp.shape, dtype=torch.complex64, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        bp.form_device(img, stream=stream)
+    barrier()
+
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        barrier()
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        t_start.record(stream)
+        for i in range(args.steps):
+            evs[i][0].record(stream)
+            bp.form_device(img, stream=stream)
+            evs[i][1].record(stream)
+        t_end.record(stream)
+        barrier()
+    total_ms = t_start.elapsed_time(t_end)
+    per_launch = [a.elapsed_time(b) for a, b in evs]
+    tm = torch.tensor([total_ms, statistics.mean(per_launch)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+    total_ms, launch_ms = float(tm[0]), float(tm[1])
+    value = dense * args.steps / (total_ms * 1e-3) / 1e9
+
+    # dominant kernel = the TDBP launch: algorithmic terms per launch / its average duration
+    props = torch.cuda.get_device_properties(dev)
+    sms = props.multi_processor_count
+    peak = roof_terms_per_s(E, sms, 1.965e9) / 1e9
+    terms_per_launch = bp.shape[0] * bp.shape[1] * bp.shape[2] * P * E   # this rank's launch
+    achieved = terms_per_launch / (launch_ms * 1e-3) / 1e9            # per GPU, vs the per-GPU peak
+
+    # ---- end to end through the C ABI with host buffers (pinned echoes -> image on host)
+    e2e = None
+    if not args.no_e2e:
+        if world == 1:
+            pinned = torch.from_numpy(echoes_h).pin_memory()
+            host_img = torch.empty(bp.shape, dtype=torch.complex64).pin_memory()
+            bp_h = pkg.Backprojector(s.fc, s.bandwidth, s.fs, s.c, g)
+            bp_h.set_pings(pinned, s.tx, s.rx, s.t0)
+            bp_h.form(host_img)  # warm
+            ts = []
+            for _ in range(max(1, min(args.steps, 3))):
+                t0 = time.perf_counter()
+                bp_h.set_pings(pinned, s.tx, s.rx, s.t0)
+                bp_h.form(host_img)
+                ts.append(time.perf_counter() - t0)
+            bp_h.close()
+            e2e_s = statistics.mean(ts)
+            h2d = P * E * Ns * 8 + (P * 3 + P * E * 3 + P) * 8
+            d2h = g["nx"] * g["ny"] * g["nz"] * 8
+            e2e = {"value": dense / e2e_s / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                   "ms_per_step": e2e_s * 1e3, "api": "sas_bp_set_pings(pinned host) + sas_bp_form(pinned host)"}
+        else:
+            # rank 0: pinned host echoes -> H2D -> NCCL broadcast -> per-rank band -> gather -> D2H
+            pinned = torch.from_numpy(echoes_h).pin_memory() if rank == 0 else None
+            former = pdist.make_cuda_former(s.fc, s.bandwidth, s.fs, s.c)
+            ts = []
+            for it in range(max(1, min(args.steps, 3)) + 1):
+                barrier()
+                t0 = time.perf_counter()
+                if rank == 0:
+                    echoes_d.copy_(pinned, non_blocking=True)
+                pdist.broadcast_echoes(echoes_d, dist)
+                full = pdist.form_image_sharded(g, echoes_d, s.tx, s.rx, s.t0, former, dist, device=dev)
+                if rank == 0:
+                    full.cpu()
+                barrier()
+                dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+                dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+                if it > 0:
+                    ts.append(float(dt[0]))
+            e2e_s = statistics.mean(ts)
+            e2e = {"value": dense / e2e_s / 1e9, "unit": UNIT, "h2d_bytes_per_step": P * E * Ns * 8,
+                   "d2h_bytes_per_step": g["nx"] * g["ny"] * g["nz"] * 8, "ms_per_step": e2e_s * 1e3,
+                   "api": "pinned H2D on rank 0 + NCCL broadcast + sas_bp_form_device per band + all_gather + D2H"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_oracle_rate(s, echoes_h, args.cpu_seconds)
+        cpu["cpu_model"] = host_cpu_model()
+
+    if rank == 0:
+        traffic = None
+        prof = os.path.join(ROOT, "profiles", "ncu_tdbp_summary.json")
+        if os.path.exists(prof):
+            try:
+                with open(prof) as f:
+                    pj = json.load(f)
+                if pj.get("config") == args.config:
+                    traffic = pj.get("dram_bytes_per_launch")
+            except Exception:
+                traffic = None
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded synth/ forward model)",
+            "config": {"workload": f"BASELINE config {args.config}: {s.name} 2D stripmap {g['nx']}x{g['ny']}x{g['nz']} "
+                                   f"pixels, P={P} pings x E={E} elements x Ns={Ns} samples",
+                       "terms_per_step": dense, "parallelism": f"image-shard x{world}" if world > 1 else "single GPU",
+                       "l2": f"inputs larger than L2 ({P * E * Ns * 8 / 1e9:.2f} GB echoes)"},
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": UNIT, "frac": achieved / peak,
+                         "traffic": traffic,
+                         "peak_basis": f"{sms} SMs x 1965 MHz x min(128/F, 16/S), F=20+6/E, S=3+1/E, E={E}"},
+            "clocks": clk.summary(),
+            "gpu_launches": args.steps,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        if cpu:
+            out["gpu_over_cpu"] = value / cpu["value"]
+        print(json.dumps(out), flush=True)
+    bp.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_sasbp(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,144 @@
+/*
+ * sasbp.h -- C ABI of libsasbp.so: B200-native time-domain backprojection (TDBP) for
+ * synthetic aperture sonar, the data-parallel hot path of Gerg et al., "GPU Acceleration
+ * for Synthetic Aperture Sonar Image Reconstruction" (arXiv 2101.05888).
+ *
+ * Citation key: P:n = PAPER.md line n; S:n = SPEC.md line n; R1..R14 = readings in DESIGN.md.
+ *
+ * The operation (DESIGN.md §1 "Definition"): for every pixel / voxel centre
+ *   x = origin + ix*step_x + iy*step_y + iz*step_z                                   (R8)
+ * the complex image is
+ *   I(x) = sum_p sum_e  ehat_{p,e}((tau - t0_p) fs) * exp(+j 2 pi fc tau),
+ *   tau  = (|x - tx_p| + |x - rx_{p,e}|) / c                       (Eq. 1 delay)
+ * with ehat the linear interpolation of echoes[p][e][.] and echoes zero outside the
+ * recorded window (R1, R2), weight 1, no beam gate, no normalisation (R6, R7, R10).
+ * The inversion is the estimate of sigma(x) from e(t, x_RX) the paper poses.
+ *
+ * Conventions common to every call:
+ *   - complex64 = two float32 (re, im) interleaved, little endian;
+ *   - positions are fp64 NED metres; times in seconds; frequencies in Hz;
+ *   - echoes are complex baseband, range compressed, sampled at fs, sample n taken
+ *     t0_p + n/fs after ping p's transmit (R3, R4);
+ *   - all entry points return a sas_status; on failure sas_last_error() gives a
+ *     thread-local message.  No exception or abort crosses the ABI;
+ *   - a handle lives on the CUDA device that was current at sas_bp_create and is not
+ *     thread-safe; separate handles (e.g. one per device / rank) are independent;
+ *   - SAS_E_CUDA is sticky: the handle must be destroyed;
+ *   - NaN / Inf echoes are not scanned and propagate into the image.
+ */
+#ifndef SASBP_H
+#define SASBP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define SASBP_API __attribute__((visibility("default")))
+#else
+#define SASBP_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SAS_OK = 0,
+  SAS_E_INVALID = -1,      /* bad argument: see each call                                   */
+  SAS_E_STATE = -2,        /* call out of order (e.g. form before set_pings)                */
+  SAS_E_NOMEM = -3,        /* device or pinned-host allocation failed                       */
+  SAS_E_CUDA = -4,         /* CUDA runtime error (sticky for the handle)                    */
+  SAS_E_UNSUPPORTED = -5   /* no usable sm_100 device, or an unsupported option             */
+} sas_status;
+
+/* Imaging grid.  Pixel (ix,iy,iz) is centred at
+ * origin + ix*step_x + iy*step_y + iz*step_z.  Steps need not be axis aligned.
+ * nz = 1 gives a 2D image; nz > 1 a voxel grid ("3D via 2D layers"). */
+typedef struct {
+  double origin[3];
+  double step_x[3];
+  double step_y[3];
+  double step_z[3];
+  int32_t nx, ny, nz;
+} sas_grid;
+
+typedef struct sas_bp_s* sas_bp_t;
+
+/* Create a TDBP plan for `grid` on the current CUDA device and allocate its device image
+ * and workspace once (the paper's slab allocator idea).
+ *   fc        carrier frequency (> 0)        bandwidth  pulse bandwidth, 0 < bandwidth <= fs
+ *   fs        complex sample rate (> 0)      c          sound speed (> 0), one constant (R9)
+ * Errors: SAS_E_INVALID for non-finite / non-positive parameters, nx|ny|nz < 1, a zero or
+ * non-finite step vector, degenerate (linearly dependent) steps when the axis has > 1
+ * pixel, or more than 2^31 pixels; SAS_E_UNSUPPORTED when no sm_100 device is current;
+ * SAS_E_NOMEM.  *out is NULL on failure. */
+SASBP_API sas_status sas_bp_create(double fc, double bandwidth, double fs, double c, const sas_grid* grid,
+                         sas_bp_t* out);
+
+/* NULL-safe; frees every resource of the handle. */
+SASBP_API void sas_bp_destroy(sas_bp_t h);
+
+/* Copy a ping set to the device (host inputs; the caller may free them on return) and
+ * replace any previous set.
+ *   echoes  complex64 [P][E][Ns] host (pinned or pageable)
+ *   tx      fp64 [P][3]     transmitter position per ping (stationary during transmit)
+ *   rx      fp64 [P][E][3]  receiver phase centre per ping and element (stop-and-hop, R5)
+ *   t0      fp64 [P] time of sample 0 after transmit, or NULL for all zero (R4)
+ * Errors: SAS_E_INVALID for P|E|Ns < 1, NULL echoes/tx/rx, non-finite tx/rx/t0, or
+ * P*E*Ns overflow; SAS_E_NOMEM; SAS_E_CUDA. Synchronous w.r.t. the host buffers. */
+SASBP_API sas_status sas_bp_set_pings(sas_bp_t h, const float* echoes, int32_t P, int32_t E, int32_t Ns,
+                            const double* tx, const double* rx, const double* t0);
+
+/* As sas_bp_set_pings but `echoes_dev` is a DEVICE pointer (complex64 [P][E][Ns], 8-byte
+ * aligned) that the handle BORROWS until work queued on `cuda_stream` by later form calls
+ * completes; tx/rx/t0 are host arrays and are copied.  cuda_stream may be NULL (legacy
+ * default stream). */
+SASBP_API sas_status sas_bp_set_pings_device(sas_bp_t h, const void* echoes_dev, int32_t P, int32_t E,
+                                   int32_t Ns, const double* tx, const double* rx, const double* t0,
+                                   void* cuda_stream);
+
+/* Form the image and copy it to the host: image_out complex64 [nz][ny][nx] (ix fastest).
+ * Overwrites (never accumulates); may be called repeatedly.  Synchronous.
+ * Errors: SAS_E_STATE before any set_pings; SAS_E_INVALID for NULL; SAS_E_CUDA. */
+SASBP_API sas_status sas_bp_form(sas_bp_t h, float* image_out);
+
+/* Form the image into DEVICE memory image_dev (complex64 [nz][ny][nx], 8-byte aligned),
+ * asynchronously on cuda_stream (NULL = legacy default stream).
+ * flags: 0 = overwrite, SAS_FORM_ACCUMULATE = add to the existing contents of image_dev
+ * (ping-chunked / ping-sharded partial images: I(A u B) = I(A) + I(B)). */
+#define SAS_FORM_ACCUMULATE 1
+SASBP_API sas_status sas_bp_form_device(sas_bp_t h, void* image_dev, void* cuda_stream, int32_t flags);
+
+/* Algorithmic work counters of the current ping set (off the clock, for the metric):
+ *   dense  = nx*ny*nz*P*E  pixel.ping.element terms;
+ *   in_win = the terms whose interpolation support meets the record, u in (-1, Ns)
+ *            (SURVEY §8(d) N_u), counted on the device in fp32 (K3).  Either may be NULL. */
+SASBP_API sas_status sas_bp_count_terms(sas_bp_t h, uint64_t* dense, uint64_t* in_win);
+
+/* Bytes of device memory the handle owns (image + workspace + owned ping copy). */
+SASBP_API size_t sas_bp_workspace_bytes(sas_bp_t h);
+
+/* Matched-filter range compression (row a1; the paper presumes compressed data; R14):
+ *   out[ch][n] = sum_{m=0}^{Nr-1} raw[ch][n+m] * conj(replica[m]),  raw zero past Ns,
+ * ch = 0..P*E-1, n = 0..Ns-1.  Host buffers, complex64; runs on the current device.
+ * Errors: SAS_E_INVALID for P|E|Ns|Nr < 1 or NULL pointers; SAS_E_NOMEM; SAS_E_CUDA. */
+SASBP_API sas_status sas_rangecompress(const float* raw, int32_t P, int32_t E, int32_t Ns,
+                             const float* replica, int32_t Nr, float* out);
+
+/* Device-pointer variant of sas_rangecompress, asynchronous on cuda_stream.  raw_dev and
+ * out_dev must not overlap. */
+SASBP_API sas_status sas_rangecompress_device(const void* raw_dev, int32_t P, int32_t E, int32_t Ns,
+                                    const void* replica_dev, int32_t Nr, void* out_dev,
+                                    void* cuda_stream);
+
+/* Thread-local message describing the last failure on this thread ("" if none). */
+SASBP_API const char* sas_last_error(void);
+
+/* Library version string, e.g. "sasbp 0.1.0 sm_100a". */
+SASBP_API const char* sas_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SASBP_H */

@@ -1,0 +1,399 @@
+// sasbp.cu -- host side of libsasbp.so: the C ABI declared in include/sasbp.h.
+//
+// Owns: argument validation, the per-grid plan (tile shape, window capacity, precision
+// mode), the one-time device allocations (image + workspace, the paper's slab idea P:156),
+// ping uploads and the K2/K3 launches.  No torch types cross this boundary.
+#include "sasbp.h"
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "tdbp_kernel.cuh"
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+sas_status fail(sas_status st, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return st;
+}
+
+bool finite3(const double* v) { return std::isfinite(v[0]) && std::isfinite(v[1]) && std::isfinite(v[2]); }
+double norm3(const double* v) { return std::sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]); }
+
+enum Variant { V2D = 0, V2D_DZ = 1, V3D = 2 };
+
+}  // namespace
+
+struct sas_bp_s {
+  int device = -1;
+  double fc = 0, bandwidth = 0, fs = 0, c = 0;
+  sas_grid grid{};
+  // plan
+  Variant variant = V2D;
+  int TX = 32, TY = 32, TZ = 1;
+  int tiles_x = 0, tiles_y = 0, tiles_z = 0;
+  double d_max = 0;  // max |pixel - tile centre| (m)
+  double hw = 0;     // half window, samples
+  int W = 0;         // window slots per channel
+  bool exact_rx = false;
+  // device memory
+  float2* image = nullptr;
+  float2* echoes_owned = nullptr;
+  size_t echoes_cap = 0;
+  const float2* echoes = nullptr;
+  double* geo = nullptr;  // tx [P*3] | rx [P*E*3] | t0 [P]
+  size_t geo_cap = 0;
+  unsigned long long* counter = nullptr;
+  cudaStream_t stream = nullptr;
+  int P = 0, E = 0, Ns = 0;
+  bool has_pings = false;
+  bool broken = false;
+  size_t bytes = 0;
+};
+
+namespace {
+
+sas_status cuda_fail(sas_bp_t h, cudaError_t e, const char* what) {
+  if (h) h->broken = true;
+  return fail(SAS_E_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+#define CK_H(h, call)                                          \
+  do {                                                         \
+    cudaError_t e_ = (call);                                   \
+    if (e_ != cudaSuccess) return cuda_fail((h), e_, #call);   \
+  } while (0)
+
+size_t smem_bytes(int W) {
+  return sizeof(sasbp::ChanConst) * sasbp::kNB + (size_t)sasbp::kNB * W * sizeof(float4);
+}
+
+// Taylor-series truncation bound: the 4-term series of sqrt(1+eps)-1 leaves
+// |rem| <= r * (7/256) eps^5 / (1 - eps); with eps <= 2 d/r + (d/r)^2 the worst case is at
+// the smallest element-to-grid distance.  Require rem <= 1e-5 wavelength and eps <= 0.3.
+bool need_exact(double d_max, double r_min, double lambda) {
+  if (!(r_min > 0)) return true;
+  double eps = 2.0 * d_max / r_min + (d_max / r_min) * (d_max / r_min);
+  if (eps > 0.3) return true;
+  double rem = r_min * (7.0 / 256.0) * std::pow(eps, 5.0) / (1.0 - eps);
+  return rem > 1e-5 * lambda;
+}
+
+// distance from point p to the axis-aligned bounding box of the grid's pixel centres
+double dist_to_box(const double* p, const double lo[3], const double hi[3]) {
+  double s = 0;
+  for (int a = 0; a < 3; ++a) {
+    double d = 0;
+    if (p[a] < lo[a]) d = lo[a] - p[a];
+    else if (p[a] > hi[a]) d = p[a] - hi[a];
+    s += d * d;
+  }
+  return std::sqrt(s);
+}
+
+template <int KX, int KY, int KZ, int WY, int WZ, bool DZ>
+cudaError_t launch_variant(const sasbp::TdbpParams& prm, bool exact, bool count, cudaStream_t st) {
+  const size_t smem = smem_bytes(prm.W);
+  const unsigned blocks = (unsigned)prm.tiles_x * prm.tiles_y * prm.tiles_z;
+  auto go = [&](auto kern) -> cudaError_t {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    kern<<<blocks, sasbp::kThreads, smem, st>>>(prm);
+    return cudaGetLastError();
+  };
+  if (count) return exact ? go(sasbp::tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, true, true>)
+                          : go(sasbp::tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, false, true>);
+  return exact ? go(sasbp::tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, true, false>)
+               : go(sasbp::tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, false, false>);
+}
+
+cudaError_t launch_tdbp(sas_bp_t h, float2* image, unsigned long long* counter, int accumulate,
+                        bool count, cudaStream_t st) {
+  sasbp::TdbpParams prm{};
+  prm.echoes = h->echoes;
+  prm.tx = h->geo;
+  prm.rx = h->geo + 3 * (size_t)h->P;
+  prm.t0 = h->geo + 3 * (size_t)h->P + 3 * (size_t)h->P * h->E;
+  prm.image = image;
+  prm.counter = counter;
+  for (int a = 0; a < 3; ++a) {
+    prm.origin[a] = h->grid.origin[a];
+    prm.sx[a] = h->grid.step_x[a];
+    prm.sy[a] = h->grid.step_y[a];
+    prm.sz[a] = h->grid.step_z[a];
+  }
+  prm.fc = h->fc; prm.fs = h->fs; prm.c = h->c;
+  prm.hw = h->hw;
+  prm.P = h->P; prm.E = h->E; prm.Ns = h->Ns;
+  prm.nx = h->grid.nx; prm.ny = h->grid.ny; prm.nz = h->grid.nz;
+  prm.tiles_x = h->tiles_x; prm.tiles_y = h->tiles_y; prm.tiles_z = h->tiles_z;
+  prm.W = h->W;
+  prm.accumulate = accumulate;
+  switch (h->variant) {
+    case V2D: return launch_variant<4, 2, 1, 4, 1, false>(prm, h->exact_rx, count, st);
+    case V2D_DZ: return launch_variant<4, 2, 1, 4, 1, true>(prm, h->exact_rx, count, st);
+    default: return launch_variant<2, 2, 2, 1, 4, true>(prm, h->exact_rx, count, st);
+  }
+}
+
+sas_status validate_geo(int32_t P, int32_t E, int32_t Ns, const double* tx, const double* rx, const double* t0) {
+  if (P < 1 || E < 1 || Ns < 1) return fail(SAS_E_INVALID, "P, E, Ns must be >= 1 (got %d, %d, %d)", P, E, Ns);
+  if (!tx || !rx) return fail(SAS_E_INVALID, "tx and rx must not be NULL");
+  const long double tot = (long double)P * E * Ns;
+  if (tot > 9.0e15L || (long double)P * E > 2.0e9L) return fail(SAS_E_INVALID, "P*E*Ns too large");
+  for (int32_t p = 0; p < P; ++p) {
+    if (!finite3(tx + 3 * (size_t)p)) return fail(SAS_E_INVALID, "non-finite tx[%d]", p);
+    if (t0 && !std::isfinite(t0[p])) return fail(SAS_E_INVALID, "non-finite t0[%d]", p);
+  }
+  for (size_t i = 0; i < (size_t)P * E; ++i)
+    if (!finite3(rx + 3 * i)) return fail(SAS_E_INVALID, "non-finite rx[%zu]", i);
+  return SAS_OK;
+}
+
+// upload nav, decide the precision mode of the plan for this ping set
+sas_status upload_geo(sas_bp_t h, int32_t P, int32_t E, int32_t Ns, const double* tx, const double* rx,
+                      const double* t0, cudaStream_t st) {
+  const size_t n = 3 * (size_t)P + 3 * (size_t)P * E + (size_t)P;
+  if (n > h->geo_cap) {
+    if (h->geo) { cudaFree(h->geo); h->bytes -= h->geo_cap * sizeof(double); h->geo = nullptr; h->geo_cap = 0; }
+    cudaError_t e = cudaMalloc(&h->geo, n * sizeof(double));
+    if (e != cudaSuccess) { h->geo = nullptr; return fail(SAS_E_NOMEM, "cudaMalloc(nav): %s", cudaGetErrorString(e)); }
+    h->geo_cap = n;
+    h->bytes += n * sizeof(double);
+  }
+  std::vector<double> host(n);
+  memcpy(host.data(), tx, 3 * (size_t)P * sizeof(double));
+  memcpy(host.data() + 3 * (size_t)P, rx, 3 * (size_t)P * E * sizeof(double));
+  for (int32_t p = 0; p < P; ++p) host[3 * (size_t)P + 3 * (size_t)P * E + p] = t0 ? t0[p] : 0.0;
+  CK_H(h, cudaMemcpyAsync(h->geo, host.data(), n * sizeof(double), cudaMemcpyHostToDevice, st));
+  CK_H(h, cudaStreamSynchronize(st));  // host vector goes out of scope
+  // precision mode: smallest element-to-grid distance decides Taylor vs exact rx leg
+  const sas_grid& g = h->grid;
+  double lo[3], hi[3];
+  for (int a = 0; a < 3; ++a) {
+    double v0 = g.origin[a];
+    double ex = (g.nx - 1) * g.step_x[a], ey = (g.ny - 1) * g.step_y[a], ez = (g.nz - 1) * g.step_z[a];
+    lo[a] = v0 + std::fmin(ex, 0.0) + std::fmin(ey, 0.0) + std::fmin(ez, 0.0) - h->d_max;
+    hi[a] = v0 + std::fmax(ex, 0.0) + std::fmax(ey, 0.0) + std::fmax(ez, 0.0) + h->d_max;
+  }
+  double rmin = INFINITY;
+  for (size_t i = 0; i < (size_t)P * E; ++i) rmin = std::fmin(rmin, dist_to_box(rx + 3 * i, lo, hi));
+  h->exact_rx = need_exact(h->d_max, rmin, h->c / h->fc);
+  h->P = P; h->E = E; h->Ns = Ns;
+  return SAS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* sas_last_error(void) { return g_err; }
+
+// internal (not in sasbp.h): lets the other translation units report through sas_last_error
+__attribute__((visibility("hidden"))) void sasbp_set_error(const char* msg) {
+  snprintf(g_err, sizeof(g_err), "%s", msg ? msg : "");
+}
+
+const char* sas_version(void) { return "sasbp 0.1.0 sm_100a"; }
+
+sas_status sas_bp_create(double fc, double bandwidth, double fs, double c, const sas_grid* grid, sas_bp_t* out) {
+  g_err[0] = 0;
+  if (!out) return fail(SAS_E_INVALID, "out must not be NULL");
+  *out = nullptr;
+  if (!grid) return fail(SAS_E_INVALID, "grid must not be NULL");
+  if (!(std::isfinite(fc) && fc > 0)) return fail(SAS_E_INVALID, "fc must be finite and > 0");
+  if (!(std::isfinite(fs) && fs > 0)) return fail(SAS_E_INVALID, "fs must be finite and > 0");
+  if (!(std::isfinite(c) && c > 0)) return fail(SAS_E_INVALID, "c must be finite and > 0");
+  if (!(std::isfinite(bandwidth) && bandwidth > 0 && bandwidth <= fs))
+    return fail(SAS_E_INVALID, "bandwidth must satisfy 0 < bandwidth <= fs");
+  const sas_grid& g = *grid;
+  if (g.nx < 1 || g.ny < 1 || g.nz < 1) return fail(SAS_E_INVALID, "grid dims must be >= 1");
+  if ((long double)g.nx * g.ny * g.nz > 2147483647.0L) return fail(SAS_E_INVALID, "grid has more than 2^31 pixels");
+  if (!finite3(g.origin) || !finite3(g.step_x) || !finite3(g.step_y) || !finite3(g.step_z))
+    return fail(SAS_E_INVALID, "grid origin/steps must be finite");
+  const double nxs = norm3(g.step_x), nys = norm3(g.step_y), nzs = norm3(g.step_z);
+  if ((g.nx > 1 && !(nxs > 0)) || (g.ny > 1 && !(nys > 0)) || (g.nz > 1 && !(nzs > 0)))
+    return fail(SAS_E_INVALID, "zero step on an axis with more than one pixel");
+  // independence of the used step vectors
+  {
+    const double* v[3] = {g.step_x, g.step_y, g.step_z};
+    int used[3] = {g.nx > 1, g.ny > 1, g.nz > 1};
+    for (int a = 0; a < 3; ++a)
+      for (int b = a + 1; b < 3; ++b)
+        if (used[a] && used[b]) {
+          double cx = v[a][1] * v[b][2] - v[a][2] * v[b][1], cy = v[a][2] * v[b][0] - v[a][0] * v[b][2],
+                 cz = v[a][0] * v[b][1] - v[a][1] * v[b][0];
+          if (!(std::sqrt(cx * cx + cy * cy + cz * cz) > 1e-12 * norm3(v[a]) * norm3(v[b])))
+            return fail(SAS_E_INVALID, "grid step vectors are linearly dependent");
+        }
+  }
+  int dev = -1;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return fail(SAS_E_UNSUPPORTED, "no CUDA device: %s", cudaGetErrorString(e));
+  int major = 0;
+  e = cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  if (e != cudaSuccess) return fail(SAS_E_UNSUPPORTED, "cudaDeviceGetAttribute: %s", cudaGetErrorString(e));
+  if (major != 10) return fail(SAS_E_UNSUPPORTED, "libsasbp is built for sm_100a only (device cc major %d)", major);
+
+  sas_bp_t h = new (std::nothrow) sas_bp_s();
+  if (!h) return fail(SAS_E_NOMEM, "host allocation failed");
+  h->device = dev;
+  h->fc = fc; h->bandwidth = bandwidth; h->fs = fs; h->c = c;
+  h->grid = g;
+  const bool flat_z = (g.nz == 1) && g.step_x[2] == 0.0 && g.step_y[2] == 0.0;
+  if (g.nz == 1) { h->variant = flat_z ? V2D : V2D_DZ; h->TX = 32; h->TY = 32; h->TZ = 1; }
+  else { h->variant = V3D; h->TX = 16; h->TY = 8; h->TZ = 8; }
+  h->tiles_x = (g.nx + h->TX - 1) / h->TX;
+  h->tiles_y = (g.ny + h->TY - 1) / h->TY;
+  h->tiles_z = (g.nz + h->TZ - 1) / h->TZ;
+  // max |d| over the tile: a convex function of the offsets, maximal at a corner
+  {
+    double best = 0;
+    for (int sxn = -1; sxn <= 1; sxn += 2)
+      for (int syn = -1; syn <= 1; syn += 2)
+        for (int szn = -1; szn <= 1; szn += 2) {
+          double ax = sxn * 0.5 * (h->TX - 1), ay = syn * 0.5 * (h->TY - 1), az = szn * 0.5 * (h->TZ - 1);
+          double d[3];
+          for (int a = 0; a < 3; ++a) d[a] = ax * g.step_x[a] + ay * g.step_y[a] + az * g.step_z[a];
+          best = std::fmax(best, norm3(d));
+        }
+    h->d_max = best;
+  }
+  h->hw = 2.0 * h->d_max * fs / c;
+  h->W = (int)std::ceil(2.0 * h->hw + 4.0) + 2;
+  if (smem_bytes(h->W) > 200 * 1024) {
+    delete h;
+    return fail(SAS_E_UNSUPPORTED, "tile window of %d samples does not fit shared memory (pixel step too large for fs)", 0);
+  }
+  e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) { delete h; return fail(SAS_E_CUDA, "cudaStreamCreate: %s", cudaGetErrorString(e)); }
+  const size_t npx = (size_t)g.nx * g.ny * g.nz;
+  e = cudaMalloc(&h->image, npx * sizeof(float2));
+  if (e != cudaSuccess) { cudaStreamDestroy(h->stream); delete h; return fail(SAS_E_NOMEM, "cudaMalloc(image): %s", cudaGetErrorString(e)); }
+  e = cudaMalloc(&h->counter, sizeof(unsigned long long));
+  if (e != cudaSuccess) { cudaFree(h->image); cudaStreamDestroy(h->stream); delete h; return fail(SAS_E_NOMEM, "cudaMalloc(counter)"); }
+  h->bytes = npx * sizeof(float2) + sizeof(unsigned long long);
+  *out = h;
+  return SAS_OK;
+}
+
+void sas_bp_destroy(sas_bp_t h) {
+  if (!h) return;
+  int prev = -1;
+  cudaGetDevice(&prev);
+  cudaSetDevice(h->device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  cudaFree(h->image);
+  cudaFree(h->echoes_owned);
+  cudaFree(h->geo);
+  cudaFree(h->counter);
+  if (h->stream) cudaStreamDestroy(h->stream);
+  if (prev >= 0) cudaSetDevice(prev);
+  delete h;
+}
+
+sas_status sas_bp_set_pings(sas_bp_t h, const float* echoes, int32_t P, int32_t E, int32_t Ns, const double* tx,
+                            const double* rx, const double* t0) {
+  g_err[0] = 0;
+  if (!h) return fail(SAS_E_INVALID, "handle is NULL");
+  if (h->broken) return fail(SAS_E_CUDA, "handle is in a failed CUDA state; destroy it");
+  if (!echoes) return fail(SAS_E_INVALID, "echoes must not be NULL");
+  sas_status st = validate_geo(P, E, Ns, tx, rx, t0);
+  if (st != SAS_OK) return st;
+  CK_H(h, cudaSetDevice(h->device));
+  const size_t n = (size_t)P * E * Ns;
+  if (n > h->echoes_cap) {
+    if (h->echoes_owned) { cudaFree(h->echoes_owned); h->bytes -= h->echoes_cap * sizeof(float2); }
+    h->echoes_owned = nullptr; h->echoes_cap = 0;
+    cudaError_t e = cudaMalloc(&h->echoes_owned, n * sizeof(float2));
+    if (e != cudaSuccess) { h->echoes_owned = nullptr; h->has_pings = false; return fail(SAS_E_NOMEM, "cudaMalloc(echoes, %zu B): %s", n * sizeof(float2), cudaGetErrorString(e)); }
+    h->echoes_cap = n;
+    h->bytes += n * sizeof(float2);
+  }
+  CK_H(h, cudaMemcpyAsync(h->echoes_owned, echoes, n * sizeof(float2), cudaMemcpyHostToDevice, h->stream));
+  st = upload_geo(h, P, E, Ns, tx, rx, t0, h->stream);  // synchronises the stream
+  if (st != SAS_OK) { h->has_pings = false; return st; }
+  h->echoes = h->echoes_owned;
+  h->has_pings = true;
+  return SAS_OK;
+}
+
+sas_status sas_bp_set_pings_device(sas_bp_t h, const void* echoes_dev, int32_t P, int32_t E, int32_t Ns,
+                                   const double* tx, const double* rx, const double* t0, void* cuda_stream) {
+  g_err[0] = 0;
+  if (!h) return fail(SAS_E_INVALID, "handle is NULL");
+  if (h->broken) return fail(SAS_E_CUDA, "handle is in a failed CUDA state; destroy it");
+  if (!echoes_dev) return fail(SAS_E_INVALID, "echoes_dev must not be NULL");
+  if (((uintptr_t)echoes_dev) & 7) return fail(SAS_E_INVALID, "echoes_dev must be 8-byte aligned");
+  sas_status st = validate_geo(P, E, Ns, tx, rx, t0);
+  if (st != SAS_OK) return st;
+  CK_H(h, cudaSetDevice(h->device));
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  st = upload_geo(h, P, E, Ns, tx, rx, t0, s);
+  if (st != SAS_OK) { h->has_pings = false; return st; }
+  h->echoes = (const float2*)echoes_dev;
+  h->has_pings = true;
+  return SAS_OK;
+}
+
+sas_status sas_bp_form_device(sas_bp_t h, void* image_dev, void* cuda_stream, int32_t flags) {
+  g_err[0] = 0;
+  if (!h) return fail(SAS_E_INVALID, "handle is NULL");
+  if (h->broken) return fail(SAS_E_CUDA, "handle is in a failed CUDA state; destroy it");
+  if (!image_dev) return fail(SAS_E_INVALID, "image_dev must not be NULL");
+  if (((uintptr_t)image_dev) & 7) return fail(SAS_E_INVALID, "image_dev must be 8-byte aligned");
+  if (flags & ~SAS_FORM_ACCUMULATE) return fail(SAS_E_INVALID, "unknown flags 0x%x", flags);
+  if (!h->has_pings) return fail(SAS_E_STATE, "sas_bp_form before sas_bp_set_pings");
+  CK_H(h, cudaSetDevice(h->device));
+  CK_H(h, launch_tdbp(h, (float2*)image_dev, h->counter, (flags & SAS_FORM_ACCUMULATE) ? 1 : 0, false,
+                      (cudaStream_t)cuda_stream));
+  return SAS_OK;
+}
+
+sas_status sas_bp_form(sas_bp_t h, float* image_out) {
+  g_err[0] = 0;
+  if (!h) return fail(SAS_E_INVALID, "handle is NULL");
+  if (h->broken) return fail(SAS_E_CUDA, "handle is in a failed CUDA state; destroy it");
+  if (!image_out) return fail(SAS_E_INVALID, "image_out must not be NULL");
+  if (!h->has_pings) return fail(SAS_E_STATE, "sas_bp_form before sas_bp_set_pings");
+  CK_H(h, cudaSetDevice(h->device));
+  CK_H(h, launch_tdbp(h, h->image, h->counter, 0, false, h->stream));
+  const size_t npx = (size_t)h->grid.nx * h->grid.ny * h->grid.nz;
+  CK_H(h, cudaMemcpyAsync(image_out, h->image, npx * sizeof(float2), cudaMemcpyDeviceToHost, h->stream));
+  CK_H(h, cudaStreamSynchronize(h->stream));
+  return SAS_OK;
+}
+
+sas_status sas_bp_count_terms(sas_bp_t h, uint64_t* dense, uint64_t* in_win) {
+  g_err[0] = 0;
+  if (!h) return fail(SAS_E_INVALID, "handle is NULL");
+  if (h->broken) return fail(SAS_E_CUDA, "handle is in a failed CUDA state; destroy it");
+  if (!h->has_pings) return fail(SAS_E_STATE, "sas_bp_count_terms before sas_bp_set_pings");
+  const uint64_t npx = (uint64_t)h->grid.nx * h->grid.ny * h->grid.nz;
+  if (dense) *dense = npx * (uint64_t)h->P * (uint64_t)h->E;
+  if (in_win) {
+    CK_H(h, cudaSetDevice(h->device));
+    CK_H(h, cudaMemsetAsync(h->counter, 0, sizeof(unsigned long long), h->stream));
+    CK_H(h, launch_tdbp(h, h->image, h->counter, 0, true, h->stream));
+    unsigned long long v = 0;
+    CK_H(h, cudaMemcpyAsync(&v, h->counter, sizeof(v), cudaMemcpyDeviceToHost, h->stream));
+    CK_H(h, cudaStreamSynchronize(h->stream));
+    *in_win = v;
+  }
+  return SAS_OK;
+}
+
+size_t sas_bp_workspace_bytes(sas_bp_t h) { return h ? h->bytes : 0; }
+
+}  // extern "C"

@@ -1,0 +1,247 @@
+"""Thin ctypes binding of libsasbp.so (include/sasbp.h) -- argument marshalling only.
+
+Every step of the hot path runs in the library's CUDA kernels; this module converts numpy
+arrays / torch tensors to pointers and status codes to exceptions.  There is no CPU
+fallback: if the library is missing or cannot find an sm_100 device, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libsasbp.so")
+
+SAS_OK, SAS_E_INVALID, SAS_E_STATE, SAS_E_NOMEM, SAS_E_CUDA, SAS_E_UNSUPPORTED = 0, -1, -2, -3, -4, -5
+SAS_FORM_ACCUMULATE = 1
+_NAMES = {0: "SAS_OK", -1: "SAS_E_INVALID", -2: "SAS_E_STATE", -3: "SAS_E_NOMEM", -4: "SAS_E_CUDA",
+          -5: "SAS_E_UNSUPPORTED"}
+
+EXPORTS = ("sas_bp_create", "sas_bp_destroy", "sas_bp_set_pings", "sas_bp_set_pings_device", "sas_bp_form",
+           "sas_bp_form_device", "sas_bp_count_terms", "sas_bp_workspace_bytes", "sas_rangecompress",
+           "sas_rangecompress_device", "sas_last_error", "sas_version")
+
+
+class SasError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+class sas_grid(ctypes.Structure):
+    _fields_ = [("origin", ctypes.c_double * 3), ("step_x", ctypes.c_double * 3),
+                ("step_y", ctypes.c_double * 3), ("step_z", ctypes.c_double * 3),
+                ("nx", ctypes.c_int32), ("ny", ctypes.c_int32), ("nz", ctypes.c_int32)]
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libsasbp.so (raises OSError loudly if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise OSError(f"libsasbp.so not built at {path}; run __graft_entry__.build()")
+    lib = ctypes.CDLL(path)
+    vp, f32p, f64p = ctypes.c_void_p, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_double)
+    i32 = ctypes.c_int32
+    sig = {
+        "sas_bp_create": ([ctypes.c_double] * 4 + [ctypes.POINTER(sas_grid), ctypes.POINTER(vp)], ctypes.c_int),
+        "sas_bp_destroy": ([vp], None),
+        "sas_bp_set_pings": ([vp, f32p, i32, i32, i32, f64p, f64p, f64p], ctypes.c_int),
+        "sas_bp_set_pings_device": ([vp, vp, i32, i32, i32, f64p, f64p, f64p, vp], ctypes.c_int),
+        "sas_bp_form": ([vp, f32p], ctypes.c_int),
+        "sas_bp_form_device": ([vp, vp, vp, i32], ctypes.c_int),
+        "sas_bp_count_terms": ([vp, ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64)], ctypes.c_int),
+        "sas_bp_workspace_bytes": ([vp], ctypes.c_size_t),
+        "sas_rangecompress": ([f32p, i32, i32, i32, f32p, i32, f32p], ctypes.c_int),
+        "sas_rangecompress_device": ([vp, i32, i32, i32, vp, i32, vp, vp], ctypes.c_int),
+        "sas_last_error": ([], ctypes.c_char_p),
+        "sas_version": ([], ctypes.c_char_p),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = lib
+    return lib
+
+
+def _check(st: int):
+    if st != SAS_OK:
+        raise SasError(st, _lib.sas_last_error().decode())
+
+
+def version() -> str:
+    return load_library().sas_version().decode()
+
+
+def make_grid(grid) -> sas_grid:
+    g = sas_grid()
+    for k in ("origin", "step_x", "step_y", "step_z"):
+        v = np.asarray(grid[k], dtype=np.float64).reshape(3)
+        getattr(g, k)[:] = [float(x) for x in v]
+    g.nx, g.ny, g.nz = int(grid["nx"]), int(grid["ny"]), int(grid["nz"])
+    return g
+
+
+def _f64(a, shape):
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    if a.size != int(np.prod(shape)):
+        raise ValueError(f"expected {shape} float64, got {a.shape}")
+    return a
+
+
+def _ptr(a, ct):
+    return None if a is None else a.ctypes.data_as(ctypes.POINTER(ct))
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        try:
+            import torch
+            if torch.cuda.is_available():
+                return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+        except ImportError:
+            pass
+        return None
+    if isinstance(stream, int):
+        return ctypes.c_void_p(stream)
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _dev_ptr(t, nbytes_min: int):
+    """Device pointer of a torch CUDA tensor (complex64 / float32), contiguity checked."""
+    if not getattr(t, "is_cuda", False):
+        raise ValueError("expected a CUDA tensor")
+    if not t.is_contiguous():
+        raise ValueError("expected a contiguous tensor")
+    if t.numel() * t.element_size() < nbytes_min:
+        raise ValueError("tensor too small")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+class Backprojector:
+    """One TDBP plan on the current CUDA device (sas_bp_create ... sas_bp_destroy)."""
+
+    def __init__(self, fc: float, bandwidth: float, fs: float, c: float, grid):
+        lib = load_library()
+        self._grid = make_grid(grid)
+        self.shape = (self._grid.nz, self._grid.ny, self._grid.nx)
+        h = ctypes.c_void_p()
+        _check(lib.sas_bp_create(fc, bandwidth, fs, c, ctypes.byref(self._grid), ctypes.byref(h)))
+        self._h = h
+        self.P = self.E = self.Ns = 0
+        self._keep = None
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.sas_bp_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def _geo(self, P, E, tx, rx, t0):
+        tx = _f64(tx, (P, 3))
+        rx = _f64(rx, (P, E, 3))
+        t0 = None if t0 is None else _f64(t0, (P,))
+        return tx, rx, t0
+
+    def set_pings(self, echoes, tx, rx, t0=None):
+        """Host echoes complex64 [P][E][Ns] (numpy or CPU torch tensor, pinned or not); copied."""
+        if hasattr(echoes, "numpy") and not hasattr(echoes, "ctypes"):
+            if echoes.is_cuda:
+                raise ValueError("set_pings takes host echoes; use set_pings_device for CUDA tensors")
+            keep = echoes.contiguous()
+            P, E, Ns = keep.shape
+            ptr = ctypes.cast(ctypes.c_void_p(keep.data_ptr()), ctypes.POINTER(ctypes.c_float))
+        else:
+            echoes = np.ascontiguousarray(echoes, dtype=np.complex64)
+            P, E, Ns = echoes.shape
+            ptr = echoes.view(np.float32).ctypes.data_as(ctypes.POINTER(ctypes.c_float))
+            keep = echoes
+        tx, rx, t0 = self._geo(P, E, tx, rx, t0)
+        _check(_lib.sas_bp_set_pings(self._h, ptr, P, E, Ns, _ptr(tx, ctypes.c_double),
+                                     _ptr(rx, ctypes.c_double), _ptr(t0, ctypes.c_double)))
+        del keep
+        self.P, self.E, self.Ns = P, E, Ns
+
+    def set_pings_device(self, echoes, tx, rx, t0=None, stream=None):
+        """Borrow a CUDA complex64 tensor [P][E][Ns] (kept alive by this object)."""
+        P, E, Ns = echoes.shape
+        tx, rx, t0 = self._geo(P, E, tx, rx, t0)
+        _check(_lib.sas_bp_set_pings_device(self._h, _dev_ptr(echoes, P * E * Ns * 8), P, E, Ns,
+                                            _ptr(tx, ctypes.c_double), _ptr(rx, ctypes.c_double),
+                                            _ptr(t0, ctypes.c_double), _stream_ptr(stream)))
+        self._keep = echoes
+        self.P, self.E, self.Ns = P, E, Ns
+
+    def form(self, out: Optional[np.ndarray] = None) -> np.ndarray:
+        """Form into host memory; returns complex64 [nz][ny][nx]."""
+        if out is None:
+            out = np.empty(self.shape, dtype=np.complex64)
+        if hasattr(out, "data_ptr") and not hasattr(out, "ctypes"):
+            ptr = ctypes.cast(ctypes.c_void_p(out.data_ptr()), ctypes.POINTER(ctypes.c_float))
+        else:
+            if out.dtype != np.complex64 or not out.flags.c_contiguous or out.shape != self.shape:
+                raise ValueError("out must be C-contiguous complex64 of the grid shape")
+            ptr = out.view(np.float32).ctypes.data_as(ctypes.POINTER(ctypes.c_float))
+        _check(_lib.sas_bp_form(self._h, ptr))
+        return out
+
+    def form_device(self, image, stream=None, accumulate: bool = False):
+        """Form into a CUDA complex64 tensor of the grid shape, asynchronously on `stream`."""
+        n = self.shape[0] * self.shape[1] * self.shape[2]
+        _check(_lib.sas_bp_form_device(self._h, _dev_ptr(image, n * 8), _stream_ptr(stream),
+                                       SAS_FORM_ACCUMULATE if accumulate else 0))
+        return image
+
+    def count_terms(self):
+        """(dense, in_window) term counts of the current ping set (K3; in_window on device)."""
+        d, w = ctypes.c_uint64(), ctypes.c_uint64()
+        _check(_lib.sas_bp_count_terms(self._h, ctypes.byref(d), ctypes.byref(w)))
+        return int(d.value), int(w.value)
+
+    @property
+    def workspace_bytes(self) -> int:
+        return int(_lib.sas_bp_workspace_bytes(self._h))
+
+
+def rangecompress(raw, replica) -> np.ndarray:
+    """Host matched filter: out[..., n] = sum_m raw[..., n+m] conj(replica[m]) (K1 on the GPU)."""
+    lib = load_library()
+    raw = np.ascontiguousarray(raw, dtype=np.complex64)
+    rep = np.ascontiguousarray(replica, dtype=np.complex64).ravel()
+    shp = raw.shape
+    Ns = shp[-1]
+    nch = int(np.prod(shp[:-1])) if len(shp) > 1 else 1
+    out = np.empty_like(raw)
+    f = lambda a: a.view(np.float32).ctypes.data_as(ctypes.POINTER(ctypes.c_float))
+    _check(lib.sas_rangecompress(f(raw), nch, 1, Ns, f(rep), rep.size, f(out)))
+    return out
+
+
+def rangecompress_device(raw, replica, out, stream=None):
+    """CUDA-tensor matched filter (complex64 [..., Ns] -> out of the same shape)."""
+    lib = load_library()
+    Ns = raw.shape[-1]
+    nch = raw.numel() // Ns
+    _check(lib.sas_rangecompress_device(_dev_ptr(raw, raw.numel() * 8), nch, 1, Ns,
+                                        _dev_ptr(replica, replica.numel() * 8), replica.numel(),
+                                        _dev_ptr(out, raw.numel() * 8), _stream_ptr(stream)))
+    return out

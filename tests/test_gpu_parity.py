@@ -1,0 +1,289 @@
+"""GPU-vs-oracle parity of the TDBP path through the C ABI (-m gpu).
+
+Bar (north star): on the same generated inputs,
+  max |I_gpu - I_oracle| <= 1e-3 * max |I_oracle| over the compared pixels, and
+  |wrap(arg I_gpu - arg I_oracle)| <= 1e-2 rad at every scatterer's oracle peak pixel.
+Compared pixels: the full image for small cases; at full BASELINE sizes (in the launch
+configuration bench.py times) 4096 seeded-random pixels plus a window around every target.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+TOL_MAG = 1e-3
+TOL_PHASE = 1e-2
+
+
+@pytest.fixture(scope="module")
+def bpmod(require_gpu):
+    import torch
+    torch.cuda.set_device(0)
+    from paper_2101_05888_b200 import _build
+    _build.build()
+    import paper_2101_05888_b200 as pkg
+    return pkg
+
+
+def _form(pkg, s, echoes, grid=None, tx=None, rx=None, t0="same"):
+    g = s.grid if grid is None else grid
+    with pkg.Backprojector(s.fc, s.bandwidth, s.fs, s.c, g) as bp:
+        bp.set_pings(echoes, s.tx if tx is None else tx, s.rx if rx is None else rx,
+                     s.t0 if isinstance(t0, str) else t0)
+        return bp.form()
+
+
+def _check(got, ref, peaks_got=None, peaks_ref=None, label=""):
+    scale = np.max(np.abs(ref))
+    assert scale > 0, f"{label}: oracle image is all zero -- the case tests nothing"
+    err = np.max(np.abs(got - ref))
+    assert err <= TOL_MAG * scale, f"{label}: max|err| = {err:.3e} > {TOL_MAG} * {scale:.3e}"
+    if peaks_ref is not None:
+        dph = np.angle(peaks_got * np.conj(peaks_ref))
+        assert np.max(np.abs(dph)) <= TOL_PHASE, f"{label}: peak phase err {np.max(np.abs(dph)):.3e} rad"
+    return err / scale
+
+
+def _peak_pixels(s, ref_fn, win=3):
+    """Oracle peak pixel near every target (brute force over a small window)."""
+    out = []
+    g = s.grid
+    for t in s.target_pixels:
+        rz = range(-win, win + 1) if g["nz"] > 1 else [0]
+        cand = np.array([(t[0] + dx, t[1] + dy, t[2] + dz) for dz in rz for dy in range(-win, win + 1)
+                         for dx in range(-win, win + 1)])
+        keep = ((cand >= 0) & (cand < np.array([g["nx"], g["ny"], g["nz"]]))).all(axis=1)
+        cand = cand[keep]
+        v = ref_fn(cand)
+        out.append(cand[np.argmax(np.abs(v))])
+    return np.array(out, dtype=np.int64)
+
+
+def _at(img, idx):
+    return img[idx[:, 2], idx[:, 1], idx[:, 0]]
+
+
+# ------------------------------------------------------------------ full images, small cases
+
+@pytest.mark.parametrize("cid", [1, 2, 3, 4, 5])
+def test_parity_full_image(bpmod, cid):
+    s = synth.scenario(cid, reduced=(cid != 1))
+    e = s.echoes()
+    got = _form(bpmod, s, e)
+    ref = oracle.tdbp_grid(e, s.tx, s.rx, s.t0, s.fc, s.fs, s.c, s.grid)
+    pk = s.target_pixels
+    rel = _check(got, ref, _at(got, pk), _at(ref, pk), label=s.name)
+    assert rel < 1e-3
+
+
+def test_cfg1_focus_on_gpu(bpmod):
+    """The GPU image focuses the config-1 target at its true pixel with phase ~ 0."""
+    s = synth.scenario(1)
+    img = _form(bpmod, s, s.echoes())[0]
+    iy, ix = np.unravel_index(np.argmax(np.abs(img)), img.shape)
+    assert (ix, iy) == tuple(s.target_pixels[0][:2])
+    assert abs(np.angle(img[iy, ix])) <= TOL_PHASE
+
+
+# ------------------------------------------------------------------ edge cases
+
+def _tiny(P=2, E=3, Ns=64, n=(5, 4, 1), seed=0, **kw):
+    r = synth.random_case(seed, P=P, E=E, Ns=Ns, n=n, **kw)
+    s = synth.Scenario(name="tiny", fc=r["fc"], bandwidth=r["fs"] / 4, fs=r["fs"], c=r["c"], tx=r["tx"],
+                       rx=r["rx"], t0=r["t0"], Ns=Ns, grid=r["grid"], targets=np.zeros((0, 3)),
+                       target_pixels=np.zeros((0, 3), dtype=np.int64), scat=np.zeros((0, 3)),
+                       sigma=np.zeros(0, dtype=np.complex128), sin_half_beam=0.0)
+    return s, r["echoes"]
+
+
+@pytest.mark.parametrize("n", [(1, 1, 1), (33, 1, 1), (1, 33, 1), (31, 33, 1), (65, 40, 1), (17, 9, 9),
+                               (3, 3, 17)])
+def test_parity_ragged_grids(bpmod, n):
+    s, e = _tiny(n=n, Ns=256, seed=sum(n))
+    got = _form(bpmod, s, e)
+    ref = oracle.tdbp_grid(e, s.tx, s.rx, s.t0, s.fc, s.fs, s.c, s.grid)
+    _check(got, ref, label=f"grid {n}")
+
+
+@pytest.mark.parametrize("P,E,Ns", [(1, 1, 1), (1, 1, 256), (1, 37, 256), (33, 1, 256), (7, 5, 300)])
+def test_parity_degenerate_sizes(bpmod, P, E, Ns):
+    """Single ping / element / sample, channel counts that are not multiples of the batch."""
+    s, e = _tiny(P=P, E=E, Ns=Ns, n=(9, 7, 3), seed=P * 100 + E)
+    got = _form(bpmod, s, e)
+    ref = oracle.tdbp_grid(e, s.tx, s.rx, s.t0, s.fc, s.fs, s.c, s.grid)
+    if np.max(np.abs(ref)) == 0:
+        assert np.max(np.abs(got)) == 0
+    else:
+        _check(got, ref, label=f"P{P} E{E} Ns{Ns}")
+
+
+def test_window_edges_zero_extension(bpmod):
+    """Delays straddling both ends of the record: zero extension (R2) on the GPU too."""
+    s, e = _tiny(P=4, E=4, Ns=90, n=(40, 30, 1), seed=3)
+    # shift t0 so the grid's delays run off both ends of the 90-sample record
+    for shift in (-70, -20, 30, 60):
+        t0 = s.t0 + shift / s.fs
+        got = _form(bpmod, s, e, t0=t0)
+        ref = oracle.tdbp_grid(e, s.tx, s.rx, t0, s.fc, s.fs, s.c, s.grid)
+        if np.max(np.abs(ref)) > 0:
+            _check(got, ref, label=f"shift {shift}")
+
+
+def test_t0_none_means_zero(bpmod):
+    s, e = _tiny(P=3, E=2, Ns=512, seed=4)
+    s.t0 = np.zeros(s.P)
+    got = _form(bpmod, s, e, t0=None)
+    ref = oracle.tdbp_grid(e, s.tx, s.rx, None, s.fc, s.fs, s.c, s.grid)
+    _check(got, ref, label="t0=None")
+
+
+def test_near_field_exact_leg(bpmod):
+    """Elements within a few tile sizes of the grid select the exact (non-series) receive leg."""
+    s = synth.scenario(4, reduced=True)
+    e = s.echoes()
+    # move the array to 20 cm above the grid top
+    dz = 1.8
+    tx, rx = s.tx + [0, 0, dz], s.rx + [0, 0, dz]
+    t0 = s.t0 - 2 * dz / s.c   # keep the delays inside the record
+    with bpmod.Backprojector(s.fc, s.bandwidth, s.fs, s.c, s.grid) as bp:
+        bp.set_pings(e, tx, rx, t0)
+        got = bp.form()
+    ref = oracle.tdbp_grid(e, tx, rx, t0, s.fc, s.fs, s.c, s.grid)
+    _check(got, ref, label="near field")
+
+
+def test_rotated_grid(bpmod):
+    """Non-axis-aligned steps (a tilted 2D image plane) use the dz-capable 2D kernel."""
+    s = synth.scenario(2, reduced=True)
+    e = s.echoes()
+    th = 0.3
+    g = dict(s.grid)
+    g["step_x"] = np.array([0.01 * np.cos(th), 0.0, 0.01 * np.sin(th)])
+    g["step_y"] = np.array([0.0, 0.01, 0.0])
+    got = _form(bpmod, s, e, grid=g)
+    ref = oracle.tdbp_grid(e, s.tx, s.rx, s.t0, s.fc, s.fs, s.c, g)
+    _check(got, ref, label="rotated grid")
+
+
+# ------------------------------------------------------------------ invariants on the GPU path
+
+def test_translation_precision(bpmod):
+    """Range-relative fp32 holds under a (1e4, -3e3, 0) m coordinate offset."""
+    s = synth.scenario(2, reduced=True)
+    e = s.echoes()
+    off = np.array([1e4, -3e3, 0.0])
+    g = dict(s.grid)
+    g["origin"] = s.grid["origin"] + off
+    got = _form(bpmod, s, e, grid=g, tx=s.tx + off, rx=s.rx + off)
+    ref = oracle.tdbp_grid(e, s.tx, s.rx, s.t0, s.fc, s.fs, s.c, s.grid)
+    pk = s.target_pixels
+    _check(got, ref, _at(got, pk), _at(ref, pk), label="offset 1e4 m")
+
+
+def test_determinism_bitwise(bpmod):
+    s = synth.scenario(2, reduced=True)
+    e = s.echoes()
+    with bpmod.Backprojector(s.fc, s.bandwidth, s.fs, s.c, s.grid) as bp:
+        bp.set_pings(e, s.tx, s.rx, s.t0)
+        a = bp.form().copy()
+        b = bp.form().copy()
+    assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+
+
+def test_ping_chunk_accumulate(bpmod):
+    """I(A u B) = I(A) + I(B) through SAS_FORM_ACCUMULATE on a device image."""
+    import torch
+    s = synth.scenario(2, reduced=True)
+    e = s.echoes()
+    full = _form(bpmod, s, e)
+    img = torch.zeros(s.grid["nz"], s.grid["ny"], s.grid["nx"], dtype=torch.complex64, device="cuda")
+    cuts = [0, 13, 27, s.P]
+    with bpmod.Backprojector(s.fc, s.bandwidth, s.fs, s.c, s.grid) as bp:
+        for i in range(len(cuts) - 1):
+            a, b = cuts[i], cuts[i + 1]
+            ed = torch.from_numpy(np.ascontiguousarray(e[a:b])).cuda()
+            bp.set_pings_device(ed, s.tx[a:b], s.rx[a:b], s.t0[a:b])
+            bp.form_device(img, accumulate=(i > 0))
+            torch.cuda.synchronize()
+    got = img.cpu().numpy()
+    assert np.max(np.abs(got - full)) <= 1e-5 * np.max(np.abs(full))
+
+
+def test_linearity_gpu(bpmod):
+    s = synth.scenario(2, reduced=True)
+    e1 = s.echoes()
+    rng = np.random.default_rng(0)
+    e2 = ((rng.normal(size=e1.shape) + 1j * rng.normal(size=e1.shape)) * 1e-4).astype(np.complex64)
+    a = np.float32(-0.5)
+    lhs = _form(bpmod, s, (a * e1 + e2).astype(np.complex64))
+    rhs = a * _form(bpmod, s, e1) + _form(bpmod, s, e2)
+    assert np.max(np.abs(lhs - rhs)) <= 1e-4 * np.max(np.abs(lhs))
+
+
+# ------------------------------------------------------------------ API semantics on device
+
+def test_form_before_set_pings_is_state_error(bpmod):
+    s = synth.scenario(1)
+    with bpmod.Backprojector(s.fc, s.bandwidth, s.fs, s.c, s.grid) as bp:
+        with pytest.raises(bpmod.SasError) as ei:
+            bp.form()
+        assert ei.value.status == -2
+
+
+def test_set_pings_device_matches_host(bpmod):
+    import torch
+    s = synth.scenario(1)
+    e = s.echoes()
+    host = _form(bpmod, s, e)
+    with bpmod.Backprojector(s.fc, s.bandwidth, s.fs, s.c, s.grid) as bp:
+        bp.set_pings_device(torch.from_numpy(e).cuda(), s.tx, s.rx, s.t0)
+        img = torch.empty(bp.shape, dtype=torch.complex64, device="cuda")
+        bp.form_device(img)
+        torch.cuda.synchronize()
+    assert np.array_equal(img.cpu().numpy(), host)
+
+
+def test_count_terms_matches_oracle(bpmod):
+    """K3 in-window count vs the fp64 oracle count (agree to 1e-4)."""
+    s, e = _tiny(P=5, E=4, Ns=90, n=(40, 30, 1), seed=7)
+    t0 = s.t0 + 20 / s.fs
+    with bpmod.Backprojector(s.fc, s.bandwidth, s.fs, s.c, s.grid) as bp:
+        bp.set_pings(e, s.tx, s.rx, t0)
+        dense, inwin = bp.count_terms()
+    _, cnt = oracle.tdbp_grid(e, s.tx, s.rx, t0, s.fc, s.fs, s.c, s.grid, with_count=True)
+    assert dense == s.n_pixels * s.P * s.E
+    assert abs(inwin - int(cnt.sum())) <= max(1, 1e-4 * cnt.sum())
+    assert 0 < inwin < dense
+
+
+def test_rangecompress_gpu_vs_oracle(bpmod):
+    rng = np.random.default_rng(1)
+    fs, B, T = 120e3, 30e3, 5e-3
+    n = int(round(T * fs))
+    t = np.arange(n) / fs - T / 2
+    rep = np.exp(1j * np.pi * (B / T) * t ** 2).astype(np.complex64)
+    rep /= np.float32(np.sqrt(np.sum(np.abs(rep) ** 2)))
+    raw = ((rng.normal(size=(3, 2, 3000)) + 1j * rng.normal(size=(3, 2, 3000))) / np.sqrt(2)).astype(np.complex64)
+    got = bpmod.rangecompress(raw, rep)
+    ref = oracle.rangecompress(raw, rep)
+    assert np.max(np.abs(got - ref)) <= 1e-5 * np.max(np.abs(ref))
+
+
+# ------------------------------------------------------------------ full BASELINE sizes (sampled)
+
+@pytest.mark.parametrize("cid", [2, 4])
+def test_parity_full_size_sampled(bpmod, cid):
+    """At the BASELINE configs' full sizes, in bench.py's launch configuration (the same
+    Backprojector plan), compare sampled pixels + windows around every target."""
+    s = synth.scenario(cid)
+    e = s.echoes()
+    got = _form(bpmod, s, e)
+    idx = s.sample_pixels(4096, window=15 if s.grid["nz"] == 1 else 5, seed=cid)
+    ref = oracle.tdbp_grid(e, s.tx, s.rx, s.t0, s.fc, s.fs, s.c, s.grid, idx=idx)
+    g = _at(got, idx)
+    pk = _peak_pixels(s, lambda c: oracle.tdbp_grid(e, s.tx, s.rx, s.t0, s.fc, s.fs, s.c, s.grid, idx=c), win=1)
+    pref = oracle.tdbp_grid(e, s.tx, s.rx, s.t0, s.fc, s.fs, s.c, s.grid, idx=pk)
+    _check(g, ref, _at(got, pk), pref, label=f"cfg{cid} full")
