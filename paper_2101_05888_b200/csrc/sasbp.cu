@@ -46,7 +46,7 @@ struct sas_bp_s {
   double d_max = 0;  // max |pixel - tile centre| (m)
   double hw = 0;     // half window, samples
   int W = 0;         // window slots per channel
-  bool exact_rx = false;
+  int mode = 0;      // receive-leg mode: sasbp::kSeries3 / kSeries4 / kExact
   // device memory
   float2* image = nullptr;
   float2* echoes_owned = nullptr;
@@ -75,19 +75,20 @@ sas_status cuda_fail(sas_bp_t h, cudaError_t e, const char* what) {
     if (e_ != cudaSuccess) return cuda_fail((h), e_, #call);   \
   } while (0)
 
-size_t smem_bytes(int W) {
-  return sizeof(sasbp::ChanConst) * sasbp::kNB + (size_t)sasbp::kNB * W * sizeof(float4);
-}
+size_t smem_bytes(int W) { return sasbp::k2_smem_bytes(W); }
 
-// Taylor-series truncation bound: the 4-term series of sqrt(1+eps)-1 leaves
-// |rem| <= r * (7/256) eps^5 / (1 - eps); with eps <= 2 d/r + (d/r)^2 the worst case is at
-// the smallest element-to-grid distance.  Require rem <= 1e-5 wavelength and eps <= 0.3.
-bool need_exact(double d_max, double r_min, double lambda) {
-  if (!(r_min > 0)) return true;
-  double eps = 2.0 * d_max / r_min + (d_max / r_min) * (d_max / r_min);
-  if (eps > 0.3) return true;
-  double rem = r_min * (7.0 / 256.0) * std::pow(eps, 5.0) / (1.0 - eps);
-  return rem > 1e-5 * lambda;
+// Receive-leg mode from the series truncation bound: sqrt(1+e) - 1 truncated
+// after n terms leaves |rem| <= r * |c_{n+1}| e^{n+1} / (1 - e) (alternating, decreasing terms),
+// c = 1/2, -1/8, 1/16, -5/128, 7/256; with |e| <= 2 d/r + (d/r)^2 the worst case is at the
+// smallest element-to-grid distance r_min.  Allowed: 3e-5 wavelength of path (1.9e-4 rad).
+int choose_mode(double d_max, double r_min, double lambda) {
+  if (!(r_min > 0)) return sasbp::kExact;
+  const double eps = 2.0 * d_max / r_min + (d_max / r_min) * (d_max / r_min);
+  if (eps > 0.3) return sasbp::kExact;
+  const double tol = 3e-5 * lambda;
+  if (r_min * (5.0 / 128.0) * std::pow(eps, 4.0) / (1.0 - eps) <= tol) return sasbp::kSeries3;
+  if (r_min * (7.0 / 256.0) * std::pow(eps, 5.0) / (1.0 - eps) <= tol) return sasbp::kSeries4;
+  return sasbp::kExact;
 }
 
 // distance from point p to the axis-aligned bounding box of the grid's pixel centres
@@ -102,20 +103,27 @@ double dist_to_box(const double* p, const double lo[3], const double hi[3]) {
   return std::sqrt(s);
 }
 
-template <int KX, int KY, int KZ, int WY, int WZ, bool DZ>
-cudaError_t launch_variant(const sasbp::TdbpParams& prm, bool exact, bool count, cudaStream_t st) {
-  const size_t smem = smem_bytes(prm.W);
+template <typename Kern>
+cudaError_t launch_k(Kern kern, const sasbp::TdbpParams& prm, size_t smem, cudaStream_t st) {
   const unsigned blocks = (unsigned)prm.tiles_x * prm.tiles_y * prm.tiles_z;
-  auto go = [&](auto kern) -> cudaError_t {
+  if (smem > 0) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    kern<<<blocks, sasbp::kThreads, smem, st>>>(prm);
-    return cudaGetLastError();
-  };
-  if (count) return exact ? go(sasbp::tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, true, true>)
-                          : go(sasbp::tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, false, true>);
-  return exact ? go(sasbp::tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, true, false>)
-               : go(sasbp::tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, false, false>);
+  }
+  kern<<<blocks, sasbp::kThreads, smem, st>>>(prm);
+  return cudaGetLastError();
+}
+
+template <int KX, int KY, int KZ, int WY, int WZ, bool DZ>
+cudaError_t launch_variant(const sasbp::TdbpParams& prm, int mode, bool count, cudaStream_t st) {
+  using namespace sasbp;
+  if (count) return launch_k(count_kernel<KX, KY, KZ, WY, WZ>, prm, 0, st);
+  const size_t smem = smem_bytes(prm.W);
+  switch (mode) {
+    case kSeries3: return launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kSeries3>, prm, smem, st);
+    case kSeries4: return launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kSeries4>, prm, smem, st);
+    default: return launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kExact>, prm, smem, st);
+  }
 }
 
 cudaError_t launch_tdbp(sas_bp_t h, float2* image, unsigned long long* counter, int accumulate,
@@ -141,9 +149,9 @@ cudaError_t launch_tdbp(sas_bp_t h, float2* image, unsigned long long* counter, 
   prm.W = h->W;
   prm.accumulate = accumulate;
   switch (h->variant) {
-    case V2D: return launch_variant<4, 2, 1, 4, 1, false>(prm, h->exact_rx, count, st);
-    case V2D_DZ: return launch_variant<4, 2, 1, 4, 1, true>(prm, h->exact_rx, count, st);
-    default: return launch_variant<2, 2, 2, 1, 4, true>(prm, h->exact_rx, count, st);
+    case V2D: return launch_variant<4, 2, 1, 4, 1, false>(prm, h->mode, count, st);
+    case V2D_DZ: return launch_variant<4, 2, 1, 4, 1, true>(prm, h->mode, count, st);
+    default: return launch_variant<2, 2, 2, 1, 4, true>(prm, h->mode, count, st);
   }
 }
 
@@ -189,7 +197,7 @@ sas_status upload_geo(sas_bp_t h, int32_t P, int32_t E, int32_t Ns, const double
   }
   double rmin = INFINITY;
   for (size_t i = 0; i < (size_t)P * E; ++i) rmin = std::fmin(rmin, dist_to_box(rx + 3 * i, lo, hi));
-  h->exact_rx = need_exact(h->d_max, rmin, h->c / h->fc);
+  h->mode = choose_mode(h->d_max, rmin, h->c / h->fc);
   h->P = P; h->E = E; h->Ns = Ns;
   return SAS_OK;
 }

@@ -1,24 +1,31 @@
-// tdbp_kernel.cuh -- the time-domain backprojection kernel (K2) for sm_100a.
+// tdbp_kernel.cuh -- the time-domain backprojection kernel (K2) and the in-window term counter
+// (K3) for sm_100a.
 //
 // Computes, for every pixel of a CTA tile and every channel (ping p, element e), the term
 //   ehat_{p,e}(u) * exp(+j 2 pi fc tau),  tau = (|x - tx_p| + |x - rx_{p,e}|)/c,  u = (tau - t0_p) fs
-// of Eq. (eqn:backprojection)'s inversion ("integrate the time-series into
-// the appropriate complex pixels" P:160) and accumulates it in registers.
+// of the inversion of Eq. (eqn:backprojection) ("integrate the time-series
+// into the appropriate complex pixels") and accumulates it in registers.
 //
-// Design ("K2"):
-//  * one CTA = one pixel tile (2D: 32x32, 3D: 16x8x8), 128 threads, K = 8 pixels per thread,
-//    complex accumulators in registers across ALL channels; one image store per tile;
-//  * channels are processed in batches of NB.  Per batch, a fp64 prologue computes for each
-//    channel the tile-centre reference geometry (rows a2): r_ref per leg, the
-//    window start k_lo, the window-relative reference index and the reference phase reduced
-//    mod 2 pi -- so the ~1e5-rad carrier phase never passes through fp32 (range-relative);
-//  * each channel's sample window [k_lo, k_lo + W] is staged in shared memory as
-//    (mid, slope) float4 pairs: mid_j = (d[k_lo+j] + d[k_lo+j+1])/2, slope_j = d[k_lo+j+1]-d[k_lo+j],
-//    zero outside 0..Ns-1 (reading R2) -> the lerp is one LDS.128 + 2 FFMA (row a4);
-//  * per term (rows a3-a5), fp32 and tile-relative: q = 2u.d + |d|^2, dU = q h(q/r^2) with
-//    h the 4-term series of (sqrt(1+eps)-1)/eps (or the exact form for near-field plans),
-//    U' = dU_tx + dU_rx + u_ref', k = rn(U') via the 1.5*2^23 trick, beta = U' - k,
-//    phase = U' * 2 pi fc/fs + phi0 -> MUFU sin/cos, 4 FFMA complex MAC.
+// Design (DESIGN.md §4 "K2"):
+//  * one CTA = one pixel tile (2D: 32x32, 3D: 16x8x8), 128 threads, K = 8 pixels per thread held
+//    as 4 x-adjacent PAIRS so the per-pixel fp32 geometry runs on the sm_100 paired FP32 path
+//    (FFMA2 / FADD2 / FMUL2: two lanes of math per issue slot); complex accumulators live in
+//    registers across ALL channels; one image store per tile;
+//  * channels are processed in batches of kNB.  Per batch a fp64 prologue (row a2) computes each
+//    channel's tile-centre reference geometry: leg lengths, window start k_lo, the
+//    window-relative reference index and the reference phase reduced mod 2 pi -- the ~1e5-rad
+//    carrier phase never passes through fp32 (range-relative delays);
+//  * software pipeline: while batch b is computed, batch b+1's prologue runs and its sample
+//    windows stream global -> shared with cp.async (zero-filled outside 0..Ns-1, reading R2);
+//    after a barrier each window is rewritten as (intercept, slope) float4 cells:
+//      cell j: slope = d[k_lo+j+1] - d[k_lo+j], intercept = mid_j - (j - Wh) * slope
+//    so the linear interpolation (row a4) at window coordinate U is one LDS.128 + one FFMA2:
+//      ehat = intercept_j + U * slope_j,  j = rn(U) + Wh;
+//  * per term (rows a3-a5): q = 2u.d + |d|^2; dU_rx = q h(q / r^2) with h the truncated series of
+//    (sqrt(1+eps) - 1)/eps (3 or 4 terms by a plan-time error bound) or the exact form for
+//    near-field plans; U = dU_tx + dU_rx + u_ref; j via the 1.5*2^23 rounding trick;
+//    phase = U * 2 pi fc/fs + phi0 -> MUFU sin/cos; the complex MAC is 2 FFMA2 into
+//    A += Re(ehat)(cos, sin), B += Im(ehat)(cos, sin); I = (A.x - B.y, A.y + B.x).
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -27,6 +34,12 @@ namespace sasbp {
 
 constexpr int kThreads = 128;   // 4 warps
 constexpr int kNB = 32;         // channels per batch
+constexpr int kChPerWarp = kNB / (kThreads / 32);
+
+// receive-leg evaluation modes
+constexpr int kSeries3 = 0;     // 3-term series in eps
+constexpr int kSeries4 = 1;     // 4-term series in eps
+constexpr int kExact = 2;       // q / (sqrt(r^2 + q) + r)
 
 struct TdbpParams {
   const float2* echoes;   // [P*E][Ns]
@@ -34,25 +47,25 @@ struct TdbpParams {
   const double* rx;       // [P*E][3]
   const double* t0;       // [P]
   float2* image;          // [nz][ny][nx]
-  unsigned long long* counter;  // COUNT mode: in-window term total
+  unsigned long long* counter;  // K3: in-window term total
   double origin[3], sx[3], sy[3], sz[3];
   double fc, fs, c;
   double hw;              // half window in samples: 2 * d_max * fs / c
   int P, E, Ns;
   int nx, ny, nz;
   int tiles_x, tiles_y, tiles_z;
-  int W;                  // window slots per channel
+  int W;                  // window cells per channel (cells j = 0..W-1 use samples k_lo+j, k_lo+j+1)
   int accumulate;
 };
 
-// per-channel constants in shared memory (computed by the fp64 prologue)
+// per-channel constants in shared memory (fp64 prologue output)
 struct __align__(16) ChanConst {
   float ux2, uy2, uz2, ir2;     // rx leg: 2 (c_T - rx), 1 / r_r^2
   float a0, a1, a2, a3;         // rx leg series coefficients * (fs/c) / r_r
-  float urr, phi0, r_r, r2_r;   // window-relative ref index - 0.5; phase offset (rad); r_r; r_r^2
+  float urr, phi0, r_r, r2_r;   // centred window coordinate offset; phase offset (rad); r_r; r_r^2
   float tx2x, tx2y, tx2z, r2_t; // tx leg: 2 (c_T - tx), r_t^2
-  float r_t, kfs, pad0, pad1;   // r_t, fs/c
-  int ping, woff, klo, pad2;    // ping index; LDS byte offset - MAGIC*16; window start
+  float r_t, kfs, klo_f, pad1;  // r_t, fs/c, (float) k_lo
+  int ping, woff, klo, pad2;    // ping index; LDS byte offset of cell Wh minus MAGIC*16; window start
 };
 
 constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23: x + kMagic rounds x to an integer in the low bits
@@ -60,11 +73,9 @@ constexpr int kMagicBits = 0x4B400000;
 
 __device__ __forceinline__ float4 lds128(uint32_t addr) {
   float4 v;
-  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
   return v;
 }
-
 __device__ __forceinline__ float rcp_approx(float x) {
   float y;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -75,194 +86,295 @@ __device__ __forceinline__ float rsqrt_approx(float x) {
   asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+__device__ __forceinline__ void cp_async8(uint32_t dst, const void* src, bool valid) {
+  // 8-byte global -> shared copy; src-size 0 writes zeros (zero extension, reading R2)
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst), "l"(src), "r"(valid ? 8 : 0));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
-// fp64 prologue for one channel (row a2)
-__device__ __forceinline__ void chan_prologue(const TdbpParams& prm, int ch, const double ct[3],
-                                              int slot, uint32_t win_base, ChanConst* out) {
+__device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
+
+// fp64 prologue for one channel (row a2): reference geometry at the tile centre ct.
+__device__ __forceinline__ ChanConst chan_prologue(const TdbpParams& prm, int ch, const double ct[3], int slot,
+                                                   uint32_t win_base) {
   const int p = ch / prm.E;
   const double* T = prm.tx + 3 * p;
   const double* R = prm.rx + 3 * (size_t)ch;
-  double utx = ct[0] - T[0], uty = ct[1] - T[1], utz = ct[2] - T[2];
-  double urx = ct[0] - R[0], ury = ct[1] - R[1], urz = ct[2] - R[2];
-  double r_t = sqrt(utx * utx + uty * uty + utz * utz);
-  double r_r = sqrt(urx * urx + ury * ury + urz * urz);
-  double K = prm.fs / prm.c;
-  double t0 = prm.t0[p];
-  double Uref = (r_t + r_r) * K - t0 * prm.fs;          // absolute sample index at tile centre
-  double klo_d = floor(Uref - prm.hw) - 2.0;
-  int klo = (int)fmax(fmin(klo_d, 2.0e9), -2.0e9);
-  double urr = Uref - (double)klo - 0.5;
-  double cyc = prm.fc * (r_t + r_r) / prm.c;             // reference phase in cycles (fp64)
-  double ph = cyc - urr * (prm.fc / prm.fs);
+  const double utx = ct[0] - T[0], uty = ct[1] - T[1], utz = ct[2] - T[2];
+  const double urx = ct[0] - R[0], ury = ct[1] - R[1], urz = ct[2] - R[2];
+  const double r_t = sqrt(utx * utx + uty * uty + utz * utz);
+  const double r_r = sqrt(urx * urx + ury * ury + urz * urz);
+  const double K = prm.fs / prm.c;
+  const double Uref = (r_t + r_r) * K - prm.t0[p] * prm.fs;   // absolute sample index at tile centre
+  const double klo_d = floor(Uref - prm.hw) - 2.0;
+  const int klo = (int)fmax(fmin(klo_d, 2.0e9), -2.0e9);
+  const int Wh = prm.W >> 1;
+  // window coordinate U = u - k_lo - 0.5 - Wh, so cell j = rn(U) + Wh
+  const double urr = Uref - (double)klo - 0.5 - (double)Wh;
+  const double cyc = prm.fc * (r_t + r_r) / prm.c;            // reference phase, cycles (fp64)
+  double ph = cyc - urr * (prm.fc / prm.fs);                   // phase at U = 0
   ph -= floor(ph);
   ChanConst k;
   k.ux2 = (float)(2.0 * urx); k.uy2 = (float)(2.0 * ury); k.uz2 = (float)(2.0 * urz);
-  double ir = 1.0 / r_r;
+  const double ir = 1.0 / r_r;
   k.ir2 = (float)(ir * ir);
-  double g = K * ir;
-  k.a0 = (float)(0.5 * g); k.a1 = (float)(-0.125 * g); k.a2 = (float)(0.0625 * g);
-  k.a3 = (float)(-0.0390625 * g);
+  const double g = K * ir;   // (sqrt(1+e)-1)/e = 1/2 - e/8 + e^2/16 - 5e^3/128 + ...
+  k.a0 = (float)(0.5 * g); k.a1 = (float)(-0.125 * g); k.a2 = (float)(0.0625 * g); k.a3 = (float)(-0.0390625 * g);
   k.urr = (float)urr;
   k.phi0 = (float)(6.283185307179586 * ph);
   k.r_r = (float)r_r; k.r2_r = (float)(r_r * r_r);
   k.tx2x = (float)(2.0 * utx); k.tx2y = (float)(2.0 * uty); k.tx2z = (float)(2.0 * utz);
   k.r2_t = (float)(r_t * r_t); k.r_t = (float)r_t; k.kfs = (float)K;
-  k.pad0 = 0.f; k.pad1 = 0.f;
+  k.klo_f = (float)klo; k.pad1 = 0.f;
   k.ping = p;
-  k.woff = (int)(win_base + (uint32_t)(slot * prm.W) * 16u - (uint32_t)kMagicBits * 16u);
+  k.woff = (int)(win_base + (uint32_t)(slot * prm.W + Wh) * 16u - (uint32_t)kMagicBits * 16u);
   k.klo = klo;
   k.pad2 = 0;
-  *out = k;
+  return k;
 }
 
-template <int KX, int KY, int KZ, int WY, int WZ, bool HAS_DZ, bool EXACT_RX, bool COUNT>
-__global__ void __launch_bounds__(kThreads, 4) tdbp_kernel(const TdbpParams prm) {
-  constexpr int K = KX * KY * KZ;
-  constexpr int TX = 8 * KX, TY = 4 * KY * WY, TZ = KZ * WZ;
-  extern __shared__ float4 smem[];
-  ChanConst* cc = reinterpret_cast<ChanConst*>(smem);
-  float4* win = smem + kNB * (sizeof(ChanConst) / 16);
+// tile bookkeeping shared by K2 and K3
+template <int KX, int KY, int KZ, int WY, int WZ>
+struct TileMap {
+  static constexpr int K = KX * KY * KZ;
+  static constexpr int NP = K / 2;  // x-adjacent pixel pairs per thread
+  static constexpr int TX = 8 * KX, TY = 4 * KY * WY, TZ = KZ * WZ;
+  int x0, y0, z0, lx, ly, wy, wz;
+  __device__ TileMap(const TdbpParams& prm) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    lx = lane >> 2; ly = lane & 3;          // quarter-warp = 4 (y) x 2 (x) pixel patch
+    wy = warp % WY; wz = warp / WY;
+    int b = blockIdx.x;
+    const int tix = b % prm.tiles_x; b /= prm.tiles_x;
+    const int tiy = b % prm.tiles_y; b /= prm.tiles_y;
+    x0 = tix * TX; y0 = tiy * TY; z0 = b * TZ;
+  }
+  // pixel k = ((kz * KY + ky) * KX + kx); pairs are (kx even, kx odd)
+  __device__ int ix(int k) const { return x0 + lx + 8 * (k % KX); }
+  __device__ int iy(int k) const { return y0 + ly + 4 * ((k / KX) % KY) + 4 * KY * wy; }
+  __device__ int iz(int k) const { return z0 + (k / (KX * KY)) + KZ * wz; }
+  __device__ void centre(const TdbpParams& prm, double ct[3]) const {
+    const double cxr = x0 + 0.5 * (TX - 1), cyr = y0 + 0.5 * (TY - 1), czr = z0 + 0.5 * (TZ - 1);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) ct[a] = prm.origin[a] + cxr * prm.sx[a] + cyr * prm.sy[a] + czr * prm.sz[a];
+  }
+  __device__ void offset(const TdbpParams& prm, int k, float& dx, float& dy, float& dz) const {
+    const float rxi = (float)(ix(k) - x0) - 0.5f * (TX - 1);
+    const float ryi = (float)(iy(k) - y0) - 0.5f * (TY - 1);
+    const float rzi = (float)(iz(k) - z0) - 0.5f * (TZ - 1);
+    dx = rxi * (float)prm.sx[0] + ryi * (float)prm.sy[0] + rzi * (float)prm.sz[0];
+    dy = rxi * (float)prm.sx[1] + ryi * (float)prm.sy[1] + rzi * (float)prm.sz[1];
+    dz = rxi * (float)prm.sx[2] + ryi * (float)prm.sy[2] + rzi * (float)prm.sz[2];
+  }
+  __device__ bool valid(const TdbpParams& prm, int k) const {
+    return ix(k) < prm.nx && iy(k) < prm.ny && iz(k) < prm.nz;
+  }
+};
+
+// shared-memory layout of K2 (bytes): cc[2][kNB] | raw[kNB][W+1] float2 (16-B padded) | win[kNB][W] float4
+__host__ __device__ inline size_t raw_stride(int W) { return (size_t)((W + 1 + 1) & ~1); }  // float2 units, even
+__host__ __device__ inline size_t k2_smem_bytes(int W) {
+  return 2 * kNB * sizeof(ChanConst) + (size_t)kNB * raw_stride(W) * sizeof(float2) + (size_t)kNB * W * sizeof(float4);
+}
+
+template <int KX, int KY, int KZ, int WY, int WZ, bool HAS_DZ, int MODE>
+__global__ void __launch_bounds__(kThreads, 3) tdbp_kernel(const TdbpParams prm) {
+  using TM = TileMap<KX, KY, KZ, WY, WZ>;
+  constexpr int NP = TM::NP;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  ChanConst* cc = reinterpret_cast<ChanConst*>(smem_raw);                       // [2][kNB]
+  float2* raw = reinterpret_cast<float2*>(smem_raw + 2 * kNB * sizeof(ChanConst));
+  const size_t rs = raw_stride(prm.W);
+  float4* win = reinterpret_cast<float4*>(reinterpret_cast<unsigned char*>(raw) + kNB * rs * sizeof(float2));
   const uint32_t win_base = (uint32_t)__cvta_generic_to_shared(win);
+  const uint32_t raw_base = (uint32_t)__cvta_generic_to_shared(raw);
 
-  const int tid = threadIdx.x;
-  const int lane = tid & 31, warp = tid >> 5;
-  const int lx = lane >> 2, ly = lane & 3;
-  const int wy = warp % WY, wz = warp / WY;
-
-  int b = blockIdx.x;
-  const int tix = b % prm.tiles_x; b /= prm.tiles_x;
-  const int tiy = b % prm.tiles_y; b /= prm.tiles_y;
-  const int tiz = b;
-  const int x0 = tix * TX, y0 = tiy * TY, z0 = tiz * TZ;
-
-  // tile centre (fp64) -- reference point for the range-relative geometry
-  const double cxr = x0 + 0.5 * (TX - 1), cyr = y0 + 0.5 * (TY - 1), czr = z0 + 0.5 * (TZ - 1);
+  const TM tm(prm);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double ct[3];
-#pragma unroll
-  for (int a = 0; a < 3; ++a)
-    ct[a] = prm.origin[a] + cxr * prm.sx[a] + cyr * prm.sy[a] + czr * prm.sz[a];
+  tm.centre(prm, ct);
 
-  // per-pixel offsets from the tile centre (small, exact-ish in fp32)
-  float dx[K], dy[K], dz[K], dd[K], acc_re[K], acc_im[K], btx[K];
-  bool valid[K];
-  unsigned cnt = 0;
+  // per-pixel-pair offsets from the tile centre and accumulators
+  float2 DX[NP], DY[NP], DZ[NP], DD[NP], BT[NP];
+  float2 A[2 * NP], B[2 * NP];
 #pragma unroll
-  for (int kz = 0; kz < KZ; ++kz)
-#pragma unroll
-    for (int ky = 0; ky < KY; ++ky)
-#pragma unroll
-      for (int kx = 0; kx < KX; ++kx) {
-        const int k = (kz * KY + ky) * KX + kx;
-        const float rxi = (float)(lx + 8 * kx) - 0.5f * (TX - 1);
-        const float ryi = (float)(ly + 4 * ky + 4 * KY * wy) - 0.5f * (TY - 1);
-        const float rzi = (float)(kz + KZ * wz) - 0.5f * (TZ - 1);
-        dx[k] = rxi * (float)prm.sx[0] + ryi * (float)prm.sy[0] + rzi * (float)prm.sz[0];
-        dy[k] = rxi * (float)prm.sx[1] + ryi * (float)prm.sy[1] + rzi * (float)prm.sz[1];
-        dz[k] = HAS_DZ ? rxi * (float)prm.sx[2] + ryi * (float)prm.sy[2] + rzi * (float)prm.sz[2] : 0.f;
-        dd[k] = dx[k] * dx[k] + dy[k] * dy[k] + dz[k] * dz[k];
-        acc_re[k] = 0.f; acc_im[k] = 0.f; btx[k] = 0.f;
-        valid[k] = (x0 + lx + 8 * kx < prm.nx) && (y0 + ly + 4 * ky + 4 * KY * wy < prm.ny) &&
-                   (z0 + kz + KZ * wz < prm.nz);
-      }
+  for (int p = 0; p < NP; ++p) {
+    float dx0, dy0, dz0, dx1, dy1, dz1;
+    tm.offset(prm, 2 * p, dx0, dy0, dz0);
+    tm.offset(prm, 2 * p + 1, dx1, dy1, dz1);
+    if (!HAS_DZ) { dz0 = 0.f; dz1 = 0.f; }
+    DX[p] = make_float2(dx0, dx1); DY[p] = make_float2(dy0, dy1); DZ[p] = make_float2(dz0, dz1);
+    DD[p] = make_float2(dx0 * dx0 + dy0 * dy0 + dz0 * dz0, dx1 * dx1 + dy1 * dy1 + dz1 * dz1);
+    BT[p] = f2(0.f);
+    A[2 * p] = f2(0.f); A[2 * p + 1] = f2(0.f); B[2 * p] = f2(0.f); B[2 * p + 1] = f2(0.f);
+  }
 
   const float kph = (float)(6.283185307179586 * prm.fc / prm.fs);
   const int nch = prm.P * prm.E;
   const int W = prm.W;
-  int cur_ping = -1;
+  const int nbatch = (nch + kNB - 1) / kNB;
 
-  for (int ch0 = 0; ch0 < nch; ch0 += kNB) {
+  // stage batch b: prologue for this warp's channels, then cp.async of their raw windows
+  auto issue = [&](int b) {
+    const int ch0 = b * kNB;
     const int nb = min(kNB, nch - ch0);
-    __syncthreads();
-    if (tid < nb) chan_prologue(prm, ch0 + tid, ct, tid, win_base, &cc[tid]);
-    __syncthreads();
-    // stage windows: slot j of channel c holds (mid, slope) of samples k_lo+j, k_lo+j+1
-    for (int i = tid; i < nb * W; i += kThreads) {
-      const int c = i / W, j = i - c * W;
-      const int n = cc[c].klo + j;
+    ChanConst* cb = cc + (b & 1) * kNB;
+    const int c_lo = warp * kChPerWarp;
+    if (lane < kChPerWarp && c_lo + lane < nb) cb[c_lo + lane] = chan_prologue(prm, ch0 + c_lo + lane, ct, c_lo + lane, win_base);
+    __syncwarp();
+    const int cnt = W + 1;
+    for (int c = c_lo; c < c_lo + kChPerWarp && c < nb; ++c) {
+      const int klo = cb[c].klo;
       const float2* row = prm.echoes + (size_t)(ch0 + c) * prm.Ns;
-      float2 d0 = make_float2(0.f, 0.f), d1 = make_float2(0.f, 0.f);
-      if (n >= 0 && n < prm.Ns) d0 = __ldg(row + n);
-      if (n + 1 >= 0 && n + 1 < prm.Ns) d1 = __ldg(row + n + 1);
-      win[c * W + j] = make_float4(0.5f * (d0.x + d1.x), 0.5f * (d0.y + d1.y), d1.x - d0.x, d1.y - d0.y);
+      const uint32_t dst = raw_base + (uint32_t)(c * rs) * 8u;
+      for (int j = lane; j < cnt; j += 32) {
+        const int n = klo + j;
+        const bool ok = (n >= 0) && (n < prm.Ns);
+        cp_async8(dst + 8u * j, ok ? (const void*)(row + n) : (const void*)row, ok);
+      }
     }
-    __syncthreads();
+    cp_async_commit();
+  };
+
+  issue(0);
+  int cur_ping = -1;
+  const int Wh = W >> 1;
+
+  for (int b = 0; b < nbatch; ++b) {
+    const int nb = min(kNB, nch - b * kNB);
+    cp_async_wait_all();
+    __syncthreads();   // every warp's raw(b) landed; compute(b-1) is done with win
+    // each warp rewrites the raw windows it staged as (intercept, slope) cells
+    for (int c = warp * kChPerWarp; c < warp * kChPerWarp + kChPerWarp && c < nb; ++c) {
+      const float2* rw = raw + c * rs;
+      float4* wc = win + c * W;
+      for (int j = lane; j < W; j += 32) {
+        const float2 d0 = rw[j], d1 = rw[j + 1];
+        const float sr = d1.x - d0.x, si = d1.y - d0.y;
+        const float jj = (float)(j - Wh);
+        wc[j] = make_float4(fmaf(-jj, sr, 0.5f * (d0.x + d1.x)), fmaf(-jj, si, 0.5f * (d0.y + d1.y)), sr, si);
+      }
+    }
+    __syncthreads();   // win(b) complete
+    if (b + 1 < nbatch) issue(b + 1);
+    const ChanConst* cb = cc + (b & 1) * kNB;
 
 #pragma unroll 1
     for (int c = 0; c < nb; ++c) {
-      const ChanConst kc = cc[c];
+      const ChanConst kc = cb[c];
       if (kc.ping != cur_ping) {
         cur_ping = kc.ping;
-        // transmit leg, exact range-relative form: dR = q / (sqrt(r^2 + q) + r)
+        // transmit leg, exact range-relative form: dR = q / (sqrt(r^2 + q) + r), in samples
 #pragma unroll
-        for (int k = 0; k < K; ++k) {
-          float q = fmaf(kc.tx2x, dx[k], fmaf(kc.tx2y, dy[k], HAS_DZ ? fmaf(kc.tx2z, dz[k], dd[k]) : dd[k]));
-          float r2 = kc.r2_t + q;
-          float den = fmaf(r2, rsqrt_approx(r2), kc.r_t);
-          btx[k] = q * rcp_approx(den) * kc.kfs;
+        for (int p = 0; p < NP; ++p) {
+          float2 q = __ffma2_rn(f2(kc.tx2y), DY[p], DD[p]);
+          q = __ffma2_rn(f2(kc.tx2x), DX[p], q);
+          if (HAS_DZ) q = __ffma2_rn(f2(kc.tx2z), DZ[p], q);
+          const float2 r2 = __fadd2_rn(q, f2(kc.r2_t));
+          const float den0 = fmaf(r2.x, rsqrt_approx(r2.x), kc.r_t);
+          const float den1 = fmaf(r2.y, rsqrt_approx(r2.y), kc.r_t);
+          BT[p] = __fmul2_rn(__fmul2_rn(q, make_float2(rcp_approx(den0), rcp_approx(den1))), f2(kc.kfs));
         }
       }
 #pragma unroll
-      for (int k = 0; k < K; ++k) {
-        float q = fmaf(kc.ux2, dx[k], fmaf(kc.uy2, dy[k], HAS_DZ ? fmaf(kc.uz2, dz[k], dd[k]) : dd[k]));
-        float du;
-        if (EXACT_RX) {
-          float r2 = kc.r2_r + q;
-          float den = fmaf(r2, rsqrt_approx(r2), kc.r_r);
-          du = q * rcp_approx(den) * kc.kfs;
-          du += btx[k];
+      for (int p = 0; p < NP; ++p) {
+        float2 q = __ffma2_rn(f2(kc.uy2), DY[p], DD[p]);
+        q = __ffma2_rn(f2(kc.ux2), DX[p], q);
+        if (HAS_DZ) q = __ffma2_rn(f2(kc.uz2), DZ[p], q);
+        float2 U;
+        if (MODE == kExact) {
+          const float2 r2 = __fadd2_rn(q, f2(kc.r2_r));
+          const float den0 = fmaf(r2.x, rsqrt_approx(r2.x), kc.r_r);
+          const float den1 = fmaf(r2.y, rsqrt_approx(r2.y), kc.r_r);
+          U = __ffma2_rn(__fmul2_rn(q, make_float2(rcp_approx(den0), rcp_approx(den1))), f2(kc.kfs), BT[p]);
         } else {
-          float e = q * kc.ir2;
-          float h = fmaf(fmaf(fmaf(kc.a3, e, kc.a2), e, kc.a1), e, kc.a0);
-          du = fmaf(q, h, btx[k]);
+          const float2 e = __fmul2_rn(q, f2(kc.ir2));
+          float2 h;
+          if (MODE == kSeries4) {
+            h = __ffma2_rn(f2(kc.a3), e, f2(kc.a2));
+            h = __ffma2_rn(h, e, f2(kc.a1));
+          } else {
+            h = __ffma2_rn(f2(kc.a2), e, f2(kc.a1));
+          }
+          h = __ffma2_rn(h, e, f2(kc.a0));
+          U = __ffma2_rn(q, h, BT[p]);
         }
-        const float U = du + kc.urr;   // window-relative sample index - 0.5
-        if (COUNT) {
-          // absolute u = k_lo + U + 0.5 in (-1, Ns): the term's support meets the record
-          const float ua = (float)kc.klo + U + 0.5f;
-          cnt += (valid[k] && ua > -1.f && ua < (float)prm.Ns) ? 1u : 0u;
-        } else {
-          const float T = U + kMagic;
-          const float beta = U - (T - kMagic);
-          const uint32_t addr = (uint32_t)__float_as_int(T) * 16u + (uint32_t)kc.woff;
-          const float4 w = lds128(addr);
-          const float er = fmaf(beta, w.z, w.x);
-          const float ei = fmaf(beta, w.w, w.y);
+        U = __fadd2_rn(U, f2(kc.urr));                       // centred window coordinate
+        const float2 T = __fadd2_rn(U, f2(kMagic));          // rn(U) in the mantissa
+        const float2 ph = __ffma2_rn(U, f2(kph), f2(kc.phi0));
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+          const float Us = s ? U.y : U.x;
+          const float Ts = s ? T.y : T.x;
+          const float phs = s ? ph.y : ph.x;
+          const float4 w = lds128((uint32_t)__float_as_int(Ts) * 16u + (uint32_t)kc.woff);
+          const float2 eh = __ffma2_rn(f2(Us), make_float2(w.z, w.w), make_float2(w.x, w.y));
           float sn, cs;
-          __sincosf(fmaf(U, kph, kc.phi0), &sn, &cs);
-          acc_re[k] = fmaf(er, cs, acc_re[k]);
-          acc_re[k] = fmaf(-ei, sn, acc_re[k]);
-          acc_im[k] = fmaf(er, sn, acc_im[k]);
-          acc_im[k] = fmaf(ei, cs, acc_im[k]);
+          __sincosf(phs, &sn, &cs);
+          const float2 rot = make_float2(cs, sn);
+          A[2 * p + s] = __ffma2_rn(f2(eh.x), rot, A[2 * p + s]);
+          B[2 * p + s] = __ffma2_rn(f2(eh.y), rot, B[2 * p + s]);
         }
       }
     }
   }
 
-  if (COUNT) {
-    // warp reduce then one atomic per warp
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-    if (lane == 0) atomicAdd(prm.counter, (unsigned long long)cnt);
-    return;
+  for (int k = 0; k < 2 * NP; ++k) {
+    if (tm.valid(prm, k)) {
+      float2* o = prm.image + ((size_t)tm.iz(k) * prm.ny + tm.iy(k)) * prm.nx + tm.ix(k);
+      float2 v = make_float2(A[k].x - B[k].y, A[k].y + B[k].x);
+      if (prm.accumulate) { const float2 a = *o; v.x += a.x; v.y += a.y; }
+      *o = v;
+    }
   }
+}
 
+// K3: count terms whose interpolation support meets the record, u in (-1, Ns).
+// Same tiles and fp32 delay arithmetic as K2 (exact leg form), no echo traffic.
+template <int KX, int KY, int KZ, int WY, int WZ>
+__global__ void __launch_bounds__(kThreads) count_kernel(const TdbpParams prm) {
+  using TM = TileMap<KX, KY, KZ, WY, WZ>;
+  constexpr int K = TM::K;
+  __shared__ ChanConst cc[kNB];
+  const TM tm(prm);
+  const int tid = threadIdx.x;
+  double ct[3];
+  tm.centre(prm, ct);
+  float dx[K], dy[K], dz[K], dd[K];
+  bool ok[K];
 #pragma unroll
-  for (int kz = 0; kz < KZ; ++kz)
+  for (int k = 0; k < K; ++k) {
+    tm.offset(prm, k, dx[k], dy[k], dz[k]);
+    dd[k] = dx[k] * dx[k] + dy[k] * dy[k] + dz[k] * dz[k];
+    ok[k] = tm.valid(prm, k);
+  }
+  const int nch = prm.P * prm.E;
+  const float Nsf = (float)prm.Ns;
+  unsigned cnt = 0;
+  for (int ch0 = 0; ch0 < nch; ch0 += kNB) {
+    const int nb = min(kNB, nch - ch0);
+    __syncthreads();
+    if (tid < nb) cc[tid] = chan_prologue(prm, ch0 + tid, ct, tid, 0u);
+    __syncthreads();
+    for (int c = 0; c < nb; ++c) {
+      const ChanConst kc = cc[c];
 #pragma unroll
-    for (int ky = 0; ky < KY; ++ky)
-#pragma unroll
-      for (int kx = 0; kx < KX; ++kx) {
-        const int k = (kz * KY + ky) * KX + kx;
-        const int ix = x0 + lx + 8 * kx;
-        const int iy = y0 + ly + 4 * ky + 4 * KY * wy;
-        const int iz = z0 + kz + KZ * wz;
-        if (valid[k]) {
-          float2* o = prm.image + ((size_t)iz * prm.ny + iy) * prm.nx + ix;
-          float2 v = make_float2(acc_re[k], acc_im[k]);
-          if (prm.accumulate) { float2 a = *o; v.x += a.x; v.y += a.y; }
-          *o = v;
-        }
+      for (int k = 0; k < K; ++k) {
+        const float qt = fmaf(kc.tx2x, dx[k], fmaf(kc.tx2y, dy[k], fmaf(kc.tx2z, dz[k], dd[k])));
+        const float qr = fmaf(kc.ux2, dx[k], fmaf(kc.uy2, dy[k], fmaf(kc.uz2, dz[k], dd[k])));
+        const float rt = sqrtf(kc.r2_t + qt), rr = sqrtf(kc.r2_r + qr);
+        const float du = (qt / (rt + kc.r_t) + qr / (rr + kc.r_r)) * kc.kfs;
+        // absolute u = k_lo + 0.5 + Wh + (du + urr)
+        const float ua = kc.klo_f + 0.5f + (float)(prm.W >> 1) + (du + kc.urr);
+        cnt += (ok[k] && ua > -1.f && ua < Nsf) ? 1u : 0u;
       }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if ((tid & 31) == 0) atomicAdd(prm.counter, (unsigned long long)cnt);
 }
 
 }  // namespace sasbp

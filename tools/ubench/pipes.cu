@@ -13,7 +13,7 @@
   fprintf(stderr, "CUDA %s at %s:%d\n", cudaGetErrorString(e_), __FILE__, __LINE__); return 1; } } while (0)
 
 constexpr int CH = 8;        // independent chains per thread
-constexpr int ITERS = 4096;
+constexpr int ITERS = 1 << 16;
 
 __device__ unsigned long long g_cycles[4096];
 
@@ -49,6 +49,35 @@ __global__ void k_ffma_imm(float* out, float a) {
   float s = 0.f;
 #pragma unroll
   for (int i = 0; i < CH; ++i) s += x[i];
+  if (s == 1234.5f) out[0] = s;
+  if (threadIdx.x == 0) g_cycles[blockIdx.x] = t1 - t0;
+}
+
+__device__ __forceinline__ unsigned long long ffma2(unsigned long long a, unsigned long long b,
+                                                    unsigned long long c) {
+  unsigned long long d;
+  asm volatile("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+
+__global__ void k_ffma2(float* out, float a, float b) {
+  unsigned long long x[CH];
+#pragma unroll
+  for (int i = 0; i < CH; ++i) {
+    float2 v = make_float2(threadIdx.x * 1e-3f + i, i * 0.5f);
+    x[i] = *reinterpret_cast<unsigned long long*>(&v);
+  }
+  float2 yv = make_float2(a * 0.5f, a * 0.25f), zv = make_float2(b * 0.25f, b);
+  unsigned long long y = *reinterpret_cast<unsigned long long*>(&yv), z = *reinterpret_cast<unsigned long long*>(&zv);
+  unsigned long long t0 = clock64();
+  for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+    for (int i = 0; i < CH; ++i) x[i] = ffma2(x[i], y, z);
+  }
+  unsigned long long t1 = clock64();
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < CH; ++i) { float2 v = *reinterpret_cast<float2*>(&x[i]); s += v.x + v.y; }
   if (s == 1234.5f) out[0] = s;
   if (threadIdx.x == 0) g_cycles[blockIdx.x] = t1 - t0;
 }
@@ -150,6 +179,8 @@ int main() {
   float* out; CK(cudaMalloc(&out, 16));
   const int T = 256, B = sms * 4;  // 32 warps/SM, all co-resident
   if (run("ffma_3reg", [&] { k_ffma<<<B, T>>>(out, 1.0001f, 0.999f); }, B, T, (double)ITERS * CH, sms, clk_khz)) return 1;
+  // FFMA2 (fma.rn.f32x2): count scalar FMAs (2 per instruction)
+  if (run("ffma2_pairs", [&] { k_ffma2<<<B, T>>>(out, 1.0001f, 0.999f); }, B, T, (double)ITERS * CH * 2, sms, clk_khz)) return 1;
   if (run("ffma_imm", [&] { k_ffma_imm<<<B, T>>>(out, 1.0001f); }, B, T, (double)ITERS * CH, sms, clk_khz)) return 1;
   // sincos: count MUFU ops (2 per step)
   if (run("mufu_sin_cos", [&] { k_sincos<<<B, T>>>(out, 1.f); }, B, T, (double)(ITERS / 4) * CH * 2, sms, clk_khz)) return 1;
