@@ -115,6 +115,24 @@ SASBP_API sas_status sas_bp_form_device(sas_bp_t h, void* image_dev, void* cuda_
  *            (SURVEY §8(d) N_u), counted on the device in fp32 (K3).  Either may be NULL. */
 SASBP_API sas_status sas_bp_count_terms(sas_bp_t h, uint64_t* dense, uint64_t* in_win);
 
+/* The execution plan chosen for the current grid and ping set (diagnostics / tests):
+ *   tile      pixels per CTA tile (x, y, z)
+ *   window    samples staged per (tile, channel): cells of the interpolation window
+ *   rx_mode   0 = 3-term series, 1 = 4-term series, 2 = exact receive-leg delay (chosen from
+ *             the series truncation bound)
+ *   tma       1 = windows staged by TMA tensor loads, 0 = cp.async fallback (odd Ns, unaligned
+ *             device echoes, or SASBP_NO_TMA=1 in the environment at set_pings time)
+ *   batch     channels (ping x element) staged per pipeline step
+ * Errors: SAS_E_INVALID for NULL; rx_mode / tma are -1 before the first set_pings. */
+typedef struct {
+  int32_t tile[3];
+  int32_t window;
+  int32_t rx_mode;
+  int32_t tma;
+  int32_t batch;
+} sas_bp_plan;
+SASBP_API sas_status sas_bp_get_plan(sas_bp_t h, sas_bp_plan* out);
+
 /* Bytes of device memory the handle owns (image + workspace + owned ping copy). */
 SASBP_API size_t sas_bp_workspace_bytes(sas_bp_t h);
 

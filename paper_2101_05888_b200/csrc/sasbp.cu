@@ -8,10 +8,13 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <vector>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include "tdbp_kernel.cuh"
@@ -57,6 +60,9 @@ struct sas_bp_s {
   unsigned long long* counter = nullptr;
   cudaStream_t stream = nullptr;
   int P = 0, E = 0, Ns = 0;
+  // TMA descriptor of the current echoes (row staging), rebuilt when the ping set changes
+  sasbp::TmaDesc tmap{};
+  bool use_tma = false;
   bool has_pings = false;
   bool broken = false;
   size_t bytes = 0;
@@ -104,26 +110,65 @@ double dist_to_box(const double* p, const double lo[3], const double hi[3]) {
 }
 
 template <typename Kern>
-cudaError_t launch_k(Kern kern, const sasbp::TdbpParams& prm, size_t smem, cudaStream_t st) {
+cudaError_t launch_k(Kern kern, const sasbp::TdbpParams& prm, const sasbp::TmaDesc& tmap, size_t smem, cudaStream_t st) {
   const unsigned blocks = (unsigned)prm.tiles_x * prm.tiles_y * prm.tiles_z;
   if (smem > 0) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  kern<<<blocks, sasbp::kThreads, smem, st>>>(prm);
+  kern<<<blocks, sasbp::kThreads, smem, st>>>(prm, tmap);
   return cudaGetLastError();
 }
 
-template <int KX, int KY, int KZ, int WY, int WZ, bool DZ>
-cudaError_t launch_variant(const sasbp::TdbpParams& prm, int mode, bool count, cudaStream_t st) {
+template <int KX, int KY, int KZ, int WY, int WZ, bool DZ, bool TMA>
+cudaError_t launch_mode(const sasbp::TdbpParams& prm, const sasbp::TmaDesc& tmap, int mode, cudaStream_t st) {
   using namespace sasbp;
-  if (count) return launch_k(count_kernel<KX, KY, KZ, WY, WZ>, prm, 0, st);
   const size_t smem = smem_bytes(prm.W);
   switch (mode) {
-    case kSeries3: return launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kSeries3>, prm, smem, st);
-    case kSeries4: return launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kSeries4>, prm, smem, st);
-    default: return launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kExact>, prm, smem, st);
+    case kSeries3: return launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kSeries3, TMA>, prm, tmap, smem, st);
+    case kSeries4: return launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kSeries4, TMA>, prm, tmap, smem, st);
+    default: return launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kExact, TMA>, prm, tmap, smem, st);
   }
+}
+
+template <int KX, int KY, int KZ, int WY, int WZ, bool DZ>
+cudaError_t launch_variant(const sasbp::TdbpParams& prm, const sasbp::TmaDesc& tmap, bool tma, int mode, bool count,
+                           cudaStream_t st) {
+  using namespace sasbp;
+  if (count) {
+    const unsigned blocks = (unsigned)prm.tiles_x * prm.tiles_y * prm.tiles_z;
+    count_kernel<KX, KY, KZ, WY, WZ><<<blocks, kThreads, 0, st>>>(prm);
+    return cudaGetLastError();
+  }
+  return tma ? launch_mode<KX, KY, KZ, WY, WZ, DZ, true>(prm, tmap, mode, st)
+             : launch_mode<KX, KY, KZ, WY, WZ, DZ, false>(prm, tmap, mode, st);
+}
+
+// Encode the TMA descriptor for the echo array [P*E][Ns] of 8-byte samples, box = one window
+// row.  Returns false (cp.async fallback) when the layout does not meet TMA's rules: 16-B
+// aligned base and row pitch (Ns even), box <= 256 samples.
+bool encode_tma(sas_bp_t h) {
+  const char* no = getenv("SASBP_NO_TMA");
+  if (no && no[0] == '1') return false;
+  const int box = sasbp::box_samples(h->W);
+  if ((h->Ns & 1) || box > 256 || (((uintptr_t)h->echoes) & 15)) return false;
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return false;
+    encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)h->Ns, (cuuint64_t)h->P * (cuuint64_t)h->E};
+  cuuint64_t strides[1] = {(cuuint64_t)h->Ns * 8};
+  cuuint32_t boxd[2] = {(cuuint32_t)box, 1};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode(reinterpret_cast<CUtensorMap*>(&h->tmap), CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, (void*)h->echoes,
+                      dims, strides, boxd, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
 }
 
 cudaError_t launch_tdbp(sas_bp_t h, float2* image, unsigned long long* counter, int accumulate,
@@ -149,9 +194,9 @@ cudaError_t launch_tdbp(sas_bp_t h, float2* image, unsigned long long* counter, 
   prm.W = h->W;
   prm.accumulate = accumulate;
   switch (h->variant) {
-    case V2D: return launch_variant<4, 2, 1, 4, 1, false>(prm, h->mode, count, st);
-    case V2D_DZ: return launch_variant<4, 2, 1, 4, 1, true>(prm, h->mode, count, st);
-    default: return launch_variant<2, 2, 2, 1, 4, true>(prm, h->mode, count, st);
+    case V2D: return launch_variant<4, 2, 1, 4, 1, false>(prm, h->tmap, h->use_tma, h->mode, count, st);
+    case V2D_DZ: return launch_variant<4, 2, 1, 4, 1, true>(prm, h->tmap, h->use_tma, h->mode, count, st);
+    default: return launch_variant<2, 2, 2, 1, 4, true>(prm, h->tmap, h->use_tma, h->mode, count, st);
   }
 }
 
@@ -333,6 +378,7 @@ sas_status sas_bp_set_pings(sas_bp_t h, const float* echoes, int32_t P, int32_t 
   st = upload_geo(h, P, E, Ns, tx, rx, t0, h->stream);  // synchronises the stream
   if (st != SAS_OK) { h->has_pings = false; return st; }
   h->echoes = h->echoes_owned;
+  h->use_tma = encode_tma(h);
   h->has_pings = true;
   return SAS_OK;
 }
@@ -351,6 +397,7 @@ sas_status sas_bp_set_pings_device(sas_bp_t h, const void* echoes_dev, int32_t P
   st = upload_geo(h, P, E, Ns, tx, rx, t0, s);
   if (st != SAS_OK) { h->has_pings = false; return st; }
   h->echoes = (const float2*)echoes_dev;
+  h->use_tma = encode_tma(h);
   h->has_pings = true;
   return SAS_OK;
 }
@@ -403,5 +450,16 @@ sas_status sas_bp_count_terms(sas_bp_t h, uint64_t* dense, uint64_t* in_win) {
 }
 
 size_t sas_bp_workspace_bytes(sas_bp_t h) { return h ? h->bytes : 0; }
+
+sas_status sas_bp_get_plan(sas_bp_t h, sas_bp_plan* out) {
+  g_err[0] = 0;
+  if (!h || !out) return fail(SAS_E_INVALID, "NULL argument");
+  out->tile[0] = h->TX; out->tile[1] = h->TY; out->tile[2] = h->TZ;
+  out->window = h->W;
+  out->rx_mode = h->has_pings ? h->mode : -1;
+  out->tma = h->has_pings ? (h->use_tma ? 1 : 0) : -1;
+  out->batch = sasbp::kNB;
+  return SAS_OK;
+}
 
 }  // extern "C"

@@ -33,8 +33,7 @@
 namespace sasbp {
 
 constexpr int kThreads = 128;   // 4 warps
-constexpr int kNB = 32;         // channels per batch
-constexpr int kChPerWarp = kNB / (kThreads / 32);
+constexpr int kNB = 16;         // channels per batch
 
 // receive-leg evaluation modes
 constexpr int kSeries3 = 0;     // 3-term series in eps
@@ -117,10 +116,11 @@ __device__ __forceinline__ ChanConst chan_prologue(const TdbpParams& prm, int ch
   ph -= floor(ph);
   ChanConst k;
   k.ux2 = (float)(2.0 * urx); k.uy2 = (float)(2.0 * ury); k.uz2 = (float)(2.0 * urz);
-  const double ir = 1.0 / r_r;
-  k.ir2 = (float)(ir * ir);
-  const double g = K * ir;   // (sqrt(1+e)-1)/e = 1/2 - e/8 + e^2/16 - 5e^3/128 + ...
-  k.a0 = (float)(0.5 * g); k.a1 = (float)(-0.125 * g); k.a2 = (float)(0.0625 * g); k.a3 = (float)(-0.0390625 * g);
+  // series coefficients only need fp32 relative accuracy
+  const float ir = 1.0f / (float)r_r;
+  k.ir2 = ir * ir;
+  const float g = (float)K * ir;   // (sqrt(1+e)-1)/e = 1/2 - e/8 + e^2/16 - 5e^3/128 + ...
+  k.a0 = 0.5f * g; k.a1 = -0.125f * g; k.a2 = 0.0625f * g; k.a3 = -0.0390625f * g;
   k.urr = (float)urr;
   k.phi0 = (float)(6.283185307179586 * ph);
   k.r_r = (float)r_r; k.r2_r = (float)(r_r * r_r);
@@ -172,30 +172,60 @@ struct TileMap {
   }
 };
 
-// shared-memory layout of K2 (bytes): cc[2][kNB] | raw[kNB][W+1] float2 (16-B padded) | win[kNB][W] float4
-__host__ __device__ inline size_t raw_stride(int W) { return (size_t)((W + 1 + 1) & ~1); }  // float2 units, even
-__host__ __device__ inline size_t k2_smem_bytes(int W) {
-  return 2 * kNB * sizeof(ChanConst) + (size_t)kNB * raw_stride(W) * sizeof(float2) + (size_t)kNB * W * sizeof(float4);
+// shared-memory layout of K2 (bytes):
+//   cc[2][kNB] ChanConst | mbarrier (16 B) | raw[kNB] slots of RS bytes (128-B aligned, TMA
+//   destinations) | win[kNB][W] float4 (intercept, slope) cells
+__host__ __device__ inline int box_samples(int W) { return (W + 1 + 1) & ~1; }      // even => 16-B rows
+__host__ __device__ inline size_t raw_slot_bytes(int W) { return ((size_t)box_samples(W) * 8 + 127) & ~(size_t)127; }
+__host__ __device__ inline size_t k2_raw_off() { return (2 * kNB * sizeof(ChanConst) + 16 + 127) & ~(size_t)127; }
+__host__ __device__ inline size_t k2_win_off(int W) { return k2_raw_off() + kNB * raw_slot_bytes(W); }
+__host__ __device__ inline size_t k2_smem_bytes(int W) { return k2_win_off(W) + (size_t)kNB * W * sizeof(float4) + 128; }
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(bar), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void tma_load_row(uint32_t dst, const void* tmap, int x, int y, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+      ::"r"(dst), "l"(tmap), "r"(x), "r"(y), "r"(bar) : "memory");
 }
 
-template <int KX, int KY, int KZ, int WY, int WZ, bool HAS_DZ, int MODE>
-__global__ void __launch_bounds__(kThreads, 3) tdbp_kernel(const TdbpParams prm) {
+// TMA descriptor of the echo array seen as a 2D tensor of 8-byte samples [P*E][Ns] (inner dim
+// Ns); box = box_samples(W) x 1; out-of-bounds samples read as zero (reading R2).
+struct __align__(64) TmaDesc { unsigned char bytes[128]; };
+
+template <int KX, int KY, int KZ, int WY, int WZ, bool HAS_DZ, int MODE, bool USE_TMA>
+__global__ void __launch_bounds__(kThreads, 4) tdbp_kernel(const TdbpParams prm, const __grid_constant__ TmaDesc tmap) {
   using TM = TileMap<KX, KY, KZ, WY, WZ>;
   constexpr int NP = TM::NP;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  ChanConst* cc = reinterpret_cast<ChanConst*>(smem_raw);                       // [2][kNB]
-  float2* raw = reinterpret_cast<float2*>(smem_raw + 2 * kNB * sizeof(ChanConst));
-  const size_t rs = raw_stride(prm.W);
-  float4* win = reinterpret_cast<float4*>(reinterpret_cast<unsigned char*>(raw) + kNB * rs * sizeof(float2));
+  constexpr int kWarps = kThreads / 32;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  // the dynamic smem base is only guaranteed 16-B aligned: align it to 128 B ourselves
+  unsigned char* sbase = smem_raw + ((128 - ((uint32_t)__cvta_generic_to_shared(smem_raw) & 127)) & 127);
+  ChanConst* cc = reinterpret_cast<ChanConst*>(sbase);                       // [2][kNB]
+  const uint32_t bar = (uint32_t)__cvta_generic_to_shared(sbase + 2 * kNB * sizeof(ChanConst));
+  const int W = prm.W;
+  const uint32_t rsb = (uint32_t)raw_slot_bytes(W);
+  unsigned char* rawp = sbase + k2_raw_off();
+  float4* win = reinterpret_cast<float4*>(sbase + k2_win_off(W));
   const uint32_t win_base = (uint32_t)__cvta_generic_to_shared(win);
-  const uint32_t raw_base = (uint32_t)__cvta_generic_to_shared(raw);
+  const uint32_t raw_base = (uint32_t)__cvta_generic_to_shared(rawp);
 
   const TM tm(prm);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double ct[3];
   tm.centre(prm, ct);
 
-  // per-pixel-pair offsets from the tile centre and accumulators
   float2 DX[NP], DY[NP], DZ[NP], DD[NP], BT[NP];
   float2 A[2 * NP], B[2 * NP];
 #pragma unroll
@@ -212,42 +242,57 @@ __global__ void __launch_bounds__(kThreads, 3) tdbp_kernel(const TdbpParams prm)
 
   const float kph = (float)(6.283185307179586 * prm.fc / prm.fs);
   const int nch = prm.P * prm.E;
-  const int W = prm.W;
   const int nbatch = (nch + kNB - 1) / kNB;
+  const int Wh = W >> 1;
+  const int nbox = box_samples(W);
 
-  // stage batch b: prologue for this warp's channels, then cp.async of their raw windows
+  if (USE_TMA && tid == 0) {
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  // producer (one warp): fp64 prologue of batch b's channels, then their window loads
   auto issue = [&](int b) {
     const int ch0 = b * kNB;
     const int nb = min(kNB, nch - ch0);
     ChanConst* cb = cc + (b & 1) * kNB;
-    const int c_lo = warp * kChPerWarp;
-    if (lane < kChPerWarp && c_lo + lane < nb) cb[c_lo + lane] = chan_prologue(prm, ch0 + c_lo + lane, ct, c_lo + lane, win_base);
-    __syncwarp();
-    const int cnt = W + 1;
-    for (int c = c_lo; c < c_lo + kChPerWarp && c < nb; ++c) {
-      const int klo = cb[c].klo;
-      const float2* row = prm.echoes + (size_t)(ch0 + c) * prm.Ns;
-      const uint32_t dst = raw_base + (uint32_t)(c * rs) * 8u;
-      for (int j = lane; j < cnt; j += 32) {
-        const int n = klo + j;
-        const bool ok = (n >= 0) && (n < prm.Ns);
-        cp_async8(dst + 8u * j, ok ? (const void*)(row + n) : (const void*)row, ok);
-      }
+    ChanConst kc;
+    if (lane < nb) {
+      kc = chan_prologue(prm, ch0 + lane, ct, lane, win_base);
+      cb[lane] = kc;
     }
-    cp_async_commit();
+    if (USE_TMA) {
+      if (lane == 0) mbar_expect_tx(bar, (uint32_t)(nb * nbox * 8));
+      __syncwarp();
+      if (lane < nb) tma_load_row(raw_base + lane * rsb, &tmap, kc.klo, ch0 + lane, bar);
+    } else {
+      __syncwarp();
+      for (int c = 0; c < nb; ++c) {
+        const int klo = cb[c].klo;
+        const float2* row = prm.echoes + (size_t)(ch0 + c) * prm.Ns;
+        const uint32_t dst = raw_base + c * rsb;
+        for (int j = lane; j < nbox; j += 32) {
+          const int n = klo + j;
+          const bool ok = (n >= 0) && (n < prm.Ns);
+          cp_async8(dst + 8u * j, ok ? (const void*)(row + n) : (const void*)row, ok);
+        }
+      }
+      cp_async_commit();
+    }
   };
 
-  issue(0);
+  if (warp == 0) issue(0);
   int cur_ping = -1;
-  const int Wh = W >> 1;
 
   for (int b = 0; b < nbatch; ++b) {
     const int nb = min(kNB, nch - b * kNB);
-    cp_async_wait_all();
-    __syncthreads();   // every warp's raw(b) landed; compute(b-1) is done with win
-    // each warp rewrites the raw windows it staged as (intercept, slope) cells
-    for (int c = warp * kChPerWarp; c < warp * kChPerWarp + kChPerWarp && c < nb; ++c) {
-      const float2* rw = raw + c * rs;
+    if (USE_TMA) mbar_wait(bar, (uint32_t)(b & 1));
+    else cp_async_wait_all();
+    __syncthreads();   // raw(b) landed; every warp is done with win(b-1)
+    // rewrite raw windows as (intercept, slope) cells; warp w owns channels w, w+4, ...
+    for (int c = warp; c < nb; c += kWarps) {
+      const float2* rw = reinterpret_cast<const float2*>(rawp + c * rsb);
       float4* wc = win + c * W;
       for (int j = lane; j < W; j += 32) {
         const float2 d0 = rw[j], d1 = rw[j + 1];
@@ -256,8 +301,8 @@ __global__ void __launch_bounds__(kThreads, 3) tdbp_kernel(const TdbpParams prm)
         wc[j] = make_float4(fmaf(-jj, sr, 0.5f * (d0.x + d1.x)), fmaf(-jj, si, 0.5f * (d0.y + d1.y)), sr, si);
       }
     }
-    __syncthreads();   // win(b) complete
-    if (b + 1 < nbatch) issue(b + 1);
+    __syncthreads();   // win(b) complete; raw free
+    if (b + 1 < nbatch && warp == ((b + 1) & (kWarps - 1))) issue(b + 1);
     const ChanConst* cb = cc + (b & 1) * kNB;
 
 #pragma unroll 1

@@ -22,13 +22,18 @@ _NAMES = {0: "SAS_OK", -1: "SAS_E_INVALID", -2: "SAS_E_STATE", -3: "SAS_E_NOMEM"
 
 EXPORTS = ("sas_bp_create", "sas_bp_destroy", "sas_bp_set_pings", "sas_bp_set_pings_device", "sas_bp_form",
            "sas_bp_form_device", "sas_bp_count_terms", "sas_bp_workspace_bytes", "sas_rangecompress",
-           "sas_rangecompress_device", "sas_last_error", "sas_version")
+           "sas_rangecompress_device", "sas_last_error", "sas_version", "sas_bp_get_plan")
 
 
 class SasError(RuntimeError):
     def __init__(self, status: int, msg: str):
         super().__init__(f"{_NAMES.get(status, status)}: {msg}")
         self.status = status
+
+
+class sas_bp_plan(ctypes.Structure):
+    _fields_ = [("tile", ctypes.c_int32 * 3), ("window", ctypes.c_int32), ("rx_mode", ctypes.c_int32),
+                ("tma", ctypes.c_int32), ("batch", ctypes.c_int32)]
 
 
 class sas_grid(ctypes.Structure):
@@ -63,6 +68,7 @@ def load_library(path: str = LIB_PATH):
         "sas_rangecompress_device": ([vp, i32, i32, i32, vp, i32, vp, vp], ctypes.c_int),
         "sas_last_error": ([], ctypes.c_char_p),
         "sas_version": ([], ctypes.c_char_p),
+        "sas_bp_get_plan": ([vp, ctypes.POINTER(sas_bp_plan)], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -216,6 +222,13 @@ class Backprojector:
         d, w = ctypes.c_uint64(), ctypes.c_uint64()
         _check(_lib.sas_bp_count_terms(self._h, ctypes.byref(d), ctypes.byref(w)))
         return int(d.value), int(w.value)
+
+    def plan(self) -> dict:
+        """The execution plan (tile, window, rx_mode, tma, batch) -- sas_bp_get_plan."""
+        p = sas_bp_plan()
+        _check(_lib.sas_bp_get_plan(self._h, ctypes.byref(p)))
+        return {"tile": tuple(p.tile), "window": p.window, "rx_mode": ("series3", "series4", "exact")[p.rx_mode]
+                if p.rx_mode >= 0 else None, "tma": None if p.tma < 0 else bool(p.tma), "batch": p.batch}
 
     @property
     def workspace_bytes(self) -> int:

@@ -287,3 +287,36 @@ def test_parity_full_size_sampled(bpmod, cid):
     pk = _peak_pixels(s, lambda c: oracle.tdbp_grid(e, s.tx, s.rx, s.t0, s.fc, s.fs, s.c, s.grid, idx=c), win=1)
     pref = oracle.tdbp_grid(e, s.tx, s.rx, s.t0, s.fc, s.fs, s.c, s.grid, idx=pk)
     _check(g, ref, _at(got, pk), pref, label=f"cfg{cid} full")
+
+
+# ------------------------------------------------------------------ plan selection and staging paths
+
+def test_plan_selection(bpmod):
+    """Far-field stripmap uses the 3-term series and TMA staging; near field the exact leg."""
+    s = synth.scenario(2, reduced=True)
+    with bpmod.Backprojector(s.fc, s.bandwidth, s.fs, s.c, s.grid) as bp:
+        bp.set_pings(s.echoes(), s.tx, s.rx, s.t0)
+        pl = bp.plan()
+    assert pl["tile"] == (32, 32, 1) and pl["tma"] is True and pl["rx_mode"] == "series3", pl
+    s4 = synth.scenario(4, reduced=True)
+    with bpmod.Backprojector(s4.fc, s4.bandwidth, s4.fs, s4.c, s4.grid) as bp:
+        bp.set_pings(s4.echoes(), s4.tx + [0, 0, 1.8], s4.rx + [0, 0, 1.8], s4.t0 - 3.6 / s4.c)
+        assert bp.plan()["rx_mode"] == "exact"
+
+
+@pytest.mark.parametrize("how", ["env", "odd_ns"])
+def test_cp_async_fallback_path(bpmod, how, monkeypatch):
+    """The cp.async staging fallback (odd Ns, or SASBP_NO_TMA=1) gives the same images."""
+    s = synth.scenario(2, reduced=True)
+    e = s.echoes()
+    if how == "odd_ns":
+        e = np.ascontiguousarray(e[:, :, :-1])
+    else:
+        monkeypatch.setenv("SASBP_NO_TMA", "1")
+    with bpmod.Backprojector(s.fc, s.bandwidth, s.fs, s.c, s.grid) as bp:
+        bp.set_pings(e, s.tx, s.rx, s.t0)
+        assert bp.plan()["tma"] is False
+        got = bp.form()
+    ref = oracle.tdbp_grid(e, s.tx, s.rx, s.t0, s.fc, s.fs, s.c, s.grid)
+    pk = s.target_pixels
+    _check(got, ref, _at(got, pk), _at(ref, pk), label=f"cp.async {how}")
