@@ -324,7 +324,7 @@ sas_status sas_bp_create(double fc, double bandwidth, double fs, double c, const
     h->d_max = best;
   }
   h->hw = 2.0 * h->d_max * fs / c;
-  h->W = (int)std::ceil(2.0 * h->hw + 4.0) + 2;
+  h->W = (int)std::ceil(2.0 * h->hw + 4.0) + 3;  // + 1 cell for the even (TMA-aligned) window start
   if (smem_bytes(h->W) > 200 * 1024) {
     delete h;
     return fail(SAS_E_UNSUPPORTED, "tile window of %d samples does not fit shared memory (pixel step too large for fs)", 0);

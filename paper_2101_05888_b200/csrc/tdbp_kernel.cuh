@@ -107,7 +107,9 @@ __device__ __forceinline__ ChanConst chan_prologue(const TdbpParams& prm, int ch
   const double K = prm.fs / prm.c;
   const double Uref = (r_t + r_r) * K - prm.t0[p] * prm.fs;   // absolute sample index at tile centre
   const double klo_d = floor(Uref - prm.hw) - 2.0;
-  const int klo = (int)fmax(fmin(klo_d, 2.0e9), -2.0e9);
+  // even window start: a TMA box must start 16-B aligned (2 samples); the plan's W has one
+  // spare cell for this
+  const int klo = ((int)fmax(fmin(klo_d, 2.0e9), -2.0e9)) & ~1;
   const int Wh = prm.W >> 1;
   // window coordinate U = u - k_lo - 0.5 - Wh, so cell j = rn(U) + Wh
   const double urr = Uref - (double)klo - 0.5 - (double)Wh;
@@ -257,17 +259,15 @@ __global__ void __launch_bounds__(kThreads, 4) tdbp_kernel(const TdbpParams prm,
     const int ch0 = b * kNB;
     const int nb = min(kNB, nch - ch0);
     ChanConst* cb = cc + (b & 1) * kNB;
-    ChanConst kc;
-    if (lane < nb) {
-      kc = chan_prologue(prm, ch0 + lane, ct, lane, win_base);
-      cb[lane] = kc;
-    }
+    if (lane < nb) cb[lane] = chan_prologue(prm, ch0 + lane, ct, lane, win_base);
+    __syncwarp();
     if (USE_TMA) {
-      if (lane == 0) mbar_expect_tx(bar, (uint32_t)(nb * nbox * 8));
-      __syncwarp();
-      if (lane < nb) tma_load_row(raw_base + lane * rsb, &tmap, kc.klo, ch0 + lane, bar);
+      // one elected thread arms the barrier with the byte count and issues every row load
+      if (lane == 0) {
+        mbar_expect_tx(bar, (uint32_t)(nb * nbox * 8));
+        for (int c = 0; c < nb; ++c) tma_load_row(raw_base + c * rsb, &tmap, cb[c].klo, ch0 + c, bar);
+      }
     } else {
-      __syncwarp();
       for (int c = 0; c < nb; ++c) {
         const int klo = cb[c].klo;
         const float2* row = prm.echoes + (size_t)(ch0 + c) * prm.Ns;
