@@ -187,6 +187,7 @@ cudaError_t launch_tdbp(sas_bp_t h, float2* image, unsigned long long* counter, 
     prm.sz[a] = h->grid.step_z[a];
   }
   prm.fc = h->fc; prm.fs = h->fs; prm.c = h->c;
+  prm.k_s = h->fs / h->c; prm.k_c = h->fc / h->c; prm.k_r = h->fc / h->fs; prm.inv_e = 1.0 / h->E;
   prm.hw = h->hw;
   prm.P = h->P; prm.E = h->E; prm.Ns = h->Ns;
   prm.nx = h->grid.nx; prm.ny = h->grid.ny; prm.nz = h->grid.nz;

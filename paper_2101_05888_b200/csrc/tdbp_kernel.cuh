@@ -49,6 +49,10 @@ struct TdbpParams {
   unsigned long long* counter;  // K3: in-window term total
   double origin[3], sx[3], sy[3], sz[3];
   double fc, fs, c;
+  double k_s;             // fs / c   (samples per metre of path)
+  double k_c;             // fc / c   (carrier cycles per metre of path)
+  double k_r;             // fc / fs  (carrier cycles per sample)
+  double inv_e;           // 1 / E
   double hw;              // half window in samples: 2 * d_max * fs / c
   int P, E, Ns;
   int nx, ny, nz;
@@ -97,37 +101,36 @@ __device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
 // fp64 prologue for one channel (row a2): reference geometry at the tile centre ct.
 __device__ __forceinline__ ChanConst chan_prologue(const TdbpParams& prm, int ch, const double ct[3], int slot,
                                                    uint32_t win_base) {
-  const int p = ch / prm.E;
+  const int p = (int)(((double)ch + 0.5) * prm.inv_e);   // ch / E, exact for ch < 2^40
   const double* T = prm.tx + 3 * p;
   const double* R = prm.rx + 3 * (size_t)ch;
   const double utx = ct[0] - T[0], uty = ct[1] - T[1], utz = ct[2] - T[2];
   const double urx = ct[0] - R[0], ury = ct[1] - R[1], urz = ct[2] - R[2];
   const double r_t = sqrt(utx * utx + uty * uty + utz * utz);
   const double r_r = sqrt(urx * urx + ury * ury + urz * urz);
-  const double K = prm.fs / prm.c;
-  const double Uref = (r_t + r_r) * K - prm.t0[p] * prm.fs;   // absolute sample index at tile centre
+  const double S = r_t + r_r;
+  const double Uref = fma(S, prm.k_s, -prm.t0[p] * prm.fs);   // absolute sample index at tile centre
   const double klo_d = floor(Uref - prm.hw) - 2.0;
   // even window start: a TMA box must start 16-B aligned (2 samples); the plan's W has one
   // spare cell for this
   const int klo = ((int)fmax(fmin(klo_d, 2.0e9), -2.0e9)) & ~1;
   const int Wh = prm.W >> 1;
   // window coordinate U = u - k_lo - 0.5 - Wh, so cell j = rn(U) + Wh
-  const double urr = Uref - (double)klo - 0.5 - (double)Wh;
-  const double cyc = prm.fc * (r_t + r_r) / prm.c;            // reference phase, cycles (fp64)
-  double ph = cyc - urr * (prm.fc / prm.fs);                   // phase at U = 0
+  const double urr = Uref - (double)(klo + Wh) - 0.5;
+  double ph = fma(-urr, prm.k_r, S * prm.k_c);                // reference phase (cycles) at U = 0
   ph -= floor(ph);
   ChanConst k;
   k.ux2 = (float)(2.0 * urx); k.uy2 = (float)(2.0 * ury); k.uz2 = (float)(2.0 * urz);
   // series coefficients only need fp32 relative accuracy
   const float ir = 1.0f / (float)r_r;
   k.ir2 = ir * ir;
-  const float g = (float)K * ir;   // (sqrt(1+e)-1)/e = 1/2 - e/8 + e^2/16 - 5e^3/128 + ...
+  const float g = (float)prm.k_s * ir;   // (sqrt(1+e)-1)/e = 1/2 - e/8 + e^2/16 - 5e^3/128 + ...
   k.a0 = 0.5f * g; k.a1 = -0.125f * g; k.a2 = 0.0625f * g; k.a3 = -0.0390625f * g;
   k.urr = (float)urr;
   k.phi0 = (float)(6.283185307179586 * ph);
   k.r_r = (float)r_r; k.r2_r = (float)(r_r * r_r);
   k.tx2x = (float)(2.0 * utx); k.tx2y = (float)(2.0 * uty); k.tx2z = (float)(2.0 * utz);
-  k.r2_t = (float)(r_t * r_t); k.r_t = (float)r_t; k.kfs = (float)K;
+  k.r2_t = (float)(r_t * r_t); k.r_t = (float)r_t; k.kfs = (float)prm.k_s;
   k.klo_f = (float)klo; k.pad1 = 0.f;
   k.ping = p;
   k.woff = (int)(win_base + (uint32_t)(slot * prm.W + Wh) * 16u - (uint32_t)kMagicBits * 16u);
@@ -242,33 +245,38 @@ __global__ void __launch_bounds__(kThreads, 4) tdbp_kernel(const TdbpParams prm,
     A[2 * p] = f2(0.f); A[2 * p + 1] = f2(0.f); B[2 * p] = f2(0.f); B[2 * p + 1] = f2(0.f);
   }
 
-  const float kph = (float)(6.283185307179586 * prm.fc / prm.fs);
+  const float kph = (float)(6.283185307179586 * prm.k_r);
   const int nch = prm.P * prm.E;
   const int nbatch = (nch + kNB - 1) / kNB;
   const int Wh = W >> 1;
   const int nbox = box_samples(W);
 
   if (USE_TMA && tid == 0) {
-    mbar_init(bar, 1);
+    mbar_init(bar, kWarps);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
 
-  // producer (one warp): fp64 prologue of batch b's channels, then their window loads
+  // producer work is spread over the warps: warp w runs the fp64 prologue of channels
+  // [w*kCW, (w+1)*kCW) of batch b and issues their window loads; every warp arrives once on
+  // the batch's mbarrier (with the byte count of its rows) so the phase completes when all
+  // rows have landed.
+  constexpr int kCW = kNB / kWarps;
   auto issue = [&](int b) {
     const int ch0 = b * kNB;
     const int nb = min(kNB, nch - ch0);
     ChanConst* cb = cc + (b & 1) * kNB;
-    if (lane < nb) cb[lane] = chan_prologue(prm, ch0 + lane, ct, lane, win_base);
+    const int c0 = warp * kCW;
+    const int mine = max(0, min(kCW, nb - c0));
+    if (lane < mine) cb[c0 + lane] = chan_prologue(prm, ch0 + c0 + lane, ct, c0 + lane, win_base);
     __syncwarp();
     if (USE_TMA) {
-      // one elected thread arms the barrier with the byte count and issues every row load
       if (lane == 0) {
-        mbar_expect_tx(bar, (uint32_t)(nb * nbox * 8));
-        for (int c = 0; c < nb; ++c) tma_load_row(raw_base + c * rsb, &tmap, cb[c].klo, ch0 + c, bar);
+        mbar_expect_tx(bar, (uint32_t)(mine * nbox * 8));
+        for (int c = c0; c < c0 + mine; ++c) tma_load_row(raw_base + c * rsb, &tmap, cb[c].klo, ch0 + c, bar);
       }
     } else {
-      for (int c = 0; c < nb; ++c) {
+      for (int c = c0; c < c0 + mine; ++c) {
         const int klo = cb[c].klo;
         const float2* row = prm.echoes + (size_t)(ch0 + c) * prm.Ns;
         const uint32_t dst = raw_base + c * rsb;
@@ -282,7 +290,7 @@ __global__ void __launch_bounds__(kThreads, 4) tdbp_kernel(const TdbpParams prm,
     }
   };
 
-  if (warp == 0) issue(0);
+  issue(0);
   int cur_ping = -1;
 
   for (int b = 0; b < nbatch; ++b) {
@@ -290,7 +298,7 @@ __global__ void __launch_bounds__(kThreads, 4) tdbp_kernel(const TdbpParams prm,
     if (USE_TMA) mbar_wait(bar, (uint32_t)(b & 1));
     else cp_async_wait_all();
     __syncthreads();   // raw(b) landed; every warp is done with win(b-1)
-    // rewrite raw windows as (intercept, slope) cells; warp w owns channels w, w+4, ...
+    // rewrite raw windows as (intercept, slope) cells (any warp -> any channel)
     for (int c = warp; c < nb; c += kWarps) {
       const float2* rw = reinterpret_cast<const float2*>(rawp + c * rsb);
       float4* wc = win + c * W;
@@ -302,7 +310,7 @@ __global__ void __launch_bounds__(kThreads, 4) tdbp_kernel(const TdbpParams prm,
       }
     }
     __syncthreads();   // win(b) complete; raw free
-    if (b + 1 < nbatch && warp == ((b + 1) & (kWarps - 1))) issue(b + 1);
+    if (b + 1 < nbatch) issue(b + 1);
     const ChanConst* cb = cc + (b & 1) * kNB;
 
 #pragma unroll 1
