@@ -6,8 +6,9 @@ independently"; images add over pings):
 
 * image-shard (default): rank r owns a contiguous band of grid rows (iy for 2D, iz for 3D) and
   forms it from ALL pings; the echoes are broadcast once from rank 0 over NVLink (the
-  north star's "ping data broadcast once"), the bands are gathered to rank 0.  Output is
-  bitwise identical to one GPU: every pixel sees the same channels in the same order.
+  north star's "ping data broadcast once"), the bands are gathered to rank 0.  Every pixel
+  sees the same channels in the same order as on one GPU; the only difference is the fp64
+  rounding of the shifted band origin (~1e-13 m), i.e. ~1e-7 relative in the image.
 * ping-shard: rank r forms the full grid from pings r::G; the partial images are summed to
   rank 0 with an NCCL reduce.  Output differs from one GPU only by fp32 summation order.
 
@@ -81,7 +82,7 @@ def form_image_sharded(grid: Dict, echoes, tx, rx, t0, former: Former, dist, dev
             part[:, : hi - lo] = img
     # all_gather is supported by both NCCL and gloo; only rank 0 keeps the result
     bufs = [torch.empty_like(part) for _ in range(world)]
-    dist.all_gather(bufs, part)
+    dist.all_gather([torch.view_as_real(b) for b in bufs], torch.view_as_real(part))
     if rank != 0:
         return None
     gathered = bufs
