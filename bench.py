@@ -116,11 +116,12 @@ def cpu_oracle_rate(s, echoes, seconds: float, seed: int = 123):
     def sample(n):
         return np.stack([rng.integers(0, g["nx"], n), rng.integers(0, g["ny"], n), rng.integers(0, g["nz"], n)], 1)
 
-    probe = sample(64)
+    oracle.tdbp_grid(echoes, s.tx, s.rx, s.t0, s.fc, s.fs, s.c, g, idx=sample(16))  # load + thread pool
+    probe = sample(512)
     t = time.perf_counter()
     oracle.tdbp_grid(echoes, s.tx, s.rx, s.t0, s.fc, s.fs, s.c, g, idx=probe)
     dt = max(time.perf_counter() - t, 1e-6)
-    n = int(max(64, min(1 << 20, 64 * seconds / dt)))
+    n = int(max(512, min(1 << 21, 512 * seconds / dt)))
     idx = sample(n)
     t = time.perf_counter()
     oracle.tdbp_grid(echoes, s.tx, s.rx, s.t0, s.fc, s.fs, s.c, g, idx=idx)
@@ -304,7 +305,7 @@ def run_sasbp(args):
 
     if rank == 0:
         traffic = None
-        prof = os.path.join(ROOT, "profiles", "ncu_tdbp_summary.json")
+        prof = os.path.join(ROOT, "profiles", "ncu_tdbp_latest.json")
         if os.path.exists(prof):
             try:
                 with open(prof) as f:
@@ -324,7 +325,11 @@ def run_sasbp(args):
                        "l2": f"inputs larger than L2 ({P * E * Ns * 8 / 1e9:.2f} GB echoes)"},
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": UNIT, "frac": achieved / peak,
                          "traffic": traffic,
-                         "peak_basis": f"{sms} SMs x 1965 MHz x min(128/F, 16/S), F=20+6/E, S=3+1/E, E={E}"},
+                         "algorithmic_bytes": P * E * Ns * 8 + g["nx"] * g["ny"] * g["nz"] * 8,
+                         "peak_basis": f"{sms} SMs x 1965 MHz x min(128/F, 16/S), F=20+6/E, S=3+1/E, E={E} "
+                                       "(FP32/SFU roofline of the direct per-term formula, BASELINE.md)",
+                         "peak_sfu_2mufu": sms * 1.965e9 * 8 / 1e9,
+                         "frac_sfu_2mufu": achieved / (sms * 1.965e9 * 8 / 1e9)},
             "clocks": clk.summary(),
             "gpu_launches": args.steps,
             "e2e": e2e,
