@@ -45,6 +45,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-k1", action="store_true")
     return ap.parse_args()
 
 
@@ -130,6 +131,14 @@ def cpu_oracle_rate(s, echoes, seconds: float, seed: int = 123):
     return {"value": terms / dt / 1e9, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
             "sample": f"{n} seeded-random pixels of config {s.name} x all {s.P} pings x {s.E} elements "
                       f"({terms:.3e} terms, {dt:.1f} s, fp64 C + OpenMP)"}
+
+
+def _measured_hbm():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
 
 
 def host_cpu_model():
@@ -298,6 +307,34 @@ def run_sasbp(args):
                    "d2h_bytes_per_step": g["nx"] * g["ny"] * g["nz"] * 8, "ms_per_step": e2e_s * 1e3,
                    "api": "pinned H2D on rank 0 + NCCL broadcast + sas_bp_form_device per band + all_gather + D2H"}
 
+    # ---- K1 range compression on the same channel layout (row a1), reported separately
+    k1 = None
+    if not args.no_k1 and rank == 0:
+        fsr, Br, Tp = s.fs, s.bandwidth, 5e-3
+        nr = int(round(Tp * fsr))
+        tt = np.arange(nr) / fsr - Tp / 2
+        rep = np.exp(1j * np.pi * (Br / Tp) * tt ** 2).astype(np.complex64)
+        rep_d = torch.from_numpy(rep / np.float32(np.sqrt(nr))).to(dev)
+        out_d = torch.empty_like(echoes_d)
+        for _ in range(2):
+            pkg.rangecompress_device(echoes_d, rep_d, out_d, stream=stream)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        nrep = 5
+        e0.record(stream)
+        for _ in range(nrep):
+            pkg.rangecompress_device(echoes_d, rep_d, out_d, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        k1_ms = e0.elapsed_time(e1) / nrep
+        k1_bytes = 16 * P * E * Ns
+        hbm = _measured_hbm()
+        k1 = {"kernel": "rc_fft_kernel (overlap-save, L=4096)", "Nr": nr, "ms": k1_ms,
+              "achieved": k1_bytes / (k1_ms * 1e-3) / 1e9, "unit": "GB/s", "bound": "hbm", "peak": hbm[0],
+              "peak_source": hbm[1], "frac": k1_bytes / (k1_ms * 1e-3) / 1e9 / hbm[0],
+              "algorithmic_bytes": k1_bytes, "note": "16 B per sample: read raw + write compressed once"}
+        del out_d
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_oracle_rate(s, echoes_h, args.cpu_seconds)
@@ -334,6 +371,7 @@ def run_sasbp(args):
             "gpu_launches": args.steps,
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "k1_rangecompress": k1,
         }
         if cpu:
             out["gpu_over_cpu"] = value / cpu["value"]

@@ -2,18 +2,29 @@
 // presumes compressed data; reading R14 in DESIGN.md):
 //   out[ch][n] = sum_{m=0}^{Nr-1} raw[ch][n+m] * conj(replica[m]),  raw zero past Ns.
 //
-// v0 design: direct correlation in shared memory (FP32 complex MAC), one CTA per
-// (1024-output chunk, channel).  The replica and the chunk's input span (1024 + Nr - 1
-// samples) are staged once in shared memory; each thread produces 4 outputs strided by 256
-// so shared loads are conflict-free.  FFT-domain overlap-save is the planned HBM-bound
-// replacement (K1).
+// FFT overlap-save path (Nr <= 2048): per CTA one block of L = 4096 input samples of one channel
+// -> forward FFT -> times H[k] = conj(R[k]) / L (R = FFT of the zero-padded replica, one
+// prep launch per call) -> inverse FFT -> the V = L - Nr + 1 alias-free outputs.  The FFT is a
+// radix-16 Stockham in shared memory: 256 threads each own one 16-point butterfly per pass,
+// 3 passes per transform; the first forward pass reads global memory directly, the last forward
+// pass hands its registers straight to the first inverse pass (the spectrum product needs no
+// reordering), the last inverse pass writes global memory; smem indices are padded by one
+// complex per 16 so every pass is bank-conflict free.  Twiddles come from a 4096-entry table
+// computed in double precision.  HBM traffic: the block inputs (L / V of the channel) + outputs.
+//
+// Direct path (2048 < Nr <= 8192): correlation in shared memory (FP32 complex MAC).
 #include "sasbp.h"
 
 #include <cstdarg>
 #include <cstdio>
+#include <mutex>
 #include <cuda_runtime.h>
 
+extern "C" void sasbp_set_error(const char* msg);  // sasbp.cu: the thread-local sas_last_error buffer
+
 namespace {
+
+// ---------------------------------------------------------------- direct correlation
 
 constexpr int kRcThreads = 256;
 constexpr int kRcOut = 4;                         // outputs per thread
@@ -63,28 +74,233 @@ __global__ void __launch_bounds__(kRcThreads) rc_direct_kernel(const float2* __r
   }
 }
 
-}  // namespace
+// ---------------------------------------------------------------- FFT overlap-save
 
-extern "C" void sasbp_set_error(const char* msg);  // sasbp.cu: the thread-local sas_last_error buffer
+constexpr int kL = 4096;          // FFT length
+constexpr int kFT = 256;          // threads (one radix-16 butterfly each per pass)
+constexpr int kPad = kL + kL / 16;
 
-namespace {
+__device__ __forceinline__ int pad(int i) { return i + (i >> 4); }
+
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+}
+
+// radix-4 DFT in place; INV selects exp(+i) kernels
+template <bool INV>
+__device__ __forceinline__ void dft4(float2& x0, float2& x1, float2& x2, float2& x3) {
+  const float2 t0 = make_float2(x0.x + x2.x, x0.y + x2.y), t1 = make_float2(x0.x - x2.x, x0.y - x2.y);
+  const float2 t2 = make_float2(x1.x + x3.x, x1.y + x3.y);
+  const float2 d = make_float2(x1.x - x3.x, x1.y - x3.y);
+  const float2 t3 = INV ? make_float2(-d.y, d.x) : make_float2(d.y, -d.x);   // (+/- i) * d
+  x0 = make_float2(t0.x + t2.x, t0.y + t2.y);
+  x2 = make_float2(t0.x - t2.x, t0.y - t2.y);
+  x1 = make_float2(t1.x + t3.x, t1.y + t3.y);
+  x3 = make_float2(t1.x - t3.x, t1.y - t3.y);
+}
+
+// 16-point DFT in registers (natural order in and out): n = 4a + b, k = c + 4d
+template <bool INV>
+__device__ __forceinline__ void dft16(float2 v[16]) {
+  const float s = INV ? 1.f : -1.f;
+  // step 1: radix-4 over a for each b
+#pragma unroll
+  for (int b = 0; b < 4; ++b) dft4<INV>(v[b], v[4 + b], v[8 + b], v[12 + b]);
+  // now v[4c + b] = Y[b][c]; step 2: twiddle W16^{bc}
+  const float c1 = 0.92387953251128674f, s1 = 0.38268343236508978f, r2 = 0.70710678118654752f;
+  const float2 w[10] = {make_float2(1.f, 0.f), make_float2(c1, s * s1), make_float2(r2, s * r2), make_float2(s1, s * c1),
+                        make_float2(0.f, s * 1.f), make_float2(-s1, s * c1), make_float2(-r2, s * r2), make_float2(-c1, s * s1),
+                        make_float2(-1.f, 0.f), make_float2(-c1, -s * s1)};
+#pragma unroll
+  for (int b = 1; b < 4; ++b)
+#pragma unroll
+    for (int c = 1; c < 4; ++c) v[4 * c + b] = cmul(v[4 * c + b], w[b * c]);
+  // step 3: radix-4 over b for each c: X[c + 4d]
+#pragma unroll
+  for (int c = 0; c < 4; ++c) dft4<INV>(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+  // now v[4c + d] = X[c + 4d]: transpose to natural order
+  float2 t[16];
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+#pragma unroll
+    for (int d = 0; d < 4; ++d) t[c + 4 * d] = v[4 * c + d];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = t[i];
+}
+
+// one Stockham pass (after the registers were loaded): twiddle, DFT16, store to smem
+template <bool INV, int NS>
+__device__ __forceinline__ void pass_store(float2 v[16], float2* sm, const float2* __restrict__ tw, int j) {
+  const int k = j & (NS - 1);
+  if (NS > 1) {
+#pragma unroll
+    for (int r = 1; r < 16; ++r) {
+      float2 w = __ldg(tw + ((r * k * (256 / NS)) & (kL - 1)));
+      if (INV) w.y = -w.y;
+      v[r] = cmul(v[r], w);
+    }
+  }
+  dft16<INV>(v);
+  const int base = (j - k) * 16 + k;
+#pragma unroll
+  for (int r = 0; r < 16; ++r) sm[pad(base + r * NS)] = v[r];
+}
+
+template <bool INV, int NS>
+__device__ __forceinline__ void pass_regs(float2 v[16], const float2* __restrict__ tw, int j) {
+  const int k = j & (NS - 1);
+#pragma unroll
+  for (int r = 1; r < 16; ++r) {
+    float2 w = __ldg(tw + ((r * k * (256 / NS)) & (kL - 1)));
+    if (INV) w.y = -w.y;
+    v[r] = cmul(v[r], w);
+  }
+  dft16<INV>(v);
+}
+
+__device__ __forceinline__ void load_smem(float2 v[16], const float2* sm, int j) {
+#pragma unroll
+  for (int r = 0; r < 16; ++r) v[r] = sm[pad(j + r * kFT)];
+}
+
+// forward FFT of x[n0 .. n0+L) (zero past Ns), result left in registers: v[r] = X[j + 256 r]
+__device__ __forceinline__ void fft_forward(float2 v[16], const float2* __restrict__ x, int n0, int Ns, float2* sm,
+                                            const float2* __restrict__ tw, int j) {
+#pragma unroll
+  for (int r = 0; r < 16; ++r) {
+    const int n = n0 + j + r * kFT;
+    v[r] = (n < Ns) ? __ldg(x + n) : make_float2(0.f, 0.f);
+  }
+  pass_store<false, 1>(v, sm, tw, j);
+  __syncthreads();
+  load_smem(v, sm, j);
+  __syncthreads();
+  pass_store<false, 16>(v, sm, tw, j);
+  __syncthreads();
+  load_smem(v, sm, j);
+  pass_regs<false, 256>(v, tw, j);
+}
+
+__global__ void __launch_bounds__(kFT) rc_twiddle_kernel(float2* tw) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m < kL) {
+    double s, c;
+    sincospi(-2.0 * m / kL, &s, &c);
+    tw[m] = make_float2((float)c, (float)s);
+  }
+}
+
+// H[k] = conj(FFT_L(replica zero padded))[k] / L, stored in natural order
+__global__ void __launch_bounds__(kFT) rc_prep_kernel(const float2* __restrict__ rep, int Nr, const float2* __restrict__ tw,
+                                                      float2* __restrict__ H) {
+  __shared__ float2 sm[kPad];
+  const int j = threadIdx.x;
+  float2 v[16];
+  fft_forward(v, rep, 0, Nr, sm, tw, j);
+  const float sc = 1.0f / kL;
+#pragma unroll
+  for (int r = 0; r < 16; ++r) H[j + r * kFT] = make_float2(v[r].x * sc, -v[r].y * sc);
+}
+
+__global__ void __launch_bounds__(kFT, 2) rc_fft_kernel(const float2* __restrict__ raw, int Ns, int V,
+                                                        const float2* __restrict__ H, const float2* __restrict__ tw,
+                                                        float2* __restrict__ out) {
+  __shared__ float2 sm[kPad];
+  const int j = threadIdx.x;
+  const size_t ch = blockIdx.y;
+  const int n0 = blockIdx.x * V;
+  const float2* x = raw + ch * Ns;
+  float2 v[16];
+  fft_forward(v, x, n0, Ns, sm, tw, j);
+  // spectrum product in registers (v[r] holds bin j + 256 r)
+#pragma unroll
+  for (int r = 0; r < 16; ++r) v[r] = cmul(v[r], __ldg(H + j + r * kFT));
+  // inverse FFT: its first pass consumes exactly this register layout
+  __syncthreads();
+  pass_store<true, 1>(v, sm, tw, j);
+  __syncthreads();
+  load_smem(v, sm, j);
+  __syncthreads();
+  pass_store<true, 16>(v, sm, tw, j);
+  __syncthreads();
+  load_smem(v, sm, j);
+  pass_regs<true, 256>(v, tw, j);
+  float2* y = out + ch * Ns;
+#pragma unroll
+  for (int r = 0; r < 16; ++r) {
+    const int i = j + r * kFT;
+    const int n = n0 + i;
+    if (i < V && n < Ns) y[n] = v[r];
+  }
+}
+
 sas_status rc_cuda_fail(const char* what, cudaError_t e) {
   char buf[256];
   snprintf(buf, sizeof(buf), "%s: %s", what, cudaGetErrorString(e));
   sasbp_set_error(buf);
   return SAS_E_CUDA;
 }
+
+// per-device twiddle table, built once
+std::mutex g_tw_mu;
+float2* g_tw[64] = {nullptr};
+
+sas_status twiddles(float2** out, cudaStream_t st) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return rc_cuda_fail("cudaGetDevice", e);
+  if (dev < 0 || dev >= 64) { sasbp_set_error("device index out of range"); return SAS_E_UNSUPPORTED; }
+  std::lock_guard<std::mutex> lk(g_tw_mu);
+  if (!g_tw[dev]) {
+    float2* t = nullptr;
+    e = cudaMalloc(&t, kL * sizeof(float2));
+    if (e != cudaSuccess) { sasbp_set_error("cudaMalloc(twiddles) failed"); return SAS_E_NOMEM; }
+    rc_twiddle_kernel<<<kL / kFT, kFT, 0, st>>>(t);
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) { cudaFree(t); return rc_cuda_fail("rc_twiddle_kernel", e); }
+    g_tw[dev] = t;
+  }
+  *out = g_tw[dev];
+  return SAS_OK;
+}
+
 }  // namespace
 
-static sas_status rc_launch(const float2* raw, int32_t P, int32_t E, int32_t Ns, const float2* rep, int32_t Nr,
-                            float2* out, cudaStream_t st) {
+static sas_status rc_launch_direct(const float2* raw, long nch, int32_t Ns, const float2* rep, int32_t Nr, float2* out,
+                                   cudaStream_t st) {
   const size_t smem = sizeof(float2) * ((size_t)Nr + kRcTile + Nr - 1);
   cudaError_t e = cudaFuncSetAttribute(rc_direct_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return rc_cuda_fail("cudaFuncSetAttribute(rc_direct_kernel)", e);
-  dim3 grid((Ns + kRcTile - 1) / kRcTile, (unsigned)P * E);
-  rc_direct_kernel<<<grid, kRcThreads, smem, st>>>(raw, Ns, rep, Nr, out);
+  for (long c0 = 0; c0 < nch; c0 += 65535) {
+    const unsigned n = (unsigned)((nch - c0) < 65535 ? (nch - c0) : 65535);
+    dim3 grid((Ns + kRcTile - 1) / kRcTile, n);
+    rc_direct_kernel<<<grid, kRcThreads, smem, st>>>(raw + c0 * Ns, Ns, rep, Nr, out + c0 * Ns);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return rc_cuda_fail("rc_direct_kernel launch", e);
+  }
+  return SAS_OK;
+}
+
+static sas_status rc_launch_fft(const float2* raw, long nch, int32_t Ns, const float2* rep, int32_t Nr, float2* out,
+                                cudaStream_t st) {
+  float2* tw = nullptr;
+  sas_status s = twiddles(&tw, st);
+  if (s != SAS_OK) return s;
+  float2* H = nullptr;
+  cudaError_t e = cudaMallocAsync(&H, kL * sizeof(float2), st);
+  if (e != cudaSuccess) return rc_cuda_fail("cudaMallocAsync(H)", e);
+  rc_prep_kernel<<<1, kFT, 0, st>>>(rep, Nr, tw, H);
   e = cudaGetLastError();
-  if (e != cudaSuccess) return rc_cuda_fail("rc_direct_kernel launch", e);
+  const int V = kL - Nr + 1;
+  const unsigned blocks = (unsigned)((Ns + V - 1) / V);
+  for (long c0 = 0; c0 < nch && e == cudaSuccess; c0 += 65535) {
+    const unsigned n = (unsigned)((nch - c0) < 65535 ? (nch - c0) : 65535);
+    rc_fft_kernel<<<dim3(blocks, n), kFT, 0, st>>>(raw + c0 * Ns, Ns, V, H, tw, out + c0 * Ns);
+    e = cudaGetLastError();
+  }
+  cudaFreeAsync(H, st);
+  if (e != cudaSuccess) return rc_cuda_fail("rc_fft_kernel launch", e);
   return SAS_OK;
 }
 
@@ -94,10 +310,10 @@ static sas_status rc_check(int32_t P, int32_t E, int32_t Ns, int32_t Nr) {
     return SAS_E_INVALID;
   }
   if (Nr > kRcMaxNr) {
-    sasbp_set_error("replica longer than 8192 samples is not supported by the direct kernel");
+    sasbp_set_error("replica longer than 8192 samples is not supported");
     return SAS_E_UNSUPPORTED;
   }
-  if ((long double)P * E > 65535.0L * 65535.0L) { sasbp_set_error("too many channels"); return SAS_E_INVALID; }
+  if ((long double)P * E * Ns > 9.0e15L) { sasbp_set_error("P*E*Ns too large"); return SAS_E_INVALID; }
   return SAS_OK;
 }
 
@@ -107,19 +323,13 @@ extern "C" sas_status sas_rangecompress_device(const void* raw_dev, int32_t P, i
   sas_status s = rc_check(P, E, Ns, Nr);
   if (s != SAS_OK) return s;
   if (!raw_dev || !replica_dev || !out_dev) { sasbp_set_error("NULL pointer"); return SAS_E_INVALID; }
-  if ((long)P * E > 65535) {
-    // grid.y limit: split channel ranges
-    const long nch = (long)P * E;
-    for (long c0 = 0; c0 < nch; c0 += 65535) {
-      int n = (int)((nch - c0) < 65535 ? (nch - c0) : 65535);
-      s = rc_launch((const float2*)raw_dev + c0 * Ns, n, 1, Ns, (const float2*)replica_dev, Nr,
-                    (float2*)out_dev + c0 * Ns, (cudaStream_t)cuda_stream);
-      if (s != SAS_OK) return s;
-    }
-    return SAS_OK;
-  }
-  return rc_launch((const float2*)raw_dev, P, E, Ns, (const float2*)replica_dev, Nr, (float2*)out_dev,
-                   (cudaStream_t)cuda_stream);
+  const long nch = (long)P * E;
+  const char* force = getenv("SASBP_RC_DIRECT");
+  if (Nr <= kL / 2 && !(force && force[0] == '1'))
+    return rc_launch_fft((const float2*)raw_dev, nch, Ns, (const float2*)replica_dev, Nr, (float2*)out_dev,
+                         (cudaStream_t)cuda_stream);
+  return rc_launch_direct((const float2*)raw_dev, nch, Ns, (const float2*)replica_dev, Nr, (float2*)out_dev,
+                          (cudaStream_t)cuda_stream);
 }
 
 extern "C" sas_status sas_rangecompress(const float* raw, int32_t P, int32_t E, int32_t Ns, const float* replica,
@@ -150,6 +360,7 @@ extern "C" sas_status sas_rangecompress(const float* raw, int32_t P, int32_t E, 
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) rs = rc_cuda_fail("D2H copy", e);
   }
+  cudaStreamSynchronize(st);
   cudaFree(draw); cudaFree(dout); cudaFree(drep);
   cudaStreamDestroy(st);
   return rs;
