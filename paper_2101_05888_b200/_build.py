@@ -26,18 +26,28 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str = None, defines=()) -> str:
+    """Build libsasbp.so (or an A/B variant at `out` with extra -D defines)."""
+    target = out or LIB
+    if out is None and not force and not _stale():
         return LIB
-    tmp = LIB + f".tmp{os.getpid()}"
+    tmp = target + f".tmp{os.getpid()}"
     cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
            "-Xcompiler", "-fvisibility=hidden", "-cudart", "static", "-I", os.path.join(ROOT, "include"),
-           "-Xptxas", "-v" if verbose else "-O3", "-o", tmp, *sources()]
+           "-Xptxas", "-v" if verbose else "-O3", *[f"-D{d}" for d in defines], "-o", tmp, *sources()]
     subprocess.check_call(cmd)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":
     import sys
-    print(build(force=True, verbose="-v" in sys.argv))
+    args = [a for a in sys.argv[1:] if a != "-v"]
+    out = None
+    defs = []
+    for a in args:
+        if a.startswith("-D"):
+            defs.append(a[2:])
+        elif a.startswith("--out="):
+            out = a[len("--out="):]
+    print(build(force=True, verbose="-v" in sys.argv, out=out, defines=defs))

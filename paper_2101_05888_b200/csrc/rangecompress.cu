@@ -99,14 +99,18 @@ __device__ __forceinline__ void dft4(float2& x0, float2& x1, float2& x2, float2&
   x3 = make_float2(t1.x - t3.x, t1.y - t3.y);
 }
 
-// 16-point DFT in registers (natural order in and out): n = 4a + b, k = c + 4d
-template <bool INV>
+// base-4 digit reversal of a 16-point index: sigma(4a + b) = 4b + a (an involution)
+__host__ __device__ constexpr int sig(int n) { return 4 * (n & 3) + (n >> 2); }
+
+// 16-point DFT in registers, n = 4a + b, k = c + 4d, no data movement: input element n is read
+// from slot PIN ? sig(n) : n and output element k is left in slot PIN ? k : sig(k).
+template <bool INV, bool PIN>
 __device__ __forceinline__ void dft16(float2 v[16]) {
   const float s = INV ? 1.f : -1.f;
-  // step 1: radix-4 over a for each b
+#define SL(n) (PIN ? sig(n) : (n))
 #pragma unroll
-  for (int b = 0; b < 4; ++b) dft4<INV>(v[b], v[4 + b], v[8 + b], v[12 + b]);
-  // now v[4c + b] = Y[b][c]; step 2: twiddle W16^{bc}
+  for (int b = 0; b < 4; ++b) dft4<INV>(v[SL(b)], v[SL(4 + b)], v[SL(8 + b)], v[SL(12 + b)]);
+  // slot SL(4c + b) = Y[b][c]; twiddle W16^{bc}
   const float c1 = 0.92387953251128674f, s1 = 0.38268343236508978f, r2 = 0.70710678118654752f;
   const float2 w[10] = {make_float2(1.f, 0.f), make_float2(c1, s * s1), make_float2(r2, s * r2), make_float2(s1, s * c1),
                         make_float2(0.f, s * 1.f), make_float2(-s1, s * c1), make_float2(-r2, s * r2), make_float2(-c1, s * s1),
@@ -114,21 +118,14 @@ __device__ __forceinline__ void dft16(float2 v[16]) {
 #pragma unroll
   for (int b = 1; b < 4; ++b)
 #pragma unroll
-    for (int c = 1; c < 4; ++c) v[4 * c + b] = cmul(v[4 * c + b], w[b * c]);
-  // step 3: radix-4 over b for each c: X[c + 4d]
+    for (int c = 1; c < 4; ++c) v[SL(4 * c + b)] = cmul(v[SL(4 * c + b)], w[b * c]);
+  // radix-4 over b: X[c + 4d] lands in slot SL(4c + d) = PIN ? (c + 4d) : sig(c + 4d)
 #pragma unroll
-  for (int c = 0; c < 4; ++c) dft4<INV>(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
-  // now v[4c + d] = X[c + 4d]: transpose to natural order
-  float2 t[16];
-#pragma unroll
-  for (int c = 0; c < 4; ++c)
-#pragma unroll
-    for (int d = 0; d < 4; ++d) t[c + 4 * d] = v[4 * c + d];
-#pragma unroll
-  for (int i = 0; i < 16; ++i) v[i] = t[i];
+  for (int c = 0; c < 4; ++c) dft4<INV>(v[SL(4 * c)], v[SL(4 * c + 1)], v[SL(4 * c + 2)], v[SL(4 * c + 3)]);
+#undef SL
 }
 
-// one Stockham pass (after the registers were loaded): twiddle, DFT16, store to smem
+// one Stockham pass on natural-order registers: twiddle, DFT16 (output left in sig order), store
 template <bool INV, int NS>
 __device__ __forceinline__ void pass_store(float2 v[16], float2* sm, const float2* __restrict__ tw, int j) {
   const int k = j & (NS - 1);
@@ -140,12 +137,13 @@ __device__ __forceinline__ void pass_store(float2 v[16], float2* sm, const float
       v[r] = cmul(v[r], w);
     }
   }
-  dft16<INV>(v);
+  dft16<INV, false>(v);
   const int base = (j - k) * 16 + k;
 #pragma unroll
-  for (int r = 0; r < 16; ++r) sm[pad(base + r * NS)] = v[r];
+  for (int r = 0; r < 16; ++r) sm[pad(base + r * NS)] = v[sig(r)];
 }
 
+// last pass of a transform: result left in registers, element r in slot sig(r)
 template <bool INV, int NS>
 __device__ __forceinline__ void pass_regs(float2 v[16], const float2* __restrict__ tw, int j) {
   const int k = j & (NS - 1);
@@ -155,7 +153,7 @@ __device__ __forceinline__ void pass_regs(float2 v[16], const float2* __restrict
     if (INV) w.y = -w.y;
     v[r] = cmul(v[r], w);
   }
-  dft16<INV>(v);
+  dft16<INV, false>(v);
 }
 
 __device__ __forceinline__ void load_smem(float2 v[16], const float2* sm, int j) {
@@ -163,7 +161,7 @@ __device__ __forceinline__ void load_smem(float2 v[16], const float2* sm, int j)
   for (int r = 0; r < 16; ++r) v[r] = sm[pad(j + r * kFT)];
 }
 
-// forward FFT of x[n0 .. n0+L) (zero past Ns), result left in registers: v[r] = X[j + 256 r]
+// forward FFT of x[n0 .. n0+L) (zero past Ns); bin j + 256 r is left in slot sig(r)
 __device__ __forceinline__ void fft_forward(float2 v[16], const float2* __restrict__ x, int n0, int Ns, float2* sm,
                                             const float2* __restrict__ tw, int j) {
 #pragma unroll
@@ -199,10 +197,10 @@ __global__ void __launch_bounds__(kFT) rc_prep_kernel(const float2* __restrict__
   fft_forward(v, rep, 0, Nr, sm, tw, j);
   const float sc = 1.0f / kL;
 #pragma unroll
-  for (int r = 0; r < 16; ++r) H[j + r * kFT] = make_float2(v[r].x * sc, -v[r].y * sc);
+  for (int r = 0; r < 16; ++r) H[j + r * kFT] = make_float2(v[sig(r)].x * sc, -v[sig(r)].y * sc);
 }
 
-__global__ void __launch_bounds__(kFT, 2) rc_fft_kernel(const float2* __restrict__ raw, int Ns, int V,
+__global__ void __launch_bounds__(kFT, 1) rc_fft_kernel(const float2* __restrict__ raw, int Ns, int V,
                                                         const float2* __restrict__ H, const float2* __restrict__ tw,
                                                         float2* __restrict__ out) {
   __shared__ float2 sm[kPad];
@@ -212,12 +210,14 @@ __global__ void __launch_bounds__(kFT, 2) rc_fft_kernel(const float2* __restrict
   const float2* x = raw + ch * Ns;
   float2 v[16];
   fft_forward(v, x, n0, Ns, sm, tw, j);
-  // spectrum product in registers (v[r] holds bin j + 256 r)
+  // spectrum product in registers (slot sig(r) holds bin j + 256 r)
 #pragma unroll
-  for (int r = 0; r < 16; ++r) v[r] = cmul(v[r], __ldg(H + j + r * kFT));
-  // inverse FFT: its first pass consumes exactly this register layout
+  for (int r = 0; r < 16; ++r) v[sig(r)] = cmul(v[sig(r)], __ldg(H + j + r * kFT));
+  // inverse FFT: its first pass (no twiddles) reads this very layout (PIN: input r in slot sig(r))
+  dft16<true, true>(v);
   __syncthreads();
-  pass_store<true, 1>(v, sm, tw, j);
+#pragma unroll
+  for (int r = 0; r < 16; ++r) sm[pad(j * 16 + r)] = v[r];
   __syncthreads();
   load_smem(v, sm, j);
   __syncthreads();
@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(kFT, 2) rc_fft_kernel(const float2* __restrict
   for (int r = 0; r < 16; ++r) {
     const int i = j + r * kFT;
     const int n = n0 + i;
-    if (i < V && n < Ns) y[n] = v[r];
+    if (i < V && n < Ns) y[n] = v[sig(r)];
   }
 }
 

@@ -19,6 +19,13 @@
 
 #include "tdbp_kernel.cuh"
 
+#ifndef SASBP_K4
+#define SASBP_K4 0
+#endif
+#ifndef SASBP_AXIS
+#define SASBP_AXIS 0
+#endif
+
 namespace {
 
 thread_local char g_err[512] = "";
@@ -110,13 +117,14 @@ double dist_to_box(const double* p, const double lo[3], const double hi[3]) {
 }
 
 template <typename Kern>
-cudaError_t launch_k(Kern kern, const sasbp::TdbpParams& prm, const sasbp::TmaDesc& tmap, size_t smem, cudaStream_t st) {
+cudaError_t launch_k(Kern kern, int threads, const sasbp::TdbpParams& prm, const sasbp::TmaDesc& tmap, size_t smem,
+                     cudaStream_t st) {
   const unsigned blocks = (unsigned)prm.tiles_x * prm.tiles_y * prm.tiles_z;
   if (smem > 0) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  kern<<<blocks, sasbp::kThreads, smem, st>>>(prm, tmap);
+  kern<<<blocks, threads, smem, st>>>(prm, tmap);
   return cudaGetLastError();
 }
 
@@ -124,10 +132,24 @@ template <int KX, int KY, int KZ, int WY, int WZ, bool DZ, bool TMA>
 cudaError_t launch_mode(const sasbp::TdbpParams& prm, const sasbp::TmaDesc& tmap, int mode, cudaStream_t st) {
   using namespace sasbp;
   const size_t smem = smem_bytes(prm.W);
+  const int nt = 32 * WY * WZ;
+  // axis-aligned plane: step_x along x only and step_y with no x/z part -> x-pairs share dy
+  const bool axis = !DZ && KZ == 1 && prm.sx[1] == 0.0 && prm.sx[2] == 0.0 && prm.sy[2] == 0.0;
+#if SASBP_AXIS
+  if (axis) {
+    switch (mode) {
+      case kSeries3: return launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kSeries3, TMA, true>, nt, prm, tmap, smem, st);
+      case kSeries4: return launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kSeries4, TMA, true>, nt, prm, tmap, smem, st);
+      default: return launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kExact, TMA, true>, nt, prm, tmap, smem, st);
+    }
+  }
+#else
+  (void)axis;
+#endif
   switch (mode) {
-    case kSeries3: return launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kSeries3, TMA>, prm, tmap, smem, st);
-    case kSeries4: return launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kSeries4, TMA>, prm, tmap, smem, st);
-    default: return launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kExact, TMA>, prm, tmap, smem, st);
+    case kSeries3: return launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kSeries3, TMA>, nt, prm, tmap, smem, st);
+    case kSeries4: return launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kSeries4, TMA>, nt, prm, tmap, smem, st);
+    default: return launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kExact, TMA>, nt, prm, tmap, smem, st);
   }
 }
 
@@ -137,7 +159,7 @@ cudaError_t launch_variant(const sasbp::TdbpParams& prm, const sasbp::TmaDesc& t
   using namespace sasbp;
   if (count) {
     const unsigned blocks = (unsigned)prm.tiles_x * prm.tiles_y * prm.tiles_z;
-    count_kernel<KX, KY, KZ, WY, WZ><<<blocks, kThreads, 0, st>>>(prm);
+    count_kernel<KX, KY, KZ, WY, WZ><<<blocks, 32 * WY * WZ, 0, st>>>(prm);
     return cudaGetLastError();
   }
   return tma ? launch_mode<KX, KY, KZ, WY, WZ, DZ, true>(prm, tmap, mode, st)
@@ -195,8 +217,13 @@ cudaError_t launch_tdbp(sas_bp_t h, float2* image, unsigned long long* counter, 
   prm.W = h->W;
   prm.accumulate = accumulate;
   switch (h->variant) {
-    case V2D: return launch_variant<4, 2, 1, 4, 1, false>(prm, h->tmap, h->use_tma, h->mode, count, st);
-    case V2D_DZ: return launch_variant<4, 2, 1, 4, 1, true>(prm, h->tmap, h->use_tma, h->mode, count, st);
+#if SASBP_K4
+    case V2D: return launch_variant<4, 1, 1, 8, 1, false>(prm, h->tmap, h->use_tma, h->mode, count, st);
+    case V2D_DZ: return launch_variant<4, 1, 1, 8, 1, true>(prm, h->tmap, h->use_tma, h->mode, count, st);
+#else
+    case V2D: return launch_variant<4, 2, 1, SASBP_WY2D, 1, false>(prm, h->tmap, h->use_tma, h->mode, count, st);
+    case V2D_DZ: return launch_variant<4, 2, 1, SASBP_WY2D, 1, true>(prm, h->tmap, h->use_tma, h->mode, count, st);
+#endif
     default: return launch_variant<2, 2, 2, 1, 4, true>(prm, h->tmap, h->use_tma, h->mode, count, st);
   }
 }
@@ -306,7 +333,7 @@ sas_status sas_bp_create(double fc, double bandwidth, double fs, double c, const
   h->fc = fc; h->bandwidth = bandwidth; h->fs = fs; h->c = c;
   h->grid = g;
   const bool flat_z = (g.nz == 1) && g.step_x[2] == 0.0 && g.step_y[2] == 0.0;
-  if (g.nz == 1) { h->variant = flat_z ? V2D : V2D_DZ; h->TX = 32; h->TY = 32; h->TZ = 1; }
+  if (g.nz == 1) { h->variant = flat_z ? V2D : V2D_DZ; h->TX = 32; h->TY = 8 * SASBP_WY2D; h->TZ = 1; }
   else { h->variant = V3D; h->TX = 16; h->TY = 8; h->TZ = 8; }
   h->tiles_x = (g.nx + h->TX - 1) / h->TX;
   h->tiles_y = (g.ny + h->TY - 1) / h->TY;

@@ -30,10 +30,22 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#ifndef SASBP_FLAT_TRANSFORM
+#define SASBP_FLAT_TRANSFORM 0
+#endif
+#ifndef SASBP_WY2D
+#define SASBP_WY2D 4   // warps per 2D CTA (tile = 32 x 8*SASBP_WY2D pixels)
+#endif
+
 namespace sasbp {
 
-constexpr int kThreads = 128;   // 4 warps
-constexpr int kNB = 16;         // channels per batch
+#ifndef SASBP_MINB
+#define SASBP_MINB 4   // resident 4-warp CTAs per SM the register allocation targets
+#endif
+#ifndef SASBP_NB
+#define SASBP_NB 16
+#endif
+constexpr int kNB = SASBP_NB;   // channels per batch
 
 // receive-leg evaluation modes
 constexpr int kSeries3 = 0;     // 3-term series in eps
@@ -209,11 +221,14 @@ __device__ __forceinline__ void tma_load_row(uint32_t dst, const void* tmap, int
 // Ns); box = box_samples(W) x 1; out-of-bounds samples read as zero (reading R2).
 struct __align__(64) TmaDesc { unsigned char bytes[128]; };
 
-template <int KX, int KY, int KZ, int WY, int WZ, bool HAS_DZ, int MODE, bool USE_TMA>
-__global__ void __launch_bounds__(kThreads, 4) tdbp_kernel(const TdbpParams prm, const __grid_constant__ TmaDesc tmap) {
+// HAS_DZ = false means the grid is a z-level plane (step_x, step_y have no z component); then
+// both pixels of an x-pair share their y offset whenever step_x has no y component (AXIS).
+template <int KX, int KY, int KZ, int WY, int WZ, bool HAS_DZ, int MODE, bool USE_TMA, bool AXIS = false>
+__global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp_kernel(const TdbpParams prm,
+                                                                          const __grid_constant__ TmaDesc tmap) {
   using TM = TileMap<KX, KY, KZ, WY, WZ>;
   constexpr int NP = TM::NP;
-  constexpr int kWarps = kThreads / 32;
+  constexpr int kWarps = WY * WZ;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   // the dynamic smem base is only guaranteed 16-B aligned: align it to 128 B ourselves
   unsigned char* sbase = smem_raw + ((128 - ((uint32_t)__cvta_generic_to_shared(smem_raw) & 127)) & 127);
@@ -232,6 +247,7 @@ __global__ void __launch_bounds__(kThreads, 4) tdbp_kernel(const TdbpParams prm,
   tm.centre(prm, ct);
 
   float2 DX[NP], DY[NP], DZ[NP], DD[NP], BT[NP];
+  float DYS[NP];
   float2 A[2 * NP], B[2 * NP];
 #pragma unroll
   for (int p = 0; p < NP; ++p) {
@@ -240,6 +256,7 @@ __global__ void __launch_bounds__(kThreads, 4) tdbp_kernel(const TdbpParams prm,
     tm.offset(prm, 2 * p + 1, dx1, dy1, dz1);
     if (!HAS_DZ) { dz0 = 0.f; dz1 = 0.f; }
     DX[p] = make_float2(dx0, dx1); DY[p] = make_float2(dy0, dy1); DZ[p] = make_float2(dz0, dz1);
+    DYS[p] = dy0;
     DD[p] = make_float2(dx0 * dx0 + dy0 * dy0 + dz0 * dz0, dx1 * dx1 + dy1 * dy1 + dz1 * dz1);
     BT[p] = f2(0.f);
     A[2 * p] = f2(0.f); A[2 * p + 1] = f2(0.f); B[2 * p] = f2(0.f); B[2 * p + 1] = f2(0.f);
@@ -250,6 +267,9 @@ __global__ void __launch_bounds__(kThreads, 4) tdbp_kernel(const TdbpParams prm,
   const int nbatch = (nch + kNB - 1) / kNB;
   const int Wh = W >> 1;
   const int nbox = box_samples(W);
+#if SASBP_FLAT_TRANSFORM
+  const float inv_w = 1.0f / (float)W;
+#endif
 
   if (USE_TMA && tid == 0) {
     mbar_init(bar, kWarps);
@@ -298,17 +318,35 @@ __global__ void __launch_bounds__(kThreads, 4) tdbp_kernel(const TdbpParams prm,
     if (USE_TMA) mbar_wait(bar, (uint32_t)(b & 1));
     else cp_async_wait_all();
     __syncthreads();   // raw(b) landed; every warp is done with win(b-1)
-    // rewrite raw windows as (intercept, slope) cells (any warp -> any channel)
+    // rewrite raw windows as (intercept, slope) cells; cell j serves u in [k_lo+j, k_lo+j+1]:
+    //   slope = d1 - d0,  intercept = d0 + (0.5 - (j - Wh)) * slope   (ehat = intercept + U slope)
+#if SASBP_FLAT_TRANSFORM
+    {  // warp w takes channels w, w+kWarps, ...; flattened over (channel, cell)
+      const int nmine = (nb - warp + kWarps - 1) / kWarps;
+      const int tot = nmine * W;
+      for (int i = lane; i < tot; i += 32) {
+        const int q = (int)(((float)i + 0.5f) * inv_w);   // i / W (exact: i < 2^20)
+        const int j = i - q * W;
+        const int c = warp + q * kWarps;
+        const float2* rw = reinterpret_cast<const float2*>(rawp + c * rsb);
+        const float2 d0 = rw[j], d1 = rw[j + 1];
+        const float2 sl = __fadd2_rn(d1, make_float2(-d0.x, -d0.y));
+        const float2 ic = __ffma2_rn(sl, f2(0.5f - (float)(j - Wh)), d0);
+        win[c * W + j] = make_float4(ic.x, ic.y, sl.x, sl.y);
+      }
+    }
+#else
     for (int c = warp; c < nb; c += kWarps) {
       const float2* rw = reinterpret_cast<const float2*>(rawp + c * rsb);
       float4* wc = win + c * W;
       for (int j = lane; j < W; j += 32) {
         const float2 d0 = rw[j], d1 = rw[j + 1];
-        const float sr = d1.x - d0.x, si = d1.y - d0.y;
-        const float jj = (float)(j - Wh);
-        wc[j] = make_float4(fmaf(-jj, sr, 0.5f * (d0.x + d1.x)), fmaf(-jj, si, 0.5f * (d0.y + d1.y)), sr, si);
+        const float2 sl = __fadd2_rn(d1, make_float2(-d0.x, -d0.y));
+        const float2 ic = __ffma2_rn(sl, f2(0.5f - (float)(j - Wh)), d0);
+        wc[j] = make_float4(ic.x, ic.y, sl.x, sl.y);
       }
     }
+#endif
     __syncthreads();   // win(b) complete; raw free
     if (b + 1 < nbatch) issue(b + 1);
     const ChanConst* cb = cc + (b & 1) * kNB;
@@ -321,7 +359,7 @@ __global__ void __launch_bounds__(kThreads, 4) tdbp_kernel(const TdbpParams prm,
         // transmit leg, exact range-relative form: dR = q / (sqrt(r^2 + q) + r), in samples
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
-          float2 q = __ffma2_rn(f2(kc.tx2y), DY[p], DD[p]);
+          float2 q = __ffma2_rn(f2(kc.tx2y), AXIS ? f2(DYS[p]) : DY[p], DD[p]);
           q = __ffma2_rn(f2(kc.tx2x), DX[p], q);
           if (HAS_DZ) q = __ffma2_rn(f2(kc.tx2z), DZ[p], q);
           const float2 r2 = __fadd2_rn(q, f2(kc.r2_t));
@@ -332,7 +370,7 @@ __global__ void __launch_bounds__(kThreads, 4) tdbp_kernel(const TdbpParams prm,
       }
 #pragma unroll
       for (int p = 0; p < NP; ++p) {
-        float2 q = __ffma2_rn(f2(kc.uy2), DY[p], DD[p]);
+        float2 q = __ffma2_rn(f2(kc.uy2), AXIS ? f2(DYS[p]) : DY[p], DD[p]);
         q = __ffma2_rn(f2(kc.ux2), DX[p], q);
         if (HAS_DZ) q = __ffma2_rn(f2(kc.uz2), DZ[p], q);
         float2 U;
@@ -387,7 +425,7 @@ __global__ void __launch_bounds__(kThreads, 4) tdbp_kernel(const TdbpParams prm,
 // K3: count terms whose interpolation support meets the record, u in (-1, Ns).
 // Same tiles and fp32 delay arithmetic as K2 (exact leg form), no echo traffic.
 template <int KX, int KY, int KZ, int WY, int WZ>
-__global__ void __launch_bounds__(kThreads) count_kernel(const TdbpParams prm) {
+__global__ void __launch_bounds__(32 * WY * WZ) count_kernel(const TdbpParams prm) {
   using TM = TileMap<KX, KY, KZ, WY, WZ>;
   constexpr int K = TM::K;
   __shared__ ChanConst cc[kNB];

@@ -45,11 +45,13 @@ class sas_grid(ctypes.Structure):
 _lib = None
 
 
-def load_library(path: str = LIB_PATH):
-    """Load libsasbp.so (raises OSError loudly if it was not built)."""
+def load_library(path: Optional[str] = None):
+    """Load libsasbp.so (raises OSError loudly if it was not built).  SASBP_LIB overrides the
+    path (A/B builds of the same library)."""
     global _lib
     if _lib is not None:
         return _lib
+    path = path or os.environ.get("SASBP_LIB") or LIB_PATH
     if not os.path.exists(path):
         raise OSError(f"libsasbp.so not built at {path}; run __graft_entry__.build()")
     lib = ctypes.CDLL(path)
