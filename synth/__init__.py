@@ -128,6 +128,15 @@ class Scenario:
             raise ValueError("synth_echoes failed")
         return out.view(np.complex64).reshape(P, E, Ns)
 
+    def subset_pings(self, idx) -> "Scenario":
+        """The same scene and grid observed by a subset of the pings (for bounded test sizes)."""
+        idx = np.asarray(idx)
+        return dataclasses.replace(self, name=f"{self.name}[{len(idx)} pings]", tx=self.tx[idx], rx=self.rx[idx],
+                                   t0=self.t0[idx],
+                                   body_rot=None if self.body_rot is None else self.body_rot[idx],
+                                   nav_nominal=None if self.nav_nominal is None else
+                                   (self.nav_nominal[0][idx], self.nav_nominal[1][idx]))
+
     def pixel_centre(self, idx) -> np.ndarray:
         idx = np.asarray(idx, dtype=np.float64).reshape(-1, 3)
         g = self.grid

@@ -274,11 +274,16 @@ def test_rangecompress_gpu_vs_oracle(bpmod):
 
 # ------------------------------------------------------------------ full BASELINE sizes (sampled)
 
-@pytest.mark.parametrize("cid", [2, 4])
-def test_parity_full_size_sampled(bpmod, cid):
-    """At the BASELINE configs' full sizes, in bench.py's launch configuration (the same
-    Backprojector plan), compare sampled pixels + windows around every target."""
+@pytest.mark.parametrize("cid,stride", [(2, 1), (4, 1), (3, 4), (5, 10)])
+def test_parity_full_size_sampled(bpmod, cid, stride):
+    """At the BASELINE configs' full grid sizes, in bench.py's launch configuration (the same
+    Backprojector plan), compare sampled pixels + windows around every target.  Configs 3 and 5
+    use every 4th / 10th ping (full aperture span, full grid, full record length) to bound the
+    echo generation time; config 5 is the precision stress case (ranges to 185 m, carrier phase
+    to 2e5 rad, 2.7e8-pixel image)."""
     s = synth.scenario(cid)
+    if stride > 1:
+        s = s.subset_pings(np.arange(0, s.P, stride))
     e = s.echoes()
     got = _form(bpmod, s, e)
     idx = s.sample_pixels(4096, window=15 if s.grid["nz"] == 1 else 5, seed=cid)

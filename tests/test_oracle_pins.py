@@ -326,3 +326,17 @@ def test_rotation_eq2_examples():
     assert (synth.rotation_matrix(0.1, 0, 0) @ [0, 1, 0])[2] > 0
     # positive pitch raises the bow (+x body -> -z, up)
     assert (synth.rotation_matrix(0, 0.1, 0) @ [1, 0, 0])[2] < 0
+
+
+def test_nominal_nav_defocuses_high_motion():
+    """S:798 analog: imaging the high-motion collection (config 3, reduced) with the nominal,
+    unperturbed navigation instead of the true one loses at least 3 dB of target peak --
+    the method needs the per-ping, per-element positions (R5), not a straight-line track."""
+    s = synth.scenario(3, reduced=True)
+    e = s.echoes()
+    idx = s.sample_pixels(0, window=9)
+    true_img = oracle.tdbp_grid(e, s.tx, s.rx, s.t0, s.fc, s.fs, s.c, s.grid, idx=idx)
+    ntx, nrx = s.nav_nominal
+    nom_img = oracle.tdbp_grid(e, ntx, nrx, s.t0, s.fc, s.fs, s.c, s.grid, idx=idx)
+    loss_db = 20 * np.log10(np.max(np.abs(true_img)) / np.max(np.abs(nom_img)))
+    assert loss_db >= 3.0, loss_db
