@@ -76,7 +76,7 @@ struct TdbpParams {
 // per-channel constants in shared memory (fp64 prologue output)
 struct __align__(16) ChanConst {
   float ux2, uy2, uz2, ir2;     // rx leg: 2 (c_T - rx), 1 / r_r^2
-  float a0, a1, a2, a3;         // rx leg series coefficients * (fs/c) / r_r
+  float a0, a1, a2, a3;         // rx leg series in q: dU = q (a0 + a1 q + a2 q^2 + a3 q^3), see prologue
   float urr, phi0, r_r, r2_r;   // centred window coordinate offset; phase offset (rad); r_r; r_r^2
   float tx2x, tx2y, tx2z, r2_t; // tx leg: 2 (c_T - tx), r_t^2
   float r_t, kfs, klo_f, pad1;  // r_t, fs/c, (float) k_lo
@@ -135,9 +135,12 @@ __device__ __forceinline__ ChanConst chan_prologue(const TdbpParams& prm, int ch
   k.ux2 = (float)(2.0 * urx); k.uy2 = (float)(2.0 * ury); k.uz2 = (float)(2.0 * urz);
   // series coefficients only need fp32 relative accuracy
   const float ir = 1.0f / (float)r_r;
-  k.ir2 = ir * ir;
-  const float g = (float)prm.k_s * ir;   // (sqrt(1+e)-1)/e = 1/2 - e/8 + e^2/16 - 5e^3/128 + ...
-  k.a0 = 0.5f * g; k.a1 = -0.125f * g; k.a2 = 0.0625f * g; k.a3 = -0.0390625f * g;
+  const float ir2 = ir * ir;
+  k.ir2 = ir2;
+  // (sqrt(1+e)-1)/e = 1/2 - e/8 + e^2/16 - 5e^3/128 + ..., e = q / r^2; folded into a polynomial
+  // in q so the kernel needs no e = q / r^2 multiply: a_n = c_n (fs/c) / r^(2n+1)
+  const float g = (float)prm.k_s * ir;
+  k.a0 = 0.5f * g; k.a1 = -0.125f * g * ir2; k.a2 = 0.0625f * g * ir2 * ir2; k.a3 = -0.0390625f * g * ir2 * ir2 * ir2;
   k.urr = (float)urr;
   k.phi0 = (float)(6.283185307179586 * ph);
   k.r_r = (float)r_r; k.r2_r = (float)(r_r * r_r);
@@ -339,11 +342,18 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
     for (int c = warp; c < nb; c += kWarps) {
       const float2* rw = reinterpret_cast<const float2*>(rawp + c * rsb);
       float4* wc = win + c * W;
-      for (int j = lane; j < W; j += 32) {
-        const float2 d0 = rw[j], d1 = rw[j + 1];
-        const float2 sl = __fadd2_rn(d1, make_float2(-d0.x, -d0.y));
-        const float2 ic = __ffma2_rn(sl, f2(0.5f - (float)(j - Wh)), d0);
-        wc[j] = make_float4(ic.x, ic.y, sl.x, sl.y);
+      // two cells per lane: samples 2t, 2t+1 (one 16-B load) and 2t+2
+      for (int t = lane; 2 * t < W; t += 32) {
+        const float4 d01 = *reinterpret_cast<const float4*>(rw + 2 * t);
+        const float2 d2 = rw[2 * t + 2];
+        const float2 d0 = make_float2(d01.x, d01.y), d1 = make_float2(d01.z, d01.w);
+        const float2 s0 = __fadd2_rn(d1, make_float2(-d0.x, -d0.y));
+        const float2 s1 = __fadd2_rn(d2, make_float2(-d1.x, -d1.y));
+        const float j0 = 0.5f - (float)(2 * t - Wh);
+        const float2 i0 = __ffma2_rn(s0, f2(j0), d0);
+        const float2 i1 = __ffma2_rn(s1, f2(j0 - 1.0f), d1);
+        wc[2 * t] = make_float4(i0.x, i0.y, s0.x, s0.y);
+        if (2 * t + 1 < W) wc[2 * t + 1] = make_float4(i1.x, i1.y, s1.x, s1.y);
       }
     }
 #endif
@@ -380,15 +390,14 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
           const float den1 = fmaf(r2.y, rsqrt_approx(r2.y), kc.r_r);
           U = __ffma2_rn(__fmul2_rn(q, make_float2(rcp_approx(den0), rcp_approx(den1))), f2(kc.kfs), BT[p]);
         } else {
-          const float2 e = __fmul2_rn(q, f2(kc.ir2));
           float2 h;
           if (MODE == kSeries4) {
-            h = __ffma2_rn(f2(kc.a3), e, f2(kc.a2));
-            h = __ffma2_rn(h, e, f2(kc.a1));
+            h = __ffma2_rn(f2(kc.a3), q, f2(kc.a2));
+            h = __ffma2_rn(h, q, f2(kc.a1));
           } else {
-            h = __ffma2_rn(f2(kc.a2), e, f2(kc.a1));
+            h = __ffma2_rn(f2(kc.a2), q, f2(kc.a1));
           }
-          h = __ffma2_rn(h, e, f2(kc.a0));
+          h = __ffma2_rn(h, q, f2(kc.a0));
           U = __ffma2_rn(q, h, BT[p]);
         }
         U = __fadd2_rn(U, f2(kc.urr));                       // centred window coordinate
