@@ -109,6 +109,17 @@ SASBP_API sas_status sas_bp_form(sas_bp_t h, float* image_out);
 #define SAS_FORM_ACCUMULATE 1
 SASBP_API sas_status sas_bp_form_device(sas_bp_t h, void* image_dev, void* cuda_stream, int32_t flags);
 
+/* End-to-end formation from HOST echoes with the H2D copy overlapped with the backprojection:
+ * the channels (ping x element rows) are split into `chunks` contiguous ranges (0 = automatic);
+ * chunk c is copied on a copy stream while chunk c-1 is backprojected, each chunk accumulating
+ * into the device image (I(A u B) = I(A) + I(B)), then the image is copied to image_out.
+ * Arguments as sas_bp_set_pings + sas_bp_form (echoes should be pinned for the overlap to
+ * happen; pageable memory works but serialises the copies).  Afterwards the handle holds the
+ * ping set, so sas_bp_form / sas_bp_form_device may be called again.  Synchronous. */
+SASBP_API sas_status sas_bp_form_streamed(sas_bp_t h, const float* echoes, int32_t P, int32_t E, int32_t Ns,
+                                          const double* tx, const double* rx, const double* t0, float* image_out,
+                                          int32_t chunks);
+
 /* Algorithmic work counters of the current ping set (off the clock, for the metric):
  *   dense  = nx*ny*nz*P*E  pixel.ping.element terms;
  *   in_win = the terms whose interpolation support meets the record, u in (-1, Ns)

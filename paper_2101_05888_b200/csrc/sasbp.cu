@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
 #include <new>
 #include <vector>
 
@@ -66,6 +67,7 @@ struct sas_bp_s {
   size_t geo_cap = 0;
   unsigned long long* counter = nullptr;
   cudaStream_t stream = nullptr;
+  cudaStream_t copy_stream = nullptr;   // H2D of ping chunks in sas_bp_form_streamed
   int P = 0, E = 0, Ns = 0;
   // TMA descriptor of the current echoes (row staging), rebuilt when the ping set changes
   sasbp::TmaDesc tmap{};
@@ -194,7 +196,7 @@ bool encode_tma(sas_bp_t h) {
 }
 
 cudaError_t launch_tdbp(sas_bp_t h, float2* image, unsigned long long* counter, int accumulate,
-                        bool count, cudaStream_t st) {
+                        bool count, cudaStream_t st, int ch_lo = 0, int ch_hi = -1) {
   sasbp::TdbpParams prm{};
   prm.echoes = h->echoes;
   prm.tx = h->geo;
@@ -216,6 +218,8 @@ cudaError_t launch_tdbp(sas_bp_t h, float2* image, unsigned long long* counter, 
   prm.tiles_x = h->tiles_x; prm.tiles_y = h->tiles_y; prm.tiles_z = h->tiles_z;
   prm.W = h->W;
   prm.accumulate = accumulate;
+  prm.ch_lo = ch_lo;
+  prm.ch_hi = ch_hi < 0 ? h->P * h->E : ch_hi;
   switch (h->variant) {
 #if SASBP_K4
     case V2D: return launch_variant<4, 1, 1, 8, 1, false>(prm, h->tmap, h->use_tma, h->mode, count, st);
@@ -380,6 +384,7 @@ void sas_bp_destroy(sas_bp_t h) {
   cudaFree(h->geo);
   cudaFree(h->counter);
   if (h->stream) cudaStreamDestroy(h->stream);
+  if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
   if (prev >= 0) cudaSetDevice(prev);
   delete h;
 }
@@ -455,6 +460,54 @@ sas_status sas_bp_form(sas_bp_t h, float* image_out) {
   const size_t npx = (size_t)h->grid.nx * h->grid.ny * h->grid.nz;
   CK_H(h, cudaMemcpyAsync(image_out, h->image, npx * sizeof(float2), cudaMemcpyDeviceToHost, h->stream));
   CK_H(h, cudaStreamSynchronize(h->stream));
+  return SAS_OK;
+}
+
+sas_status sas_bp_form_streamed(sas_bp_t h, const float* echoes, int32_t P, int32_t E, int32_t Ns, const double* tx,
+                                const double* rx, const double* t0, float* image_out, int32_t chunks) {
+  g_err[0] = 0;
+  if (!h) return fail(SAS_E_INVALID, "handle is NULL");
+  if (h->broken) return fail(SAS_E_CUDA, "handle is in a failed CUDA state; destroy it");
+  if (!echoes || !image_out) return fail(SAS_E_INVALID, "echoes and image_out must not be NULL");
+  if (chunks < 0) return fail(SAS_E_INVALID, "chunks must be >= 0");
+  sas_status st = validate_geo(P, E, Ns, tx, rx, t0);
+  if (st != SAS_OK) return st;
+  CK_H(h, cudaSetDevice(h->device));
+  const size_t n = (size_t)P * E * Ns;
+  if (n > h->echoes_cap) {
+    if (h->echoes_owned) { cudaFree(h->echoes_owned); h->bytes -= h->echoes_cap * sizeof(float2); }
+    h->echoes_owned = nullptr; h->echoes_cap = 0;
+    cudaError_t e = cudaMalloc(&h->echoes_owned, n * sizeof(float2));
+    if (e != cudaSuccess) { h->echoes_owned = nullptr; h->has_pings = false; return fail(SAS_E_NOMEM, "cudaMalloc(echoes, %zu B): %s", n * sizeof(float2), cudaGetErrorString(e)); }
+    h->echoes_cap = n;
+    h->bytes += n * sizeof(float2);
+  }
+  if (!h->copy_stream) CK_H(h, cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
+  st = upload_geo(h, P, E, Ns, tx, rx, t0, h->stream);  // small, synchronous
+  if (st != SAS_OK) { h->has_pings = false; return st; }
+  h->echoes = h->echoes_owned;
+  h->use_tma = encode_tma(h);
+  h->has_pings = true;
+  const int nch = P * E;
+  int nchunk = chunks > 0 ? chunks : 8;
+  nchunk = std::max(1, std::min(nchunk, (nch + 63) / 64));   // >= 64 channels per chunk
+  std::vector<cudaEvent_t> ev(nchunk, nullptr);
+  for (auto& x : ev) CK_H(h, cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+  cudaError_t err = cudaSuccess;
+  for (int c = 0; c < nchunk && err == cudaSuccess; ++c) {
+    const int c0 = (int)((long long)nch * c / nchunk), c1 = (int)((long long)nch * (c + 1) / nchunk);
+    err = cudaMemcpyAsync(h->echoes_owned + (size_t)c0 * Ns, echoes + 2 * (size_t)c0 * Ns,
+                          (size_t)(c1 - c0) * Ns * sizeof(float2), cudaMemcpyHostToDevice, h->copy_stream);
+    if (err == cudaSuccess) err = cudaEventRecord(ev[c], h->copy_stream);
+    if (err == cudaSuccess) err = cudaStreamWaitEvent(h->stream, ev[c], 0);
+    if (err == cudaSuccess) err = launch_tdbp(h, h->image, h->counter, c > 0 ? 1 : 0, false, h->stream, c0, c1);
+  }
+  const size_t npx = (size_t)h->grid.nx * h->grid.ny * h->grid.nz;
+  if (err == cudaSuccess)
+    err = cudaMemcpyAsync(image_out, h->image, npx * sizeof(float2), cudaMemcpyDeviceToHost, h->stream);
+  if (err == cudaSuccess) err = cudaStreamSynchronize(h->stream);
+  for (auto& x : ev) cudaEventDestroy(x);
+  if (err != cudaSuccess) return cuda_fail(h, err, "sas_bp_form_streamed");
   return SAS_OK;
 }
 

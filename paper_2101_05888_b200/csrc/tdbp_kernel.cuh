@@ -71,6 +71,7 @@ struct TdbpParams {
   int tiles_x, tiles_y, tiles_z;
   int W;                  // window cells per channel (cells j = 0..W-1 use samples k_lo+j, k_lo+j+1)
   int accumulate;
+  int ch_lo, ch_hi;       // channel range [ch_lo, ch_hi) of this launch (ch = p * E + e)
 };
 
 // per-channel constants in shared memory (fp64 prologue output)
@@ -266,7 +267,7 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
   }
 
   const float kph = (float)(6.283185307179586 * prm.k_r);
-  const int nch = prm.P * prm.E;
+  const int nch = prm.ch_hi - prm.ch_lo;
   const int nbatch = (nch + kNB - 1) / kNB;
   const int Wh = W >> 1;
   const int nbox = box_samples(W);
@@ -286,8 +287,8 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
   // rows have landed.
   constexpr int kCW = kNB / kWarps;
   auto issue = [&](int b) {
-    const int ch0 = b * kNB;
-    const int nb = min(kNB, nch - ch0);
+    const int nb = min(kNB, nch - b * kNB);
+    const int ch0 = prm.ch_lo + b * kNB;
     ChanConst* cb = cc + (b & 1) * kNB;
     const int c0 = warp * kCW;
     const int mine = max(0, min(kCW, nb - c0));
@@ -450,11 +451,10 @@ __global__ void __launch_bounds__(32 * WY * WZ) count_kernel(const TdbpParams pr
     dd[k] = dx[k] * dx[k] + dy[k] * dy[k] + dz[k] * dz[k];
     ok[k] = tm.valid(prm, k);
   }
-  const int nch = prm.P * prm.E;
   const float Nsf = (float)prm.Ns;
   unsigned cnt = 0;
-  for (int ch0 = 0; ch0 < nch; ch0 += kNB) {
-    const int nb = min(kNB, nch - ch0);
+  for (int ch0 = prm.ch_lo; ch0 < prm.ch_hi; ch0 += kNB) {
+    const int nb = min(kNB, prm.ch_hi - ch0);
     __syncthreads();
     if (tid < nb) cc[tid] = chan_prologue(prm, ch0 + tid, ct, tid, 0u);
     __syncthreads();

@@ -22,7 +22,7 @@ _NAMES = {0: "SAS_OK", -1: "SAS_E_INVALID", -2: "SAS_E_STATE", -3: "SAS_E_NOMEM"
 
 EXPORTS = ("sas_bp_create", "sas_bp_destroy", "sas_bp_set_pings", "sas_bp_set_pings_device", "sas_bp_form",
            "sas_bp_form_device", "sas_bp_count_terms", "sas_bp_workspace_bytes", "sas_rangecompress",
-           "sas_rangecompress_device", "sas_last_error", "sas_version", "sas_bp_get_plan")
+           "sas_rangecompress_device", "sas_last_error", "sas_version", "sas_bp_get_plan", "sas_bp_form_streamed")
 
 
 class SasError(RuntimeError):
@@ -71,6 +71,7 @@ def load_library(path: Optional[str] = None):
         "sas_last_error": ([], ctypes.c_char_p),
         "sas_version": ([], ctypes.c_char_p),
         "sas_bp_get_plan": ([vp, ctypes.POINTER(sas_bp_plan)], ctypes.c_int),
+        "sas_bp_form_streamed": ([vp, f32p, i32, i32, i32, f64p, f64p, f64p, f32p, i32], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -210,6 +211,31 @@ class Backprojector:
                 raise ValueError("out must be C-contiguous complex64 of the grid shape")
             ptr = out.view(np.float32).ctypes.data_as(ctypes.POINTER(ctypes.c_float))
         _check(_lib.sas_bp_form(self._h, ptr))
+        return out
+
+    def form_streamed(self, echoes, tx, rx, t0=None, out=None, chunks: int = 0) -> np.ndarray:
+        """End to end from host echoes with chunked H2D overlapped with backprojection
+        (sas_bp_form_streamed).  `echoes`: complex64 [P][E][Ns] numpy / CPU torch (pin it for
+        overlap); returns the image in host memory."""
+        if hasattr(echoes, "numpy") and not hasattr(echoes, "ctypes"):
+            ek = echoes.contiguous()
+            P, E, Ns = ek.shape
+            eptr = ctypes.cast(ctypes.c_void_p(ek.data_ptr()), ctypes.POINTER(ctypes.c_float))
+        else:
+            ek = np.ascontiguousarray(echoes, dtype=np.complex64)
+            P, E, Ns = ek.shape
+            eptr = ek.view(np.float32).ctypes.data_as(ctypes.POINTER(ctypes.c_float))
+        if out is None:
+            out = np.empty(self.shape, dtype=np.complex64)
+        if hasattr(out, "data_ptr") and not hasattr(out, "ctypes"):
+            optr = ctypes.cast(ctypes.c_void_p(out.data_ptr()), ctypes.POINTER(ctypes.c_float))
+        else:
+            optr = out.view(np.float32).ctypes.data_as(ctypes.POINTER(ctypes.c_float))
+        tx, rx, t0 = self._geo(P, E, tx, rx, t0)
+        _check(_lib.sas_bp_form_streamed(self._h, eptr, P, E, Ns, _ptr(tx, ctypes.c_double), _ptr(rx, ctypes.c_double),
+                                         _ptr(t0, ctypes.c_double), optr, int(chunks)))
+        del ek
+        self.P, self.E, self.Ns = P, E, Ns
         return out
 
     def form_device(self, image, stream=None, accumulate: bool = False):

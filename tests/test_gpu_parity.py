@@ -365,3 +365,21 @@ def test_rangecompress_then_backproject(bpmod):
     img_g = _form(bpmod, s, g)
     img_o = oracle.tdbp_grid(o, s.tx, s.rx, s.t0, s.fc, s.fs, s.c, s.grid)
     _check(img_g, img_o, label="compress -> backproject")
+
+
+@pytest.mark.parametrize("chunks", [1, 3, 0])
+def test_form_streamed_matches_form(bpmod, chunks):
+    """sas_bp_form_streamed (chunked H2D overlapped with accumulating launches) equals
+    set_pings + form: bitwise for one chunk, to fp32 summation order otherwise."""
+    import torch
+    s = synth.scenario(2, reduced=True)
+    e = s.echoes()
+    ref = _form(bpmod, s, e)
+    pinned = torch.from_numpy(e).pin_memory()
+    with bpmod.Backprojector(s.fc, s.bandwidth, s.fs, s.c, s.grid) as bp:
+        got = bp.form_streamed(pinned, s.tx, s.rx, s.t0, chunks=chunks)
+        again = bp.form()            # the handle now holds the ping set
+    if chunks == 1:
+        assert np.array_equal(got, ref)
+    assert np.max(np.abs(got - ref)) <= 1e-5 * np.max(np.abs(ref))
+    assert np.array_equal(again, ref)

@@ -52,10 +52,11 @@ def main():
         path = sys.argv[sys.argv.index("--json") + 1]
         cfg = int(sys.argv[sys.argv.index("--config") + 1]) if "--config" in sys.argv else None
         num = lambda k: float(res[k][0].replace(",", "")) if k in res else None
+        scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+        nbytes = lambda k: num(k) * scale.get(res[k][1], float("nan")) if k in res else 0.0
         summ = {"report": rep, "config": cfg,
                 "duration_ns": num("gpu__time_duration.sum"),
-                "dram_bytes_per_launch": (num("dram__bytes_read.sum") or 0) + (num("dram__bytes_write.sum") or 0),
-                "dram_units": res.get("dram__bytes_read.sum", ("", ""))[1],
+                "dram_bytes_per_launch": nbytes("dram__bytes_read.sum") + nbytes("dram__bytes_write.sum"),
                 "metrics": {k: v for k, (v, u) in res.items()}, "stalls_per_issue": stalls}
         with open(path, "w") as f:
             json.dump(summ, f, indent=1)
