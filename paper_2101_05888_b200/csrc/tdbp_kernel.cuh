@@ -274,6 +274,8 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
 #if SASBP_FLAT_TRANSFORM
   const float inv_w = 1.0f / (float)W;
 #endif
+  const int P2 = (W + 1) >> 1;                // cell pairs per channel
+  const float inv_p2 = 1.0f / (float)P2;
 
   if (USE_TMA && tid == 0) {
     mbar_init(bar, kWarps);
@@ -340,21 +342,26 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
       }
     }
 #else
-    for (int c = warp; c < nb; c += kWarps) {
-      const float2* rw = reinterpret_cast<const float2*>(rawp + c * rsb);
-      float4* wc = win + c * W;
-      // two cells per lane: samples 2t, 2t+1 (one 16-B load) and 2t+2
-      for (int t = lane; 2 * t < W; t += 32) {
-        const float4 d01 = *reinterpret_cast<const float4*>(rw + 2 * t);
-        const float2 d2 = rw[2 * t + 2];
+    {  // warp w rewrites channels w, w+kWarps, ...: two cells per lane-step, flattened over
+       // (channel, cell pair) so the lanes stay busy across channel boundaries
+      const int nmine = (nb - warp + kWarps - 1) / kWarps;
+      const int tot = nmine * P2;
+      for (int i = lane; i < tot; i += 32) {
+        const int q = (int)(((float)i + 0.5f) * inv_p2);   // i / P2, exact for i < 2^20
+        const int t = i - q * P2;
+        const int c = warp + q * kWarps;
+        const float2* rw = reinterpret_cast<const float2*>(rawp + c * rsb) + 2 * t;
+        const float4 d01 = *reinterpret_cast<const float4*>(rw);
+        const float2 d2 = rw[2];
         const float2 d0 = make_float2(d01.x, d01.y), d1 = make_float2(d01.z, d01.w);
         const float2 s0 = __fadd2_rn(d1, make_float2(-d0.x, -d0.y));
         const float2 s1 = __fadd2_rn(d2, make_float2(-d1.x, -d1.y));
-        const float j0 = 0.5f - (float)(2 * t - Wh);
+        const float j0 = (float)(Wh - 2 * t) + 0.5f;
         const float2 i0 = __ffma2_rn(s0, f2(j0), d0);
         const float2 i1 = __ffma2_rn(s1, f2(j0 - 1.0f), d1);
-        wc[2 * t] = make_float4(i0.x, i0.y, s0.x, s0.y);
-        if (2 * t + 1 < W) wc[2 * t + 1] = make_float4(i1.x, i1.y, s1.x, s1.y);
+        float4* wc = win + c * W + 2 * t;
+        wc[0] = make_float4(i0.x, i0.y, s0.x, s0.y);
+        if (2 * t + 1 < W) wc[1] = make_float4(i1.x, i1.y, s1.x, s1.y);
       }
     }
 #endif
