@@ -198,7 +198,8 @@ struct TileMap {
 //   destinations) | win[kNB][W] float4 (intercept, slope) cells
 __host__ __device__ inline int box_samples(int W) { return (W + 1 + 1) & ~1; }      // even => 16-B rows
 __host__ __device__ inline size_t raw_slot_bytes(int W) { return ((size_t)box_samples(W) * 8 + 127) & ~(size_t)127; }
-__host__ __device__ inline size_t k2_raw_off() { return (2 * kNB * sizeof(ChanConst) + 16 + 127) & ~(size_t)127; }
+constexpr int kRing = 8;   // ChanConst batches kept in shared memory (prologues run 2-5 batches ahead)
+__host__ __device__ inline size_t k2_raw_off() { return (kRing * kNB * sizeof(ChanConst) + 16 + 127) & ~(size_t)127; }
 __host__ __device__ inline size_t k2_win_off(int W) { return k2_raw_off() + kNB * raw_slot_bytes(W); }
 __host__ __device__ inline size_t k2_smem_bytes(int W) { return k2_win_off(W) + (size_t)kNB * W * sizeof(float4) + 128; }
 
@@ -236,8 +237,8 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
   extern __shared__ __align__(128) unsigned char smem_raw[];
   // the dynamic smem base is only guaranteed 16-B aligned: align it to 128 B ourselves
   unsigned char* sbase = smem_raw + ((128 - ((uint32_t)__cvta_generic_to_shared(smem_raw) & 127)) & 127);
-  ChanConst* cc = reinterpret_cast<ChanConst*>(sbase);                       // [2][kNB]
-  const uint32_t bar = (uint32_t)__cvta_generic_to_shared(sbase + 2 * kNB * sizeof(ChanConst));
+  ChanConst* cc = reinterpret_cast<ChanConst*>(sbase);                       // [kRing][kNB]
+  const uint32_t bar = (uint32_t)__cvta_generic_to_shared(sbase + kRing * kNB * sizeof(ChanConst));
   const int W = prm.W;
   const uint32_t rsb = (uint32_t)raw_slot_bytes(W);
   unsigned char* rawp = sbase + k2_raw_off();
@@ -283,19 +284,26 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
   }
   __syncthreads();
 
-  // producer work is spread over the warps: warp w runs the fp64 prologue of channels
-  // [w*kCW, (w+1)*kCW) of batch b and issues their window loads; every warp arrives once on
-  // the batch's mbarrier (with the byte count of its rows) so the phase completes when all
-  // rows have landed.
+  // fp64 prologues run in groups: warp w computes all kNB channels of batch g + w (one lane per
+  // channel), four batches ahead of use, into a ring of kRing constant batches -- one pass of
+  // the prologue code per warp per kWarps batches instead of one per batch.
+  auto prologue_group = [&](int g) {
+    const int bb = g + warp;
+    if (bb < nbatch && lane < kNB) {
+      const int nbb = min(kNB, nch - bb * kNB);
+      if (lane < nbb)
+        cc[(bb % kRing) * kNB + lane] = chan_prologue(prm, prm.ch_lo + bb * kNB + lane, ct, lane, win_base);
+    }
+  };
+  // window loads of batch b: warp w issues the rows of channels [w*kCW, (w+1)*kCW); every warp
+  // arrives once on the batch's mbarrier with the byte count of its rows.
   constexpr int kCW = kNB / kWarps;
   auto issue = [&](int b) {
     const int nb = min(kNB, nch - b * kNB);
     const int ch0 = prm.ch_lo + b * kNB;
-    ChanConst* cb = cc + (b & 1) * kNB;
+    const ChanConst* cb = cc + (b % kRing) * kNB;
     const int c0 = warp * kCW;
     const int mine = max(0, min(kCW, nb - c0));
-    if (lane < mine) cb[c0 + lane] = chan_prologue(prm, ch0 + c0 + lane, ct, c0 + lane, win_base);
-    __syncwarp();
     if (USE_TMA) {
       if (lane == 0) {
         mbar_expect_tx(bar, (uint32_t)(mine * nbox * 8));
@@ -316,6 +324,8 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
     }
   };
 
+  prologue_group(0);
+  __syncthreads();
   issue(0);
   int cur_ping = -1;
 
@@ -367,7 +377,8 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
 #endif
     __syncthreads();   // win(b) complete; raw free
     if (b + 1 < nbatch) issue(b + 1);
-    const ChanConst* cb = cc + (b & 1) * kNB;
+    if ((b + 2) % kWarps == 0) prologue_group(b + 2);   // batches b+2 .. b+5 (ring slots not in use)
+    const ChanConst* cb = cc + (b % kRing) * kNB;
 
 #pragma unroll 1
     for (int c = 0; c < nb; ++c) {
