@@ -42,6 +42,9 @@ namespace sasbp {
 #ifndef SASBP_MINB
 #define SASBP_MINB 4   // resident 4-warp CTAs per SM the register allocation targets
 #endif
+#ifndef SASBP_CUNROLL2
+#define SASBP_CUNROLL2 0
+#endif
 #ifndef SASBP_NB
 #define SASBP_NB 16
 #endif
@@ -198,7 +201,11 @@ struct TileMap {
 //   destinations) | win[kNB][W] float4 (intercept, slope) cells
 __host__ __device__ inline int box_samples(int W) { return (W + 1 + 1) & ~1; }      // even => 16-B rows
 __host__ __device__ inline size_t raw_slot_bytes(int W) { return ((size_t)box_samples(W) * 8 + 127) & ~(size_t)127; }
-constexpr int kRing = 8;   // ChanConst batches kept in shared memory (prologues run 2-5 batches ahead)
+#ifndef SASBP_BPW
+#define SASBP_BPW 2   // batches per warp in one prologue group (lanes = BPW * kNB <= 32)
+#endif
+constexpr int kBPW = SASBP_BPW;
+constexpr int kRing = 8 * kBPW;   // ChanConst batches kept in shared memory (prologues run ahead)
 __host__ __device__ inline size_t k2_raw_off() { return (kRing * kNB * sizeof(ChanConst) + 16 + 127) & ~(size_t)127; }
 __host__ __device__ inline size_t k2_win_off(int W) { return k2_raw_off() + kNB * raw_slot_bytes(W); }
 __host__ __device__ inline size_t k2_smem_bytes(int W) { return k2_win_off(W) + (size_t)kNB * W * sizeof(float4) + 128; }
@@ -287,12 +294,14 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
   // fp64 prologues run in groups: warp w computes all kNB channels of batch g + w (one lane per
   // channel), four batches ahead of use, into a ring of kRing constant batches -- one pass of
   // the prologue code per warp per kWarps batches instead of one per batch.
+  constexpr int kGroup = kWarps * kBPW;   // batches per prologue group
   auto prologue_group = [&](int g) {
-    const int bb = g + warp;
-    if (bb < nbatch && lane < kNB) {
+    const int sub = lane / kNB, cl = lane % kNB;
+    const int bb = g + warp * kBPW + sub;
+    if (sub < kBPW && bb < nbatch) {
       const int nbb = min(kNB, nch - bb * kNB);
-      if (lane < nbb)
-        cc[(bb % kRing) * kNB + lane] = chan_prologue(prm, prm.ch_lo + bb * kNB + lane, ct, lane, win_base);
+      if (cl < nbb)
+        cc[(bb % kRing) * kNB + cl] = chan_prologue(prm, prm.ch_lo + bb * kNB + cl, ct, cl, win_base);
     }
   };
   // window loads of batch b: warp w issues the rows of channels [w*kCW, (w+1)*kCW); every warp
@@ -377,10 +386,14 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
 #endif
     __syncthreads();   // win(b) complete; raw free
     if (b + 1 < nbatch) issue(b + 1);
-    if ((b + 2) % kWarps == 0) prologue_group(b + 2);   // batches b+2 .. b+5 (ring slots not in use)
+    if ((b + 2) % kGroup == 0) prologue_group(b + 2);   // batches b+2 .. b+1+kGroup (ring slots not in use)
     const ChanConst* cb = cc + (b % kRing) * kNB;
 
+#if SASBP_CUNROLL2
+#pragma unroll 2
+#else
 #pragma unroll 1
+#endif
     for (int c = 0; c < nb; ++c) {
       const ChanConst kc = cb[c];
       if (kc.ping != cur_ping) {
