@@ -125,6 +125,9 @@ __device__ __forceinline__ void dft16(float2 v[16]) {
 #undef SL
 }
 
+// twiddle W_4096^m (forward sign) from the global table (L1 resident)
+__device__ __forceinline__ float2 twid(const float2* __restrict__ tw, int m) { return __ldg(tw + m); }
+
 // one Stockham pass on natural-order registers: twiddle, DFT16 (output left in sig order), store
 template <bool INV, int NS>
 __device__ __forceinline__ void pass_store(float2 v[16], float2* sm, const float2* __restrict__ tw, int j) {
@@ -132,7 +135,7 @@ __device__ __forceinline__ void pass_store(float2 v[16], float2* sm, const float
   if (NS > 1) {
 #pragma unroll
     for (int r = 1; r < 16; ++r) {
-      float2 w = __ldg(tw + ((r * k * (256 / NS)) & (kL - 1)));
+      float2 w = twid(tw, (r * k * (256 / NS)) & (kL - 1));
       if (INV) w.y = -w.y;
       v[r] = cmul(v[r], w);
     }
@@ -149,7 +152,7 @@ __device__ __forceinline__ void pass_regs(float2 v[16], const float2* __restrict
   const int k = j & (NS - 1);
 #pragma unroll
   for (int r = 1; r < 16; ++r) {
-    float2 w = __ldg(tw + ((r * k * (256 / NS)) & (kL - 1)));
+    float2 w = twid(tw, (r * k * (256 / NS)) & (kL - 1));
     if (INV) w.y = -w.y;
     v[r] = cmul(v[r], w);
   }
@@ -200,14 +203,15 @@ __global__ void __launch_bounds__(kFT) rc_prep_kernel(const float2* __restrict__
   for (int r = 0; r < 16; ++r) H[j + r * kFT] = make_float2(v[sig(r)].x * sc, -v[sig(r)].y * sc);
 }
 
-__global__ void __launch_bounds__(kFT, 1) rc_fft_kernel(const float2* __restrict__ raw, int Ns, int V,
-                                                        const float2* __restrict__ H, const float2* __restrict__ tw,
+__global__ void __launch_bounds__(kFT, 2) rc_fft_kernel(const float2* __restrict__ raw, int Ns, int V,
+                                                        const float2* __restrict__ H, const float2* __restrict__ tw_g,
                                                         float2* __restrict__ out) {
   __shared__ float2 sm[kPad];
   const int j = threadIdx.x;
   const size_t ch = blockIdx.y;
   const int n0 = blockIdx.x * V;
   const float2* x = raw + ch * Ns;
+  const float2* tw = tw_g;
   float2 v[16];
   fft_forward(v, x, n0, Ns, sm, tw, j);
   // spectrum product in registers (slot sig(r) holds bin j + 256 r)
