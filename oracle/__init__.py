@@ -11,7 +11,10 @@ ctypes marshalling plus the gcc build of ``liboracle.so``.
 Parity status: every function here is pinned (tests/test_oracle_pins.py):
 ``tdbp_points`` / ``tdbp_grid`` by closed forms, hand-computed mono/bistatic
 delays, zero-extension values, point-target physics and invariants;
-``rangecompress`` by the autocorrelation-peak, shift and mainlobe pins.
+``rangecompress`` by the autocorrelation-peak, shift and mainlobe pins;
+``tdbp_points_gated`` (NEXT-1, reading R15) by the wide-open special case (= dense),
+the azimuth / elevation boundary examples, monotonicity in the beamwidth, rigid-rotation
+invariance and the config-1 target under the generator's own beam.
 """
 from __future__ import annotations
 
@@ -54,6 +57,11 @@ def _load():
                                                 ctypes.c_double, f64p, f64p, f64p, f64p, i64p,
                                                 ctypes.c_int64, f64p, i64p]
         lib.oracle_tdbp_grid_pixels.restype = ctypes.c_int
+        lib.oracle_tdbp_points_gated.argtypes = [f32p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                                 f64p, f64p, f64p, ctypes.c_double, ctypes.c_double,
+                                                 ctypes.c_double, f64p, ctypes.c_double, ctypes.c_double,
+                                                 ctypes.c_int32, f64p, ctypes.c_int64, f64p, i64p]
+        lib.oracle_tdbp_points_gated.restype = ctypes.c_int
         lib.oracle_rangecompress.argtypes = [f32p, ctypes.c_int64, ctypes.c_int32, f32p,
                                              ctypes.c_int32, f64p]
         lib.oracle_rangecompress.restype = ctypes.c_int
@@ -95,6 +103,39 @@ def tdbp_points(echoes, tx, rx, t0, fc, fs, c, pts, with_count=False):
         raise ValueError("oracle_tdbp_points: invalid arguments")
     res = out[:, 0] + 1j * out[:, 1]
     return (res, cnt) if with_count else res
+
+
+def tdbp_points_gated(echoes, tx, rx, t0, fc, fs, c, pts, az, el=0.0, bistatic=False, axes=None,
+                      with_count=False):
+    """Gated TDBP (NEXT-1): only terms whose point lies in the tx (and, bistatic, rx) FOV cone.
+    axes: [P][2][3] per-ping along-track axis a and boresight b (NED), None = (+x, +y)."""
+    lib = _load()
+    echoes, P, E, Ns, tx, rx, t0 = _echo_arrays(echoes, tx, rx, t0)
+    pts = np.ascontiguousarray(pts, dtype=np.float64).reshape(-1, 3)
+    ax = None if axes is None else np.ascontiguousarray(axes, dtype=np.float64).reshape(P, 2, 3)
+    N = pts.shape[0]
+    out = np.zeros((N, 2), dtype=np.float64)
+    cnt = np.zeros(N, dtype=np.int64) if with_count else None
+    rc = lib.oracle_tdbp_points_gated(_p(echoes, ctypes.c_float), P, E, Ns, _p(tx, ctypes.c_double),
+                                      _p(rx, ctypes.c_double), _p(t0, ctypes.c_double), float(fc), float(fs),
+                                      float(c), _p(ax, ctypes.c_double), float(az), float(el),
+                                      1 if bistatic else 0, _p(pts, ctypes.c_double), N,
+                                      _p(out, ctypes.c_double), _p(cnt, ctypes.c_int64))
+    if rc != 0:
+        raise ValueError("oracle_tdbp_points_gated: invalid arguments")
+    res = out[:, 0] + 1j * out[:, 1]
+    return (res, cnt) if with_count else res
+
+
+def grid_points(grid, idx=None):
+    """Pixel centres (reading R8) of index triples idx [N][3] (None = full grid, z-y-x order)."""
+    if idx is None:
+        iz, iy, ix = np.meshgrid(np.arange(grid["nz"]), np.arange(grid["ny"]), np.arange(grid["nx"]), indexing="ij")
+        idx = np.stack([ix.ravel(), iy.ravel(), iz.ravel()], axis=1)
+    idx = np.asarray(idx, dtype=np.float64).reshape(-1, 3)
+    g = {k: np.asarray(grid[k], dtype=np.float64) for k in ("origin", "step_x", "step_y", "step_z")}
+    return (g["origin"][None] + idx[:, :1] * g["step_x"][None] + idx[:, 1:2] * g["step_y"][None]
+            + idx[:, 2:3] * g["step_z"][None])
 
 
 def tdbp_grid(echoes, tx, rx, t0, fc, fs, c, grid, idx=None, with_count=False):

@@ -120,6 +120,68 @@ int oracle_tdbp_points(const float* echoes, int32_t P, int32_t E, int32_t Ns, co
 }
 
 /*
+ * Field-of-view gate of a sensor at position s for the scattering location x (NEXT-1 row:
+ * "every pixel must query the sonar geometry and determine if it is in the sonar field of
+ * view"; hard FWHM cones; reading R15 in DESIGN.md):
+ *   v = x - s;  a = along-track unit axis, b = boresight unit axis of the ping (NED);
+ *   azimuth   : |v.a| <= |v| sin(az/2)                (skipped when az >= pi)
+ *   elevation : v.b > 0 and |v.c| <= (v.b) tan(el/2),  c = a x b   (skipped when el <= 0 or el >= pi)
+ */
+static int in_fov(const double* x, const double* s, const double* a, const double* b, double az, double el) {
+  double v[3] = {x[0] - s[0], x[1] - s[1], x[2] - s[2]};
+  double nv = sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
+  if (az < 3.141592653589793) {
+    double va = v[0] * a[0] + v[1] * a[1] + v[2] * a[2];
+    if (fabs(va) > nv * sin(0.5 * az)) return 0;
+  }
+  if (el > 0 && el < 3.141592653589793) {
+    double c[3] = {a[1] * b[2] - a[2] * b[1], a[2] * b[0] - a[0] * b[2], a[0] * b[1] - a[1] * b[0]};
+    double vb = v[0] * b[0] + v[1] * b[1] + v[2] * b[2];
+    double vc = v[0] * c[0] + v[1] * c[1] + v[2] * c[2];
+    if (!(vb > 0) || fabs(vc) > vb * tan(0.5 * el)) return 0;
+  }
+  return 1;
+}
+
+/*
+ * Gated TDBP at explicit points (NEXT-1): the sum of the definition restricted to the terms
+ * whose pixel lies in the transmitter's field of view (and, when bistatic != 0, also in the
+ * receiving element's, P:310 / P:315 "bistatic ray-culling"):
+ *   I_g(x) = sum_{p,e} [x in FOV(tx_p)] [bistatic -> x in FOV(rx_{p,e})] term_{p,e}(x)
+ *   axes : [P][2][3] per-ping unit along-track axis a_p and boresight b_p, or NULL for
+ *          a = (1,0,0), b = (0,1,0) (side-looking to starboard)
+ */
+int oracle_tdbp_points_gated(const float* echoes, int32_t P, int32_t E, int32_t Ns, const double* tx,
+                             const double* rx, const double* t0, double fc, double fs, double c,
+                             const double* axes, double az, double el, int32_t bistatic,
+                             const double* pts, int64_t N, double* out, int64_t* n_in) {
+  if (P < 1 || E < 1 || Ns < 1 || N < 0 || !(c > 0) || !(fs > 0)) return -1;
+  static const double def_a[3] = {1.0, 0.0, 0.0}, def_b[3] = {0.0, 1.0, 0.0};
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int64_t i = 0; i < N; ++i) {
+    const double* x = pts + 3 * i;
+    double ar = 0.0, ai = 0.0;
+    int64_t cnt = 0;
+    for (int32_t p = 0; p < P; ++p) {
+      const double* a = axes ? axes + 6 * p : def_a;
+      const double* b = axes ? axes + 6 * p + 3 : def_b;
+      if (!in_fov(x, tx + 3 * p, a, b, az, el)) continue;
+      double t0p = t0 ? t0[p] : 0.0;
+      for (int32_t e = 0; e < E; ++e) {
+        const double* r = rx + 3 * ((int64_t)p * E + e);
+        if (bistatic && !in_fov(x, r, a, b, az, el)) continue;
+        const float* ch = echoes + 2 * ((int64_t)p * E + e) * (int64_t)Ns;
+        cnt += one_term(x, ch, Ns, tx + 3 * p, r, t0p, fc, fs, c, &ar, &ai);
+      }
+    }
+    out[2 * i] = ar;
+    out[2 * i + 1] = ai;
+    if (n_in) n_in[i] = cnt;
+  }
+  return 0;
+}
+
+/*
  * TDBP at grid pixels given by index triples idx[N][3] = (ix, iy, iz) of the
  * grid (origin, step_x, step_y, step_z), reading R8.
  */

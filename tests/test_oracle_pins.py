@@ -340,3 +340,104 @@ def test_nominal_nav_defocuses_high_motion():
     nom_img = oracle.tdbp_grid(e, ntx, nrx, s.t0, s.fc, s.fs, s.c, s.grid, idx=idx)
     loss_db = 20 * np.log10(np.max(np.abs(true_img)) / np.max(np.abs(nom_img)))
     assert loss_db >= 3.0, loss_db
+
+
+# ---------------------------------------------------------------- gated TDBP (NEXT-1, reading R15)
+
+def test_gate_wide_open_equals_dense():
+    """With the azimuth test disabled (az >= pi) and no elevation test the gate admits every
+    term: the gated sum reduces to the pinned dense definition."""
+    r = synth.random_case(21)
+    pts = oracle.grid_points(r["grid"])
+    dense = oracle.tdbp_points(r["echoes"], r["tx"], r["rx"], r["t0"], r["fc"], r["fs"], r["c"], pts)
+    for bist in (False, True):
+        g = oracle.tdbp_points_gated(r["echoes"], r["tx"], r["rx"], r["t0"], r["fc"], r["fs"], r["c"], pts,
+                                     az=np.pi, el=0.0, bistatic=bist)
+        assert np.array_equal(g, dense)
+
+
+@pytest.mark.parametrize("az,inside", [(0.3, True), (0.3, False), (1.2, True), (1.2, False)])
+def test_gate_azimuth_boundary(az, inside):
+    """S:150-152 examples: a point at azimuth FWHM/2 - 1e-6 rad is in the FOV, at FWHM/2 + 1e-6
+    it is not (sensor at the origin, a = +x, b = +y, single term with ramp data)."""
+    Ns = 4096
+    d = ((1.0 + np.arange(Ns) / 1024.0) + 1j * 0.5).astype(np.complex64).reshape(1, 1, Ns)
+    alpha = az / 2 + (-1e-6 if inside else 1e-6)
+    R = 15.0
+    x = np.array([[R * np.sin(alpha), R * np.cos(alpha), 0.0]])
+    args = (d, np.zeros((1, 3)), np.zeros((1, 1, 3)), None, 120e3, 120e3, 1500.0, x)
+    dense = oracle.tdbp_points(*args)[0]
+    g = oracle.tdbp_points_gated(*args, az=az)[0]
+    assert abs(dense) > 1.0
+    assert (g == dense) if inside else (g == 0)
+
+
+def test_gate_elevation_and_behind():
+    """Elevation sector |angle(v, b) in the (b, c) plane| <= el/2 and v.b > 0 (in front)."""
+    Ns = 4096
+    d = np.ones((1, 1, Ns), dtype=np.complex64)
+    args = (d, np.zeros((1, 3)), np.zeros((1, 1, 3)), None, 120e3, 120e3, 1500.0)
+    el = 0.5
+    # c = a x b = x x y = +z (down); a point depressed by el/2 -/+ 1e-6 below boresight
+    for delta, ok in ((-1e-6, True), (1e-6, False)):
+        ang = el / 2 + delta
+        x = np.array([[0.0, 15.0 * np.cos(ang), 15.0 * np.sin(ang)]])
+        g = oracle.tdbp_points_gated(*args, x, az=np.pi, el=el)[0]
+        assert (g != 0) == ok
+    behind = np.array([[0.0, -15.0, 0.0]])
+    assert oracle.tdbp_points_gated(*args, behind, az=np.pi, el=el)[0] == 0
+    assert oracle.tdbp_points_gated(*args, behind, az=np.pi, el=0.0)[0] != 0   # no elevation test
+
+
+def test_gate_monotone_in_beamwidth():
+    """Shrinking the FWHM never admits more terms."""
+    s = synth.scenario(2, reduced=True)
+    e = s.echoes()
+    pts = oracle.grid_points(s.grid, s.sample_pixels(200, window=3))
+    prev = None
+    for az in (np.pi, 1.0, 0.5, 0.277, 0.1):
+        _, cnt = oracle.tdbp_points_gated(e, s.tx, s.rx, s.t0, s.fc, s.fs, s.c, pts, az=az, bistatic=True,
+                                          with_count=True)
+        if prev is not None:
+            assert np.all(cnt <= prev)
+        prev = cnt
+
+
+def test_gate_rigid_rotation_invariance():
+    """Rotating positions, ping axes and grid rigidly leaves the gated image unchanged
+    (frame invariance of the FOV test)."""
+    r = synth.random_case(22, P=4, E=3)
+    Rm = synth.rotation_matrix(0.3, -0.2, 1.1)
+    rng = np.random.default_rng(5)
+    centre = oracle.grid_points(r["grid"]).mean(axis=0)
+    axes = []
+    for p in range(4):   # boresight roughly at the grid, along-track axis perpendicular to it
+        b = centre - r["tx"][p] + rng.normal(size=3) * 0.2
+        b /= np.linalg.norm(b)
+        a = np.cross(b, rng.normal(size=3)); a /= np.linalg.norm(a)
+        axes.append([a, b])
+    axes = np.array(axes)
+    pts = oracle.grid_points(r["grid"])
+    kw = dict(az=0.15, el=2.0, bistatic=True)
+    g1, cnt = oracle.tdbp_points_gated(r["echoes"], r["tx"], r["rx"], r["t0"], r["fc"], r["fs"], r["c"], pts,
+                                       axes=axes, with_count=True, **kw)
+    g2 = oracle.tdbp_points_gated(r["echoes"], r["tx"] @ Rm.T, r["rx"] @ Rm.T, r["t0"], r["fc"], r["fs"], r["c"],
+                                  pts @ Rm.T, axes=axes @ Rm.T, **kw)
+    assert 0 < cnt.sum() < 4 * 3 * len(pts)             # the gate is active on this grid
+    assert np.max(np.abs(g1 - g2)) <= 1e-9 * np.max(np.abs(g1))
+
+
+def test_gate_cfg1_target_matches_generator_beam():
+    """Config 1 with the generator's own hard beam (az = 0.886 lambda / D, tested at tx): at the
+    target the gated sum equals the dense sum -- out-of-beam pings carry no echo of it -- and the
+    gated image still focuses there with phase ~ 0."""
+    s = synth.scenario(1)
+    e = s.echoes()
+    az = 2 * np.arcsin(s.sin_half_beam)
+    x = s.targets
+    dense = oracle.tdbp_points(e, s.tx, s.rx, s.t0, s.fc, s.fs, s.c, x)[0]
+    gated = oracle.tdbp_points_gated(e, s.tx, s.rx, s.t0, s.fc, s.fs, s.c, x, az=az)[0]
+    assert abs(gated - dense) <= 1e-12 * abs(dense)
+    pts = oracle.grid_points(s.grid, s.sample_pixels(0, window=9))
+    gi = np.abs(oracle.tdbp_points_gated(e, s.tx, s.rx, s.t0, s.fc, s.fs, s.c, pts, az=az))
+    assert np.argmax(gi) == np.argmin(np.linalg.norm(pts - x, axis=1))
