@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-k1", action="store_true")
+    ap.add_argument("--no-gated", action="store_true")
     return ap.parse_args()
 
 
@@ -307,6 +308,28 @@ def run_sasbp(args):
                    "d2h_bytes_per_step": g["nx"] * g["ny"] * g["nz"] * 8, "ms_per_step": e2e_s * 1e3,
                    "api": "pinned H2D on rank 0 + NCCL broadcast + sas_bp_form_device per band + all_gather + D2H"}
 
+    # ---- NEXT-1: the same workload gated to the transmit beam (generator's FWHM), ray culling on
+    gated = None
+    if not args.no_gated and world == 1 and s.sin_half_beam > 0:
+        az = 2 * float(np.arcsin(s.sin_half_beam))
+        bp.set_beam(az, 0.0, False, True)
+        _, g_terms = bp.count_terms()
+        for _ in range(2):
+            bp.form_device(img, stream=stream)
+        torch.cuda.synchronize()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for _ in range(args.steps):
+            bp.form_device(img, stream=stream)
+        g1.record(stream)
+        torch.cuda.synchronize()
+        g_ms = g0.elapsed_time(g1) / args.steps
+        bp.set_beam(None)
+        gated = {"beam": f"azimuth FWHM {az:.4f} rad at tx (monostatic), ray culling on", "ms_per_step": g_ms,
+                 "speedup_vs_dense": (total_ms / args.steps) / g_ms, "in_cone_terms": g_terms,
+                 "in_cone_fraction": g_terms / dense, "in_cone_Gterm_per_s": g_terms / (g_ms * 1e-3) / 1e9,
+                 "dense_equivalent_Gterm_per_s": dense / (g_ms * 1e-3) / 1e9}
+
     # ---- K1 range compression on the same channel layout (row a1), reported separately
     k1 = None
     if not args.no_k1 and rank == 0:
@@ -372,6 +395,7 @@ def run_sasbp(args):
             "e2e": e2e,
             "cpu_baseline": cpu,
             "k1_rangecompress": k1,
+            "next1_gated": gated,
         }
         if cpu:
             out["gpu_over_cpu"] = value / cpu["value"]

@@ -123,7 +123,8 @@ SASBP_API sas_status sas_bp_form_streamed(sas_bp_t h, const float* echoes, int32
 /* Algorithmic work counters of the current ping set (off the clock, for the metric):
  *   dense  = nx*ny*nz*P*E  pixel.ping.element terms;
  *   in_win = the terms whose interpolation support meets the record, u in (-1, Ns)
- *            (SURVEY §8(d) N_u), counted on the device in fp32 (K3).  Either may be NULL. */
+ *            (SURVEY §8(d) N_u), counted on the device in fp32 (K3); with a beam set
+ *            (sas_bp_set_beam) only terms inside the cone(s) are counted.  Either may be NULL. */
 SASBP_API sas_status sas_bp_count_terms(sas_bp_t h, uint64_t* dense, uint64_t* in_win);
 
 /* The execution plan chosen for the current grid and ping set (diagnostics / tests):
@@ -143,6 +144,28 @@ typedef struct {
   int32_t batch;
 } sas_bp_plan;
 SASBP_API sas_status sas_bp_get_plan(sas_bp_t h, sas_bp_plan* out);
+
+/* Field-of-view gating and ray culling (P:160-162 ray culling, P:310/315
+ * bistatic; reading R15).  With a beam set, form computes the GATED sum
+ *   I_g(x) = sum_{p,e} [x in FOV(tx_p)] [bistatic -> x in FOV(rx_{p,e})] term_{p,e}(x)
+ * with hard FWHM cones around per-ping axes a_p (along track) and b_p (boresight), NED unit
+ * vectors: azimuth |v.a| <= |v| sin(az/2), elevation v.b > 0 and |v.(a x b)| <= (v.b) tan(el/2),
+ * v = x - sensor.  Per-point decisions are taken in fp64 (identical to the oracle's); with cull = 1
+ * the kernel skips (tile, channel) pairs whose tile provably misses a cone (exact sphere bound),
+ * which never changes the result.
+ *   beam  NULL -> back to the dense sum; az_fwhm in (0, inf) (>= pi disables the azimuth test),
+ *         el_fwhm finite (<= 0 or >= pi disables the elevation test), bistatic / cull in {0, 1}
+ *   axes  fp64 [P][2][3] = (a_p, b_p) per ping, orthonormal, copied; NULL = a = +x, b = +y
+ *         for every ping (side-looking to starboard).  P must match the ping set at form time
+ *         (else SAS_E_STATE).
+ * Errors: SAS_E_INVALID for bad values or non-orthonormal axes; SAS_E_NOMEM; SAS_E_CUDA. */
+typedef struct {
+  double az_fwhm;
+  double el_fwhm;
+  int32_t bistatic;
+  int32_t cull;
+} sas_beam;
+SASBP_API sas_status sas_bp_set_beam(sas_bp_t h, const sas_beam* beam, const double* axes, int32_t P);
 
 /* Bytes of device memory the handle owns (image + workspace + owned ping copy). */
 SASBP_API size_t sas_bp_workspace_bytes(sas_bp_t h);

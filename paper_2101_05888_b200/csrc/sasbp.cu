@@ -72,6 +72,11 @@ struct sas_bp_s {
   // TMA descriptor of the current echoes (row staging), rebuilt when the ping set changes
   sasbp::TmaDesc tmap{};
   bool use_tma = false;
+  // field-of-view gating (sas_bp_set_beam; NEXT-1)
+  int gate = 0, cull = 0, az_on = 0, el_on = 0;
+  double half_az = 0, sin_half_az = 0, half_el = 0, tan_half_el = 0;
+  double* axes = nullptr;
+  int axes_P = 0;
   bool has_pings = false;
   bool broken = false;
   size_t bytes = 0;
@@ -130,29 +135,22 @@ cudaError_t launch_k(Kern kern, int threads, const sasbp::TdbpParams& prm, const
   return cudaGetLastError();
 }
 
-template <int KX, int KY, int KZ, int WY, int WZ, bool DZ, bool TMA>
-cudaError_t launch_mode(const sasbp::TdbpParams& prm, const sasbp::TmaDesc& tmap, int mode, cudaStream_t st) {
+template <int KX, int KY, int KZ, int WY, int WZ, bool DZ, bool TMA, bool GATE>
+cudaError_t launch_gate(const sasbp::TdbpParams& prm, const sasbp::TmaDesc& tmap, int mode, cudaStream_t st) {
   using namespace sasbp;
   const size_t smem = smem_bytes(prm.W);
   const int nt = 32 * WY * WZ;
-  // axis-aligned plane: step_x along x only and step_y with no x/z part -> x-pairs share dy
-  const bool axis = !DZ && KZ == 1 && prm.sx[1] == 0.0 && prm.sx[2] == 0.0 && prm.sy[2] == 0.0;
-#if SASBP_AXIS
-  if (axis) {
-    switch (mode) {
-      case kSeries3: return launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kSeries3, TMA, true>, nt, prm, tmap, smem, st);
-      case kSeries4: return launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kSeries4, TMA, true>, nt, prm, tmap, smem, st);
-      default: return launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kExact, TMA, true>, nt, prm, tmap, smem, st);
-    }
-  }
-#else
-  (void)axis;
-#endif
   switch (mode) {
-    case kSeries3: return launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kSeries3, TMA>, nt, prm, tmap, smem, st);
-    case kSeries4: return launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kSeries4, TMA>, nt, prm, tmap, smem, st);
-    default: return launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kExact, TMA>, nt, prm, tmap, smem, st);
+    case kSeries3: return launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kSeries3, TMA, GATE>, nt, prm, tmap, smem, st);
+    case kSeries4: return launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kSeries4, TMA, GATE>, nt, prm, tmap, smem, st);
+    default: return launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kExact, TMA, GATE>, nt, prm, tmap, smem, st);
   }
+}
+
+template <int KX, int KY, int KZ, int WY, int WZ, bool DZ, bool TMA>
+cudaError_t launch_mode(const sasbp::TdbpParams& prm, const sasbp::TmaDesc& tmap, int mode, cudaStream_t st) {
+  return prm.gate ? launch_gate<KX, KY, KZ, WY, WZ, DZ, TMA, true>(prm, tmap, mode, st)
+                  : launch_gate<KX, KY, KZ, WY, WZ, DZ, TMA, false>(prm, tmap, mode, st);
 }
 
 template <int KX, int KY, int KZ, int WY, int WZ, bool DZ>
@@ -220,6 +218,11 @@ cudaError_t launch_tdbp(sas_bp_t h, float2* image, unsigned long long* counter, 
   prm.accumulate = accumulate;
   prm.ch_lo = ch_lo;
   prm.ch_hi = ch_hi < 0 ? h->P * h->E : ch_hi;
+  prm.gate = h->gate; prm.cull = h->cull; prm.az_on = h->az_on; prm.el_on = h->el_on;
+  prm.axes = h->axes;
+  prm.sin_half_az = h->sin_half_az; prm.half_az = h->half_az;
+  prm.tan_half_el = h->tan_half_el; prm.half_el = h->half_el;
+  prm.d_max = h->d_max;
   switch (h->variant) {
 #if SASBP_K4
     case V2D: return launch_variant<4, 1, 1, 8, 1, false>(prm, h->tmap, h->use_tma, h->mode, count, st);
@@ -383,6 +386,7 @@ void sas_bp_destroy(sas_bp_t h) {
   cudaFree(h->echoes_owned);
   cudaFree(h->geo);
   cudaFree(h->counter);
+  cudaFree(h->axes);
   if (h->stream) cudaStreamDestroy(h->stream);
   if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
   if (prev >= 0) cudaSetDevice(prev);
@@ -443,6 +447,7 @@ sas_status sas_bp_form_device(sas_bp_t h, void* image_dev, void* cuda_stream, in
   if (((uintptr_t)image_dev) & 7) return fail(SAS_E_INVALID, "image_dev must be 8-byte aligned");
   if (flags & ~SAS_FORM_ACCUMULATE) return fail(SAS_E_INVALID, "unknown flags 0x%x", flags);
   if (!h->has_pings) return fail(SAS_E_STATE, "sas_bp_form before sas_bp_set_pings");
+  if (h->gate && h->axes && h->axes_P != h->P) return fail(SAS_E_STATE, "beam axes were given for %d pings, the ping set has %d", h->axes_P, h->P);
   CK_H(h, cudaSetDevice(h->device));
   CK_H(h, launch_tdbp(h, (float2*)image_dev, h->counter, (flags & SAS_FORM_ACCUMULATE) ? 1 : 0, false,
                       (cudaStream_t)cuda_stream));
@@ -455,6 +460,7 @@ sas_status sas_bp_form(sas_bp_t h, float* image_out) {
   if (h->broken) return fail(SAS_E_CUDA, "handle is in a failed CUDA state; destroy it");
   if (!image_out) return fail(SAS_E_INVALID, "image_out must not be NULL");
   if (!h->has_pings) return fail(SAS_E_STATE, "sas_bp_form before sas_bp_set_pings");
+  if (h->gate && h->axes && h->axes_P != h->P) return fail(SAS_E_STATE, "beam axes were given for %d pings, the ping set has %d", h->axes_P, h->P);
   CK_H(h, cudaSetDevice(h->device));
   CK_H(h, launch_tdbp(h, h->image, h->counter, 0, false, h->stream));
   const size_t npx = (size_t)h->grid.nx * h->grid.ny * h->grid.nz;
@@ -488,6 +494,7 @@ sas_status sas_bp_form_streamed(sas_bp_t h, const float* echoes, int32_t P, int3
   h->echoes = h->echoes_owned;
   h->use_tma = encode_tma(h);
   h->has_pings = true;
+  if (h->gate && h->axes && h->axes_P != h->P) return fail(SAS_E_STATE, "beam axes were given for %d pings, the ping set has %d", h->axes_P, h->P);
   const int nch = P * E;
   int nchunk = chunks > 0 ? chunks : 8;
   nchunk = std::max(1, std::min(nchunk, (nch + 63) / 64));   // >= 64 channels per chunk
@@ -516,6 +523,7 @@ sas_status sas_bp_count_terms(sas_bp_t h, uint64_t* dense, uint64_t* in_win) {
   if (!h) return fail(SAS_E_INVALID, "handle is NULL");
   if (h->broken) return fail(SAS_E_CUDA, "handle is in a failed CUDA state; destroy it");
   if (!h->has_pings) return fail(SAS_E_STATE, "sas_bp_count_terms before sas_bp_set_pings");
+  if (h->gate && h->axes && h->axes_P != h->P) return fail(SAS_E_STATE, "beam axes were given for %d pings, the ping set has %d", h->axes_P, h->P);
   const uint64_t npx = (uint64_t)h->grid.nx * h->grid.ny * h->grid.nz;
   if (dense) *dense = npx * (uint64_t)h->P * (uint64_t)h->E;
   if (in_win) {
@@ -531,6 +539,55 @@ sas_status sas_bp_count_terms(sas_bp_t h, uint64_t* dense, uint64_t* in_win) {
 }
 
 size_t sas_bp_workspace_bytes(sas_bp_t h) { return h ? h->bytes : 0; }
+
+sas_status sas_bp_set_beam(sas_bp_t h, const sas_beam* beam, const double* axes, int32_t P) {
+  g_err[0] = 0;
+  if (!h) return fail(SAS_E_INVALID, "handle is NULL");
+  if (h->broken) return fail(SAS_E_CUDA, "handle is in a failed CUDA state; destroy it");
+  if (!beam) {   // back to the dense sum
+    h->gate = 0;
+    return SAS_OK;
+  }
+  const double pi = 3.141592653589793;
+  if (!std::isfinite(beam->az_fwhm) || !(beam->az_fwhm > 0) || !std::isfinite(beam->el_fwhm))
+    return fail(SAS_E_INVALID, "az_fwhm must be finite and > 0, el_fwhm finite");
+  if (beam->bistatic != 0 && beam->bistatic != 1) return fail(SAS_E_INVALID, "bistatic must be 0 or 1");
+  if (beam->cull != 0 && beam->cull != 1) return fail(SAS_E_INVALID, "cull must be 0 or 1");
+  if (axes) {
+    if (P < 1) return fail(SAS_E_INVALID, "P must be >= 1 when axes are given");
+    for (int32_t p = 0; p < P; ++p) {
+      const double* a = axes + 6 * (size_t)p;
+      const double* b = a + 3;
+      if (!finite3(a) || !finite3(b)) return fail(SAS_E_INVALID, "non-finite axes of ping %d", p);
+      if (std::fabs(norm3(a) - 1.0) > 1e-6 || std::fabs(norm3(b) - 1.0) > 1e-6 ||
+          std::fabs(a[0] * b[0] + a[1] * b[1] + a[2] * b[2]) > 1e-6)
+        return fail(SAS_E_INVALID, "axes of ping %d must be orthonormal (a along track, b boresight)", p);
+    }
+    CK_H(h, cudaSetDevice(h->device));
+    if (h->axes_P != P || !h->axes) {
+      if (h->axes) { cudaFree(h->axes); h->bytes -= (size_t)h->axes_P * 6 * sizeof(double); h->axes = nullptr; }
+      cudaError_t e = cudaMalloc(&h->axes, (size_t)P * 6 * sizeof(double));
+      if (e != cudaSuccess) { h->axes = nullptr; h->axes_P = 0; h->gate = 0; return fail(SAS_E_NOMEM, "cudaMalloc(axes)"); }
+      h->bytes += (size_t)P * 6 * sizeof(double);
+    }
+    CK_H(h, cudaMemcpy(h->axes, axes, (size_t)P * 6 * sizeof(double), cudaMemcpyHostToDevice));
+    h->axes_P = P;
+  } else if (h->axes) {
+    cudaFree(h->axes);
+    h->bytes -= (size_t)h->axes_P * 6 * sizeof(double);
+    h->axes = nullptr;
+    h->axes_P = 0;
+  }
+  h->az_on = beam->az_fwhm < pi ? 1 : 0;
+  h->half_az = 0.5 * beam->az_fwhm;
+  h->sin_half_az = std::sin(0.5 * beam->az_fwhm);   // same libm expression as the oracle's
+  h->el_on = (beam->el_fwhm > 0 && beam->el_fwhm < pi) ? 1 : 0;
+  h->half_el = 0.5 * beam->el_fwhm;
+  h->tan_half_el = h->el_on ? std::tan(0.5 * beam->el_fwhm) : 0.0;
+  h->cull = beam->cull;
+  h->gate = beam->bistatic ? 2 : 1;
+  return SAS_OK;
+}
 
 sas_status sas_bp_get_plan(sas_bp_t h, sas_bp_plan* out) {
   g_err[0] = 0;

@@ -75,6 +75,13 @@ struct TdbpParams {
   int W;                  // window cells per channel (cells j = 0..W-1 use samples k_lo+j, k_lo+j+1)
   int accumulate;
   int ch_lo, ch_hi;       // channel range [ch_lo, ch_hi) of this launch (ch = p * E + e)
+  // field-of-view gating (NEXT-1, reading R15); gate = 0 -> dense sum
+  int gate;               // 1 = gate at tx; 2 = gate at tx and at each rx (bistatic)
+  int cull;               // skip (tile, channel) pairs whose tile sphere misses a cone
+  int az_on, el_on;
+  const double* axes;     // [P][2][3] per-ping along-track axis a, boresight b; NULL = (+x, +y)
+  double sin_half_az, half_az, tan_half_el, half_el;
+  double d_max;           // tile sphere radius (m)
 };
 
 // per-channel constants in shared memory (fp64 prologue output)
@@ -84,7 +91,8 @@ struct __align__(16) ChanConst {
   float urr, phi0, r_r, r2_r;   // centred window coordinate offset; phase offset (rad); r_r; r_r^2
   float tx2x, tx2y, tx2z, r2_t; // tx leg: 2 (c_T - tx), r_t^2
   float r_t, kfs, klo_f, pad1;  // r_t, fs/c, (float) k_lo
-  int ping, woff, klo, pad2;    // ping index; LDS byte offset of cell Wh minus MAGIC*16; window start
+  int ping, woff, klo, gate;    // ping index; LDS byte offset of cell Wh minus MAGIC*16; window start;
+                                // gate classes: bits 0-1 tx, 2-3 rx (kGIn/kGEdge/kGOut), bit 4 = culled
 };
 
 constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23: x + kMagic rounds x to an integer in the low bits
@@ -114,7 +122,79 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 
 __device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
 
-// fp64 prologue for one channel (row a2): reference geometry at the tile centre ct.
+// ---------------------------------------------------------------- FOV gate (NEXT-1, R15)
+constexpr int kGIn = 0, kGEdge = 1, kGOut = 2;
+
+__device__ __forceinline__ void ping_axes(const TdbpParams& prm, int p, double a[3], double b[3]) {
+  if (prm.axes) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i) { a[i] = prm.axes[6 * p + i]; b[i] = prm.axes[6 * p + 3 + i]; }
+  } else {
+    a[0] = 1.0; a[1] = 0.0; a[2] = 0.0; b[0] = 0.0; b[1] = 1.0; b[2] = 0.0;
+  }
+}
+
+// Classify a whole tile (sphere of radius d_max around its centre, v = centre - sensor) against
+// one sensor's cone: kGIn (every point inside), kGOut (every point outside) or kGEdge.  Exact
+// spherical bounds: the angle to the plane perpendicular to a ranges over alpha -/+ beta; the
+// elevation condition depends only on the projection onto span(b, c), a disk of radius d_max.
+__device__ int cone_class(const TdbpParams& prm, const double v[3], const double a[3], const double b[3]) {
+  const double rho = prm.d_max, eps = 1e-9;
+  const double nv = sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
+  if (!(nv > rho)) return kGEdge;
+  int cls = kGIn;
+  if (prm.az_on) {
+    const double beta = asin(rho / nv);
+    const double alpha = asin(fmin(1.0, fabs(v[0] * a[0] + v[1] * a[1] + v[2] * a[2]) / nv));
+    if (alpha - beta > prm.half_az + eps) return kGOut;
+    if (!(alpha + beta < prm.half_az - eps)) cls = kGEdge;
+  }
+  if (prm.el_on) {
+    const double c[3] = {a[1] * b[2] - a[2] * b[1], a[2] * b[0] - a[0] * b[2], a[0] * b[1] - a[1] * b[0]};
+    const double vb = v[0] * b[0] + v[1] * b[1] + v[2] * b[2];
+    const double vc = v[0] * c[0] + v[1] * c[1] + v[2] * c[2];
+    const double rp = sqrt(vb * vb + vc * vc);
+    if (!(rp > rho)) return kGEdge;
+    const double be = asin(rho / rp), el = atan2(fabs(vc), vb);
+    if (el - be > prm.half_el + eps) return kGOut;
+    if (!(el + be < prm.half_el - eps)) cls = kGEdge;
+  }
+  return cls;
+}
+
+// Per-point test, evaluated in fp64 in the definition's order of operations (no contraction),
+// so the decision is the plain fp64 one the test-side reference takes (R15).
+__device__ bool in_fov_px(const TdbpParams& prm, const double x[3], const double* s, const double a[3],
+                          const double b[3]) {
+  const double v0 = __dsub_rn(x[0], s[0]), v1 = __dsub_rn(x[1], s[1]), v2 = __dsub_rn(x[2], s[2]);
+  if (prm.az_on) {
+    const double nv = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(v0, v0), __dmul_rn(v1, v1)), __dmul_rn(v2, v2)));
+    const double va = __dadd_rn(__dadd_rn(__dmul_rn(v0, a[0]), __dmul_rn(v1, a[1])), __dmul_rn(v2, a[2]));
+    if (fabs(va) > __dmul_rn(nv, prm.sin_half_az)) return false;
+  }
+  if (prm.el_on) {
+    const double c0 = __dsub_rn(__dmul_rn(a[1], b[2]), __dmul_rn(a[2], b[1]));
+    const double c1 = __dsub_rn(__dmul_rn(a[2], b[0]), __dmul_rn(a[0], b[2]));
+    const double c2 = __dsub_rn(__dmul_rn(a[0], b[1]), __dmul_rn(a[1], b[0]));
+    const double vb = __dadd_rn(__dadd_rn(__dmul_rn(v0, b[0]), __dmul_rn(v1, b[1])), __dmul_rn(v2, b[2]));
+    const double vc = __dadd_rn(__dadd_rn(__dmul_rn(v0, c0), __dmul_rn(v1, c1)), __dmul_rn(v2, c2));
+    if (!(vb > 0) || fabs(vc) > __dmul_rn(vb, prm.tan_half_el)) return false;
+  }
+  return true;
+}
+
+// Pixel centre in fp64, oracle order: ((origin + ix sx) + iy sy) + iz sz (reading R8)
+__device__ __forceinline__ void pixel_centre64(const TdbpParams& prm, int ix, int iy, int iz, double x[3]) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+    x[i] = __dadd_rn(__dadd_rn(__dadd_rn(prm.origin[i], __dmul_rn((double)ix, prm.sx[i])),
+                               __dmul_rn((double)iy, prm.sy[i])),
+                     __dmul_rn((double)iz, prm.sz[i]));
+}
+
+// fp64 prologue for one channel (row a2): reference geometry at the tile centre ct (and, for
+// gated kernels, the tile's cone classes).
+template <bool GATE>
 __device__ __forceinline__ ChanConst chan_prologue(const TdbpParams& prm, int ch, const double ct[3], int slot,
                                                    uint32_t win_base) {
   const int p = (int)(((double)ch + 0.5) * prm.inv_e);   // ch / E, exact for ch < 2^40
@@ -154,7 +234,21 @@ __device__ __forceinline__ ChanConst chan_prologue(const TdbpParams& prm, int ch
   k.ping = p;
   k.woff = (int)(win_base + (uint32_t)(slot * prm.W + Wh) * 16u - (uint32_t)kMagicBits * 16u);
   k.klo = klo;
-  k.pad2 = 0;
+  k.gate = 0;
+  if (GATE && prm.gate) {
+    double a[3], b[3];
+    ping_axes(prm, p, a, b);
+    const double vt[3] = {utx, uty, utz};
+    const int ct_cls = cone_class(prm, vt, a, b);
+    int cr_cls = kGIn;
+    if (prm.gate == 2) {
+      const double vr[3] = {urx, ury, urz};
+      cr_cls = cone_class(prm, vr, a, b);
+    }
+    const bool culled = prm.cull && (ct_cls == kGOut || cr_cls == kGOut);
+    // without culling an OUT class is evaluated per pixel like an edge
+    k.gate = (ct_cls == kGOut ? kGEdge : ct_cls) | ((cr_cls == kGOut ? kGEdge : cr_cls) << 2) | (culled ? 16 : 0);
+  }
   return k;
 }
 
@@ -206,7 +300,7 @@ __host__ __device__ inline size_t raw_slot_bytes(int W) { return ((size_t)box_sa
 #endif
 constexpr int kBPW = SASBP_BPW;
 constexpr int kRing = 8 * kBPW;   // ChanConst batches kept in shared memory (prologues run ahead)
-__host__ __device__ inline size_t k2_raw_off() { return (kRing * kNB * sizeof(ChanConst) + 16 + 127) & ~(size_t)127; }
+__host__ __device__ inline size_t k2_raw_off() { return (kRing * kNB * sizeof(ChanConst) + 32 + 127) & ~(size_t)127; }
 __host__ __device__ inline size_t k2_win_off(int W) { return k2_raw_off() + kNB * raw_slot_bytes(W); }
 __host__ __device__ inline size_t k2_smem_bytes(int W) { return k2_win_off(W) + (size_t)kNB * W * sizeof(float4) + 128; }
 
@@ -235,7 +329,8 @@ struct __align__(64) TmaDesc { unsigned char bytes[128]; };
 
 // HAS_DZ = false means the grid is a z-level plane (step_x, step_y have no z component); then
 // both pixels of an x-pair share their y offset whenever step_x has no y component (AXIS).
-template <int KX, int KY, int KZ, int WY, int WZ, bool HAS_DZ, int MODE, bool USE_TMA, bool AXIS = false>
+template <int KX, int KY, int KZ, int WY, int WZ, bool HAS_DZ, int MODE, bool USE_TMA, bool GATE = false,
+          bool AXIS = false>
 __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp_kernel(const TdbpParams prm,
                                                                           const __grid_constant__ TmaDesc tmap) {
   using TM = TileMap<KX, KY, KZ, WY, WZ>;
@@ -246,6 +341,7 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
   unsigned char* sbase = smem_raw + ((128 - ((uint32_t)__cvta_generic_to_shared(smem_raw) & 127)) & 127);
   ChanConst* cc = reinterpret_cast<ChanConst*>(sbase);                       // [kRing][kNB]
   const uint32_t bar = (uint32_t)__cvta_generic_to_shared(sbase + kRing * kNB * sizeof(ChanConst));
+  const uint32_t zcell = bar + 16;   // a zero float4: the cell gated-out terms read
   const int W = prm.W;
   const uint32_t rsb = (uint32_t)raw_slot_bytes(W);
   unsigned char* rawp = sbase + k2_raw_off();
@@ -285,9 +381,12 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
   const int P2 = (W + 1) >> 1;                // cell pairs per channel
   const float inv_p2 = 1.0f / (float)P2;
 
-  if (USE_TMA && tid == 0) {
-    mbar_init(bar, kWarps);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  if (tid == 0) {
+    if (USE_TMA) {
+      mbar_init(bar, kWarps);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("st.shared.v4.f32 [%0], {%1, %1, %1, %1};" ::"r"(zcell), "f"(0.f) : "memory");
   }
   __syncthreads();
 
@@ -301,7 +400,7 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
     if (sub < kBPW && bb < nbatch) {
       const int nbb = min(kNB, nch - bb * kNB);
       if (cl < nbb)
-        cc[(bb % kRing) * kNB + cl] = chan_prologue(prm, prm.ch_lo + bb * kNB + cl, ct, cl, win_base);
+        cc[(bb % kRing) * kNB + cl] = chan_prologue<GATE>(prm, prm.ch_lo + bb * kNB + cl, ct, cl, win_base);
     }
   };
   // window loads of batch b: warp w issues the rows of channels [w*kCW, (w+1)*kCW); every warp
@@ -315,11 +414,16 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
     const int mine = max(0, min(kCW, nb - c0));
     if (USE_TMA) {
       if (lane == 0) {
-        mbar_expect_tx(bar, (uint32_t)(mine * nbox * 8));
-        for (int c = c0; c < c0 + mine; ++c) tma_load_row(raw_base + c * rsb, &tmap, cb[c].klo, ch0 + c, bar);
+        int live = mine;
+        if (GATE)
+          for (int c = c0; c < c0 + mine; ++c) live -= (cb[c].gate >> 4) & 1;
+        mbar_expect_tx(bar, (uint32_t)(live * nbox * 8));
+        for (int c = c0; c < c0 + mine; ++c)
+          if (!GATE || !(cb[c].gate & 16)) tma_load_row(raw_base + c * rsb, &tmap, cb[c].klo, ch0 + c, bar);
       }
     } else {
       for (int c = c0; c < c0 + mine; ++c) {
+        if (GATE && (cb[c].gate & 16)) continue;
         const int klo = cb[c].klo;
         const float2* row = prm.echoes + (size_t)(ch0 + c) * prm.Ns;
         const uint32_t dst = raw_base + c * rsb;
@@ -337,6 +441,7 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
   __syncthreads();
   issue(0);
   int cur_ping = -1;
+  uint32_t mtx = 0xFFu;   // transmit-cone pixel mask of the current ping (GATE)
 
   for (int b = 0; b < nbatch; ++b) {
     const int nb = min(kNB, nch - b * kNB);
@@ -369,6 +474,7 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
         const int q = (int)(((float)i + 0.5f) * inv_p2);   // i / P2, exact for i < 2^20
         const int t = i - q * P2;
         const int c = warp + q * kWarps;
+        if (GATE && (cc[(b % kRing) * kNB + c].gate & 16)) continue;
         const float2* rw = reinterpret_cast<const float2*>(rawp + c * rsb) + 2 * t;
         const float4 d01 = *reinterpret_cast<const float4*>(rw);
         const float2 d2 = rw[2];
@@ -396,8 +502,22 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
 #endif
     for (int c = 0; c < nb; ++c) {
       const ChanConst kc = cb[c];
+      if (GATE && (kc.gate & 16)) continue;                 // culled: tile outside a cone
       if (kc.ping != cur_ping) {
         cur_ping = kc.ping;
+        if (GATE) {   // transmit-cone mask of this thread's pixels for the new ping
+          mtx = 0xFFu;
+          if ((kc.gate & 3) == kGEdge) {
+            double a[3], bb[3], x[3];
+            ping_axes(prm, cur_ping, a, bb);
+            mtx = 0u;
+#pragma unroll
+            for (int k = 0; k < 2 * NP; ++k) {
+              pixel_centre64(prm, tm.ix(k), tm.iy(k), tm.iz(k), x);
+              if (in_fov_px(prm, x, prm.tx + 3 * cur_ping, a, bb)) mtx |= 1u << k;
+            }
+          }
+        }
         // transmit leg, exact range-relative form: dR = q / (sqrt(r^2 + q) + r), in samples
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
@@ -409,6 +529,22 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
           const float den1 = fmaf(r2.y, rsqrt_approx(r2.y), kc.r_t);
           BT[p] = __fmul2_rn(__fmul2_rn(q, make_float2(rcp_approx(den0), rcp_approx(den1))), f2(kc.kfs));
         }
+      }
+      uint32_t msk = 0xFFu;
+      bool masked = false;
+      if (GATE) {
+        msk = mtx;
+        if (((kc.gate >> 2) & 3) == kGEdge) {   // receive-cone mask (bistatic), per channel
+          double a[3], bb[3], x[3];
+          ping_axes(prm, kc.ping, a, bb);
+          const int chg = prm.ch_lo + b * kNB + c;
+#pragma unroll
+          for (int k = 0; k < 2 * NP; ++k) {
+            pixel_centre64(prm, tm.ix(k), tm.iy(k), tm.iz(k), x);
+            if (!in_fov_px(prm, x, prm.rx + 3 * (size_t)chg, a, bb)) msk &= ~(1u << k);
+          }
+        }
+        masked = (kc.gate & 3) == kGEdge || ((kc.gate >> 2) & 3) == kGEdge;   // warp-uniform
       }
 #pragma unroll
       for (int p = 0; p < NP; ++p) {
@@ -440,7 +576,12 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
           const float Us = s ? U.y : U.x;
           const float Ts = s ? T.y : T.x;
           const float phs = s ? ph.y : ph.x;
-          const float4 w = lds128((uint32_t)__float_as_int(Ts) * 16u + (uint32_t)kc.woff);
+          uint32_t addr = (uint32_t)__float_as_int(Ts) * 16u + (uint32_t)kc.woff;
+          if (GATE && masked) {   // gated-out pixel: read the zero cell
+            const uint32_t mk = 0u - ((msk >> (2 * p + s)) & 1u);
+            addr = (addr & mk) | (zcell & ~mk);
+          }
+          const float4 w = lds128(addr);
           const float2 eh = __ffma2_rn(f2(Us), make_float2(w.z, w.w), make_float2(w.x, w.y));
           float sn, cs;
           __sincosf(phs, &sn, &cs);
@@ -487,7 +628,7 @@ __global__ void __launch_bounds__(32 * WY * WZ) count_kernel(const TdbpParams pr
   for (int ch0 = prm.ch_lo; ch0 < prm.ch_hi; ch0 += kNB) {
     const int nb = min(kNB, prm.ch_hi - ch0);
     __syncthreads();
-    if (tid < nb) cc[tid] = chan_prologue(prm, ch0 + tid, ct, tid, 0u);
+    if (tid < nb) cc[tid] = chan_prologue<false>(prm, ch0 + tid, ct, tid, 0u);
     __syncthreads();
     for (int c = 0; c < nb; ++c) {
       const ChanConst kc = cc[c];
@@ -499,7 +640,15 @@ __global__ void __launch_bounds__(32 * WY * WZ) count_kernel(const TdbpParams pr
         const float du = (qt / (rt + kc.r_t) + qr / (rr + kc.r_r)) * kc.kfs;
         // absolute u = k_lo + 0.5 + Wh + (du + urr)
         const float ua = kc.klo_f + 0.5f + (float)(prm.W >> 1) + (du + kc.urr);
-        cnt += (ok[k] && ua > -1.f && ua < Nsf) ? 1u : 0u;
+        bool admit = ok[k] && ua > -1.f && ua < Nsf;
+        if (prm.gate && admit) {   // gated metric: count only terms inside the cone(s), fp64 decision
+          double a[3], bb[3], x[3];
+          ping_axes(prm, kc.ping, a, bb);
+          pixel_centre64(prm, tm.ix(k), tm.iy(k), tm.iz(k), x);
+          admit = in_fov_px(prm, x, prm.tx + 3 * kc.ping, a, bb) &&
+                  (prm.gate != 2 || in_fov_px(prm, x, prm.rx + 3 * (size_t)(ch0 + c), a, bb));
+        }
+        cnt += admit ? 1u : 0u;
       }
     }
   }

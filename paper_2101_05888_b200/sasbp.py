@@ -22,7 +22,7 @@ _NAMES = {0: "SAS_OK", -1: "SAS_E_INVALID", -2: "SAS_E_STATE", -3: "SAS_E_NOMEM"
 
 EXPORTS = ("sas_bp_create", "sas_bp_destroy", "sas_bp_set_pings", "sas_bp_set_pings_device", "sas_bp_form",
            "sas_bp_form_device", "sas_bp_count_terms", "sas_bp_workspace_bytes", "sas_rangecompress",
-           "sas_rangecompress_device", "sas_last_error", "sas_version", "sas_bp_get_plan", "sas_bp_form_streamed")
+           "sas_rangecompress_device", "sas_last_error", "sas_version", "sas_bp_get_plan", "sas_bp_form_streamed", "sas_bp_set_beam")
 
 
 class SasError(RuntimeError):
@@ -34,6 +34,11 @@ class SasError(RuntimeError):
 class sas_bp_plan(ctypes.Structure):
     _fields_ = [("tile", ctypes.c_int32 * 3), ("window", ctypes.c_int32), ("rx_mode", ctypes.c_int32),
                 ("tma", ctypes.c_int32), ("batch", ctypes.c_int32)]
+
+
+class sas_beam(ctypes.Structure):
+    _fields_ = [("az_fwhm", ctypes.c_double), ("el_fwhm", ctypes.c_double), ("bistatic", ctypes.c_int32),
+                ("cull", ctypes.c_int32)]
 
 
 class sas_grid(ctypes.Structure):
@@ -72,9 +77,12 @@ def load_library(path: Optional[str] = None):
         "sas_version": ([], ctypes.c_char_p),
         "sas_bp_get_plan": ([vp, ctypes.POINTER(sas_bp_plan)], ctypes.c_int),
         "sas_bp_form_streamed": ([vp, f32p, i32, i32, i32, f64p, f64p, f64p, f32p, i32], ctypes.c_int),
+        "sas_bp_set_beam": ([vp, ctypes.POINTER(sas_beam), f64p, i32], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
-        fn = getattr(lib, name)
+        fn = getattr(lib, name, None)
+        if fn is None:   # an older A/B build without this entry point
+            continue
         fn.argtypes = args
         fn.restype = res
     _lib = lib
@@ -250,6 +258,17 @@ class Backprojector:
         d, w = ctypes.c_uint64(), ctypes.c_uint64()
         _check(_lib.sas_bp_count_terms(self._h, ctypes.byref(d), ctypes.byref(w)))
         return int(d.value), int(w.value)
+
+    def set_beam(self, az_fwhm=None, el_fwhm: float = 0.0, bistatic: bool = False, cull: bool = True, axes=None):
+        """Gate the sum to the transmit (and, bistatic, receive) FOV cones (NEXT-1); az_fwhm=None
+        returns to the dense sum.  axes: [P][2][3] per-ping (along-track, boresight) or None."""
+        if az_fwhm is None:
+            _check(_lib.sas_bp_set_beam(self._h, None, None, 0))
+            return
+        b = sas_beam(float(az_fwhm), float(el_fwhm), 1 if bistatic else 0, 1 if cull else 0)
+        ax = None if axes is None else np.ascontiguousarray(axes, dtype=np.float64)
+        P = 0 if ax is None else ax.shape[0]
+        _check(_lib.sas_bp_set_beam(self._h, ctypes.byref(b), _ptr(ax, ctypes.c_double), P))
 
     def plan(self) -> dict:
         """The execution plan (tile, window, rx_mode, tma, batch) -- sas_bp_get_plan."""

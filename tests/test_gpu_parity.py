@@ -383,3 +383,101 @@ def test_form_streamed_matches_form(bpmod, chunks):
         assert np.array_equal(got, ref)
     assert np.max(np.abs(got - ref)) <= 1e-5 * np.max(np.abs(ref))
     assert np.array_equal(again, ref)
+
+
+# ------------------------------------------------------------------ NEXT-1: FOV gating + ray culling
+
+def _gated_ref(s, e, grid, az, el=0.0, bistatic=False, axes=None, idx=None):
+    pts = oracle.grid_points(grid, idx)
+    v = oracle.tdbp_points_gated(e, s.tx, s.rx, s.t0, s.fc, s.fs, s.c, pts, az=az, el=el, bistatic=bistatic,
+                                 axes=axes)
+    if idx is None:
+        return v.reshape(grid["nz"], grid["ny"], grid["nx"])
+    return v
+
+
+def _gated_form(bpmod, s, e, az, el=0.0, bistatic=False, cull=True, axes=None):
+    with bpmod.Backprojector(s.fc, s.bandwidth, s.fs, s.c, s.grid) as bp:
+        bp.set_pings(e, s.tx, s.rx, s.t0)
+        bp.set_beam(az, el, bistatic, cull, axes)
+        img = bp.form()
+        counts = bp.count_terms()
+    return img, counts
+
+
+@pytest.mark.parametrize("bistatic", [False, True])
+def test_gated_stripmap_vs_oracle(bpmod, bistatic):
+    """Gated sum with the generator's azimuth beam (P:160 FOV query; R15) on reduced config 2."""
+    s = synth.scenario(2, reduced=True)
+    e = s.echoes()
+    az = 2 * np.arcsin(s.sin_half_beam)
+    got, (dense, inwin) = _gated_form(bpmod, s, e, az, bistatic=bistatic)
+    ref = _gated_ref(s, e, s.grid, az, bistatic=bistatic)
+    pk = s.target_pixels
+    _check(got, ref, _at(got, pk), _at(ref, pk), label=f"gated bistatic={bistatic}")
+    _, cnt = oracle.tdbp_points_gated(e, s.tx, s.rx, s.t0, s.fc, s.fs, s.c, oracle.grid_points(s.grid), az=az,
+                                      bistatic=bistatic, with_count=True)
+    assert inwin == int(cnt.sum())       # fp64 gate decisions identical to the oracle's
+    assert 0 < inwin < dense
+
+
+def test_gated_near_field_3d_bistatic_elevation(bpmod):
+    """Bistatic gating with azimuth + elevation cones on the downward-looking 3D array
+    (P:310/315 near-field bistatic culling), per-ping axes a = +x, b = +z (down)."""
+    s = synth.scenario(4, reduced=True)
+    e = s.echoes()
+    axes = np.tile(np.array([[[1.0, 0, 0], [0, 0, 1.0]]]), (s.P, 1, 1))
+    got, _ = _gated_form(bpmod, s, e, az=0.6, el=0.9, bistatic=True, axes=axes)
+    ref = _gated_ref(s, e, s.grid, 0.6, 0.9, True, axes)
+    _check(got, ref, label="gated 3D bistatic")
+
+
+def test_culled_equals_unculled_bitwise(bpmod):
+    """S:389 cardinal property: ray culling changes run time, never pixel values."""
+    s = synth.scenario(2, reduced=True)
+    e = s.echoes()
+    az = 2 * np.arcsin(s.sin_half_beam)
+    a, _ = _gated_form(bpmod, s, e, az, cull=True)
+    b, _ = _gated_form(bpmod, s, e, az, cull=False)
+    assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+
+
+def test_open_gate_equals_dense_bitwise(bpmod):
+    """A gate with both tests disabled admits every term: identical to the dense image."""
+    s = synth.scenario(2, reduced=True)
+    e = s.echoes()
+    dense = _form(bpmod, s, e)
+    got, _ = _gated_form(bpmod, s, e, az=np.pi, el=0.0)
+    assert np.array_equal(got.view(np.uint32), dense.view(np.uint32))
+    with bpmod.Backprojector(s.fc, s.bandwidth, s.fs, s.c, s.grid) as bp:   # set_beam(None) = dense again
+        bp.set_pings(e, s.tx, s.rx, s.t0)
+        bp.set_beam(0.3)
+        bp.set_beam(None)
+        assert np.array_equal(bp.form().view(np.uint32), dense.view(np.uint32))
+
+
+def test_set_beam_errors(bpmod):
+    s = synth.scenario(1)
+    with bpmod.Backprojector(s.fc, s.bandwidth, s.fs, s.c, s.grid) as bp:
+        bp.set_pings(s.echoes(), s.tx, s.rx, s.t0)
+        with pytest.raises(bpmod.SasError) as ei:
+            bp.set_beam(0.3, axes=np.tile(np.array([[[1.0, 0, 0], [1.0, 0, 0]]]), (s.P, 1, 1)))
+        assert ei.value.status == -1
+        bp.set_beam(0.3, axes=np.tile(np.array([[[1.0, 0, 0], [0, 1.0, 0]]]), (s.P + 1, 1, 1)))
+        with pytest.raises(bpmod.SasError) as ei:
+            bp.form()
+        assert ei.value.status == -2
+
+
+def test_gated_full_size_cfg2_sampled(bpmod):
+    """Gated + culled at the full config-2 size: sampled pixels vs the gated oracle."""
+    s = synth.scenario(2)
+    e = s.echoes()
+    az = 2 * np.arcsin(s.sin_half_beam)
+    with bpmod.Backprojector(s.fc, s.bandwidth, s.fs, s.c, s.grid) as bp:
+        bp.set_pings(e, s.tx, s.rx, s.t0)
+        bp.set_beam(az)
+        got = bp.form()
+    idx = s.sample_pixels(2048, window=7, seed=7)
+    ref = _gated_ref(s, e, s.grid, az, idx=idx)
+    _check(_at(got, idx), ref, label="gated cfg2 full")
