@@ -202,6 +202,26 @@ __device__ __forceinline__ ChanConst chan_prologue(const TdbpParams& prm, int ch
   const double* R = prm.rx + 3 * (size_t)ch;
   const double utx = ct[0] - T[0], uty = ct[1] - T[1], utz = ct[2] - T[2];
   const double urx = ct[0] - R[0], ury = ct[1] - R[1], urz = ct[2] - R[2];
+  int gate_bits = 0;
+  if (GATE && prm.gate) {   // cone classes of the tile first: a culled channel needs nothing else
+    double a[3], b[3];
+    ping_axes(prm, p, a, b);
+    const double vt[3] = {utx, uty, utz};
+    const int ct_cls = cone_class(prm, vt, a, b);
+    int cr_cls = kGIn;
+    if (prm.gate == 2 && !(prm.cull && ct_cls == kGOut)) {
+      const double vr[3] = {urx, ury, urz};
+      cr_cls = cone_class(prm, vr, a, b);
+    }
+    if (prm.cull && (ct_cls == kGOut || cr_cls == kGOut)) {
+      ChanConst k{};
+      k.ping = p;
+      k.gate = 16;
+      return k;
+    }
+    // without culling an OUT class is evaluated per pixel like an edge
+    gate_bits = (ct_cls == kGOut ? kGEdge : ct_cls) | ((cr_cls == kGOut ? kGEdge : cr_cls) << 2);
+  }
   const double r_t = sqrt(utx * utx + uty * uty + utz * utz);
   const double r_r = sqrt(urx * urx + ury * ury + urz * urz);
   const double S = r_t + r_r;
@@ -234,21 +254,7 @@ __device__ __forceinline__ ChanConst chan_prologue(const TdbpParams& prm, int ch
   k.ping = p;
   k.woff = (int)(win_base + (uint32_t)(slot * prm.W + Wh) * 16u - (uint32_t)kMagicBits * 16u);
   k.klo = klo;
-  k.gate = 0;
-  if (GATE && prm.gate) {
-    double a[3], b[3];
-    ping_axes(prm, p, a, b);
-    const double vt[3] = {utx, uty, utz};
-    const int ct_cls = cone_class(prm, vt, a, b);
-    int cr_cls = kGIn;
-    if (prm.gate == 2) {
-      const double vr[3] = {urx, ury, urz};
-      cr_cls = cone_class(prm, vr, a, b);
-    }
-    const bool culled = prm.cull && (ct_cls == kGOut || cr_cls == kGOut);
-    // without culling an OUT class is evaluated per pixel like an edge
-    k.gate = (ct_cls == kGOut ? kGEdge : ct_cls) | ((cr_cls == kGOut ? kGEdge : cr_cls) << 2) | (culled ? 16 : 0);
-  }
+  k.gate = gate_bits;
   return k;
 }
 
@@ -300,7 +306,10 @@ __host__ __device__ inline size_t raw_slot_bytes(int W) { return ((size_t)box_sa
 #endif
 constexpr int kBPW = SASBP_BPW;
 constexpr int kRing = 8 * kBPW;   // ChanConst batches kept in shared memory (prologues run ahead)
-__host__ __device__ inline size_t k2_raw_off() { return (kRing * kNB * sizeof(ChanConst) + 32 + 127) & ~(size_t)127; }
+// after the ring: mbarrier (8 B, +8 pad), zero cell (16 B), per-slot batch-live flags (kRing ints)
+__host__ __device__ inline size_t k2_raw_off() {
+  return (kRing * kNB * sizeof(ChanConst) + 32 + kRing * 4 + 127) & ~(size_t)127;
+}
 __host__ __device__ inline size_t k2_win_off(int W) { return k2_raw_off() + kNB * raw_slot_bytes(W); }
 __host__ __device__ inline size_t k2_smem_bytes(int W) { return k2_win_off(W) + (size_t)kNB * W * sizeof(float4) + 128; }
 
@@ -342,6 +351,7 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
   ChanConst* cc = reinterpret_cast<ChanConst*>(sbase);                       // [kRing][kNB]
   const uint32_t bar = (uint32_t)__cvta_generic_to_shared(sbase + kRing * kNB * sizeof(ChanConst));
   const uint32_t zcell = bar + 16;   // a zero float4: the cell gated-out terms read
+  volatile int* blive = reinterpret_cast<int*>(sbase + kRing * kNB * sizeof(ChanConst) + 32);   // [kRing]
   const int W = prm.W;
   const uint32_t rsb = (uint32_t)raw_slot_bytes(W);
   unsigned char* rawp = sbase + k2_raw_off();
@@ -387,6 +397,7 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     asm volatile("st.shared.v4.f32 [%0], {%1, %1, %1, %1};" ::"r"(zcell), "f"(0.f) : "memory");
+    for (int i = 0; i < kRing; ++i) blive[i] = 1;
   }
   __syncthreads();
 
@@ -397,16 +408,25 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
   auto prologue_group = [&](int g) {
     const int sub = lane / kNB, cl = lane % kNB;
     const int bb = g + warp * kBPW + sub;
+    bool live = false;
     if (sub < kBPW && bb < nbatch) {
       const int nbb = min(kNB, nch - bb * kNB);
-      if (cl < nbb)
-        cc[(bb % kRing) * kNB + cl] = chan_prologue<GATE>(prm, prm.ch_lo + bb * kNB + cl, ct, cl, win_base);
+      if (cl < nbb) {
+        const ChanConst k = chan_prologue<GATE>(prm, prm.ch_lo + bb * kNB + cl, ct, cl, win_base);
+        cc[(bb % kRing) * kNB + cl] = k;
+        live = !(k.gate & 16);
+      }
+    }
+    if (GATE) {   // a batch with every channel culled is skipped as a whole
+      const unsigned m = __ballot_sync(0xffffffffu, live);
+      if (cl == 0 && sub < kBPW && bb < nbatch) blive[bb % kRing] = ((m >> (sub * kNB)) & ((1u << kNB) - 1u)) != 0u;
     }
   };
   // window loads of batch b: warp w issues the rows of channels [w*kCW, (w+1)*kCW); every warp
   // arrives once on the batch's mbarrier with the byte count of its rows.
   constexpr int kCW = kNB / kWarps;
   auto issue = [&](int b) {
+    if (GATE && !blive[b % kRing]) return;   // dead batch: no loads, no mbarrier phase
     const int nb = min(kNB, nch - b * kNB);
     const int ch0 = prm.ch_lo + b * kNB;
     const ChanConst* cb = cc + (b % kRing) * kNB;
@@ -443,11 +463,16 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
   int cur_ping = -1;
   uint32_t mtx = 0xFFu;   // transmit-cone pixel mask of the current ping (GATE)
 
+  uint32_t phase = 0;   // mbarrier parity of the next live batch
   for (int b = 0; b < nbatch; ++b) {
     const int nb = min(kNB, nch - b * kNB);
-    if (USE_TMA) mbar_wait(bar, (uint32_t)(b & 1));
-    else cp_async_wait_all();
+    const bool live = !GATE || blive[b % kRing] != 0;   // warp-uniform (set >= 2 barriers ago)
+    if (live) {
+      if (USE_TMA) { mbar_wait(bar, phase); phase ^= 1u; }
+      else cp_async_wait_all();
+    }
     __syncthreads();   // raw(b) landed; every warp is done with win(b-1)
+    if (live) {
     // rewrite raw windows as (intercept, slope) cells; cell j serves u in [k_lo+j, k_lo+j+1]:
     //   slope = d1 - d0,  intercept = d0 + (0.5 - (j - Wh)) * slope   (ehat = intercept + U slope)
 #if SASBP_FLAT_TRANSFORM
@@ -491,8 +516,10 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
     }
 #endif
     __syncthreads();   // win(b) complete; raw free
+    }
     if (b + 1 < nbatch) issue(b + 1);
     if ((b + 2) % kGroup == 0) prologue_group(b + 2);   // batches b+2 .. b+1+kGroup (ring slots not in use)
+    if (!live) continue;
     const ChanConst* cb = cc + (b % kRing) * kNB;
 
 #if SASBP_CUNROLL2
