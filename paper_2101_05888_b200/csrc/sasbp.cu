@@ -20,6 +20,9 @@
 
 #include "tdbp_kernel.cuh"
 
+#ifndef SASBP_ROTATE
+#define SASBP_ROTATE 0
+#endif
 #ifndef SASBP_K4
 #define SASBP_K4 0
 #endif
@@ -124,13 +127,22 @@ double dist_to_box(const double* p, const double lo[3], const double hi[3]) {
 }
 
 template <typename Kern>
-cudaError_t launch_k(Kern kern, int threads, const sasbp::TdbpParams& prm, const sasbp::TmaDesc& tmap, size_t smem,
-                     cudaStream_t st) {
-  const unsigned blocks = (unsigned)prm.tiles_x * prm.tiles_y * prm.tiles_z;
+cudaError_t launch_k(Kern kern, int threads, const sasbp::TdbpParams& prm_in, const sasbp::TmaDesc& tmap,
+                     size_t smem, cudaStream_t st) {
+  const unsigned blocks = (unsigned)prm_in.tiles_x * prm_in.tiles_y * prm_in.tiles_z;
   if (smem > 0) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
+  sasbp::TdbpParams prm = prm_in;
+  int per_sm = 0, dev = 0, sms = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem) == cudaSuccess &&
+      cudaGetDevice(&dev) == cudaSuccess &&
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess)
+    prm.resident = per_sm * sms;
+#if !SASBP_ROTATE
+  prm.resident = 0;
+#endif
   kern<<<blocks, threads, smem, st>>>(prm, tmap);
   return cudaGetLastError();
 }

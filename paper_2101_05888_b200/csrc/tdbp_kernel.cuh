@@ -45,6 +45,9 @@ namespace sasbp {
 #ifndef SASBP_CUNROLL2
 #define SASBP_CUNROLL2 0
 #endif
+#ifndef SASBP_TILE_GROUP
+#define SASBP_TILE_GROUP 8   // tiles per side of the square groups the launch order walks
+#endif
 #ifndef SASBP_NB
 #define SASBP_NB 16
 #endif
@@ -75,6 +78,7 @@ struct TdbpParams {
   int W;                  // window cells per channel (cells j = 0..W-1 use samples k_lo+j, k_lo+j+1)
   int accumulate;
   int ch_lo, ch_hi;       // channel range [ch_lo, ch_hi) of this launch (ch = p * E + e)
+  int resident;           // co-resident CTAs of the launch (SMs x CTAs/SM) for the channel rotation
   // field-of-view gating (NEXT-1, reading R15); gate = 0 -> dense sum
   int gate;               // 1 = gate at tx; 2 = gate at tx and at each rx (bistatic)
   int cull;               // skip (tile, channel) pairs whose tile sphere misses a cone
@@ -269,10 +273,20 @@ struct TileMap {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     lx = lane >> 2; ly = lane & 3;          // quarter-warp = 4 (y) x 2 (x) pixel patch
     wy = warp % WY; wz = warp / WY;
-    int b = blockIdx.x;
-    const int tix = b % prm.tiles_x; b /= prm.tiles_x;
-    const int tiy = b % prm.tiles_y; b /= prm.tiles_y;
-    x0 = tix * TX; y0 = tiy * TY; z0 = b * TZ;
+    // Tile order: square groups of G x G tiles (row-major inside a group, groups row-major)
+    // so the CTAs resident at one time cover a compact patch of the image; their windows
+    // of a channel then overlap and a channel comes from DRAM once per wave (L2 reuse).
+    const int nxy = prm.tiles_x * prm.tiles_y;
+    const int b = blockIdx.x % nxy, bz = blockIdx.x / nxy;
+    constexpr int G = SASBP_TILE_GROUP;
+    const int sr = b / (G * prm.tiles_x);                       // super-row of G tile rows
+    const int gh = min(G, prm.tiles_y - sr * G);
+    const int r = b - sr * G * prm.tiles_x;
+    const int gi = r / (G * gh);                                 // group (G columns) in the super-row
+    const int gw = min(G, prm.tiles_x - gi * G);
+    const int rr = r - gi * G * gh;
+    const int tix = gi * G + rr % gw, tiy = sr * G + rr / gw;
+    x0 = tix * TX; y0 = tiy * TY; z0 = bz * TZ;
   }
   // pixel k = ((kz * KY + ky) * KX + kx); pairs are (kx even, kx odd)
   __device__ int ix(int k) const { return x0 + lx + 8 * (k % KX); }
@@ -383,6 +397,14 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
   const float kph = (float)(6.283185307179586 * prm.k_r);
   const int nch = prm.ch_hi - prm.ch_lo;
   const int nbatch = (nch + kNB - 1) / kNB;
+  // Channel order: every tile visits all batches, starting at a batch offset proportional to
+  // its launch rank among the resident CTAs (blockIdx / resident).  CTAs that are resident at
+  // the same time then stream the same channels at the same time, so a channel's windows come
+  // from DRAM once per wave and from L2 for the other tiles.  Deterministic (depends on
+  // blockIdx only); the sum is order-free up to fp32 rounding (R11).
+  const int rot = prm.resident > 0
+      ? (int)(((long long)(blockIdx.x % prm.resident) * nbatch) / prm.resident) : 0;
+  auto bat = [&](int i) { const int t = i + rot; return t >= nbatch ? t - nbatch : t; };
   const int Wh = W >> 1;
   const int nbox = box_samples(W);
 #if SASBP_FLAT_TRANSFORM
@@ -410,9 +432,9 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
     const int bb = g + warp * kBPW + sub;
     bool live = false;
     if (sub < kBPW && bb < nbatch) {
-      const int nbb = min(kNB, nch - bb * kNB);
+      const int nbb = min(kNB, nch - bat(bb) * kNB);
       if (cl < nbb) {
-        const ChanConst k = chan_prologue<GATE>(prm, prm.ch_lo + bb * kNB + cl, ct, cl, win_base);
+        const ChanConst k = chan_prologue<GATE>(prm, prm.ch_lo + bat(bb) * kNB + cl, ct, cl, win_base);
         cc[(bb % kRing) * kNB + cl] = k;
         live = !(k.gate & 16);
       }
@@ -427,8 +449,8 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
   constexpr int kCW = kNB / kWarps;
   auto issue = [&](int b) {
     if (GATE && !blive[b % kRing]) return;   // dead batch: no loads, no mbarrier phase
-    const int nb = min(kNB, nch - b * kNB);
-    const int ch0 = prm.ch_lo + b * kNB;
+    const int nb = min(kNB, nch - bat(b) * kNB);
+    const int ch0 = prm.ch_lo + bat(b) * kNB;
     const ChanConst* cb = cc + (b % kRing) * kNB;
     const int c0 = warp * kCW;
     const int mine = max(0, min(kCW, nb - c0));
@@ -465,7 +487,7 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
 
   uint32_t phase = 0;   // mbarrier parity of the next live batch
   for (int b = 0; b < nbatch; ++b) {
-    const int nb = min(kNB, nch - b * kNB);
+    const int nb = min(kNB, nch - bat(b) * kNB);
     const bool live = !GATE || blive[b % kRing] != 0;   // warp-uniform (set >= 2 barriers ago)
     if (live) {
       if (USE_TMA) { mbar_wait(bar, phase); phase ^= 1u; }
@@ -564,7 +586,7 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
         if (((kc.gate >> 2) & 3) == kGEdge) {   // receive-cone mask (bistatic), per channel
           double a[3], bb[3], x[3];
           ping_axes(prm, kc.ping, a, bb);
-          const int chg = prm.ch_lo + b * kNB + c;
+          const int chg = prm.ch_lo + bat(b) * kNB + c;
 #pragma unroll
           for (int k = 0; k < 2 * NP; ++k) {
             pixel_centre64(prm, tm.ix(k), tm.iy(k), tm.iz(k), x);
