@@ -62,6 +62,12 @@ def _load():
                                                  ctypes.c_double, f64p, ctypes.c_double, ctypes.c_double,
                                                  ctypes.c_int32, f64p, ctypes.c_int64, f64p, i64p]
         lib.oracle_tdbp_points_gated.restype = ctypes.c_int
+        lib.oracle_tdbp_points_motion.argtypes = [f32p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                                  f64p, f64p, f64p, f64p, ctypes.c_double, ctypes.c_double,
+                                                  ctypes.c_double, f64p, ctypes.c_int64, f64p, i64p]
+        lib.oracle_tdbp_points_motion.restype = ctypes.c_int
+        lib.oracle_delay_moving.argtypes = [f64p, f64p, f64p, f64p, ctypes.c_double]
+        lib.oracle_delay_moving.restype = ctypes.c_double
         lib.oracle_rangecompress.argtypes = [f32p, ctypes.c_int64, ctypes.c_int32, f32p,
                                              ctypes.c_int32, f64p]
         lib.oracle_rangecompress.restype = ctypes.c_int
@@ -125,6 +131,31 @@ def tdbp_points_gated(echoes, tx, rx, t0, fc, fs, c, pts, az, el=0.0, bistatic=F
         raise ValueError("oracle_tdbp_points_gated: invalid arguments")
     res = out[:, 0] + 1j * out[:, 1]
     return (res, cnt) if with_count else res
+
+
+def tdbp_points_motion(echoes, tx, rx, t0, vel, fc, fs, c, pts, with_count=False):
+    """TDBP with the receiver moving at the per-ping velocity vel [P][3] during reception (NEXT-2)."""
+    lib = _load()
+    echoes, P, E, Ns, tx, rx, t0 = _echo_arrays(echoes, tx, rx, t0)
+    vel = np.ascontiguousarray(vel, dtype=np.float64).reshape(P, 3)
+    pts = np.ascontiguousarray(pts, dtype=np.float64).reshape(-1, 3)
+    N = pts.shape[0]
+    out = np.zeros((N, 2), dtype=np.float64)
+    cnt = np.zeros(N, dtype=np.int64) if with_count else None
+    rc = lib.oracle_tdbp_points_motion(_p(echoes, ctypes.c_float), P, E, Ns, _p(tx, ctypes.c_double),
+                                       _p(rx, ctypes.c_double), _p(t0, ctypes.c_double), _p(vel, ctypes.c_double),
+                                       float(fc), float(fs), float(c), _p(pts, ctypes.c_double), N,
+                                       _p(out, ctypes.c_double), _p(cnt, ctypes.c_int64))
+    if rc != 0:
+        raise ValueError("oracle_tdbp_points_motion: invalid arguments")
+    res = out[:, 0] + 1j * out[:, 1]
+    return (res, cnt) if with_count else res
+
+
+def delay_moving(x, tx, rx, v, c):
+    lib = _load()
+    a = [np.ascontiguousarray(q, dtype=np.float64).reshape(3) for q in (x, tx, rx, v)]
+    return float(lib.oracle_delay_moving(*[_p(q, ctypes.c_double) for q in a], float(c)))
 
 
 def grid_points(grid, idx=None):

@@ -69,9 +69,8 @@ void oracle_pixel_centre(const double* origin, const double* step_x, const doubl
  * one (pixel, ping, element) triple).  Returns 1 if the interpolation support
  * meets the recorded window, i.e. u in (-1, Ns), else 0 (the term is then 0).
  */
-static int one_term(const double* x, const float* ch, int32_t Ns, const double* tx, const double* rx,
-                    double t0, double fc, double fs, double c, double* acc_re, double* acc_im) {
-  double tau = (dist3(x, tx) + dist3(x, rx)) / c;           /* Eq. 1 delay, P:89 */
+static int one_term_tau(const double* x, const float* ch, int32_t Ns, double tau, double t0, double fc, double fs,
+                        double* acc_re, double* acc_im) {
   double u = (tau - t0) * fs;                                /* R4 */
   double kf = floor(u);
   double a = u - kf;
@@ -86,6 +85,35 @@ static int one_term(const double* x, const float* ch, int32_t Ns, const double* 
   *acc_re += er * cs - ei * sn;
   *acc_im += er * sn + ei * cs;
   return (u > -1.0 && u < (double)Ns) ? 1 : 0;
+}
+
+static int one_term(const double* x, const float* ch, int32_t Ns, const double* tx, const double* rx,
+                    double t0, double fc, double fs, double c, double* acc_re, double* acc_im) {
+  double tau = (dist3(x, tx) + dist3(x, rx)) / c;           /* Eq. 1 delay, P:89 */
+  return one_term_tau(x, ch, Ns, tau, t0, fc, fs, acc_re, acc_im);
+}
+
+/*
+ * Two-way delay with the receiver moving during reception (NEXT-2, reading R16): the platform
+ * moves with constant velocity v during the ping (first-order kinematics; the
+ * paper's motion model assumes continual motion), the transmitter is stationary during
+ * the instantaneous transmit, and the echo from x is received at tau, when the
+ * element is at rx + v tau:
+ *     tau = ( |x - tx| + |x - rx - v tau| ) / c .
+ * Solved by fixed-point iteration from the stop-and-hop delay (a contraction with factor
+ * <= |v|/c) until the update is below 1e-18 s.
+ */
+static double delay_moving(const double* x, const double* tx, const double* rx, const double* v, double c) {
+  const double rt = dist3(x, tx);
+  double tau = (rt + dist3(x, rx)) / c;
+  for (int it = 0; it < 64; ++it) {
+    double r[3] = {rx[0] + v[0] * tau, rx[1] + v[1] * tau, rx[2] + v[2] * tau};
+    double nt = (rt + dist3(x, r)) / c;
+    double d = fabs(nt - tau);
+    tau = nt;
+    if (d <= 1e-18) break;
+  }
+  return tau;
 }
 
 /*
@@ -179,6 +207,39 @@ int oracle_tdbp_points_gated(const float* echoes, int32_t P, int32_t E, int32_t 
     if (n_in) n_in[i] = cnt;
   }
   return 0;
+}
+
+/*
+ * TDBP with continuous receiver motion at explicit points (NEXT-2): the definition with the
+ * stop-and-hop delay replaced by delay_moving (per-ping velocity vel[P][3], NED m/s).
+ */
+int oracle_tdbp_points_motion(const float* echoes, int32_t P, int32_t E, int32_t Ns, const double* tx,
+                              const double* rx, const double* t0, const double* vel, double fc, double fs,
+                              double c, const double* pts, int64_t N, double* out, int64_t* n_in) {
+  if (P < 1 || E < 1 || Ns < 1 || N < 0 || !(c > 0) || !(fs > 0) || !vel) return -1;
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int64_t i = 0; i < N; ++i) {
+    const double* x = pts + 3 * i;
+    double ar = 0.0, ai = 0.0;
+    int64_t cnt = 0;
+    for (int32_t p = 0; p < P; ++p) {
+      double t0p = t0 ? t0[p] : 0.0;
+      for (int32_t e = 0; e < E; ++e) {
+        const float* ch = echoes + 2 * ((int64_t)p * E + e) * (int64_t)Ns;
+        double tau = delay_moving(x, tx + 3 * p, rx + 3 * ((int64_t)p * E + e), vel + 3 * p, c);
+        cnt += one_term_tau(x, ch, Ns, tau, t0p, fc, fs, &ar, &ai);
+      }
+    }
+    out[2 * i] = ar;
+    out[2 * i + 1] = ai;
+    if (n_in) n_in[i] = cnt;
+  }
+  return 0;
+}
+
+/* The moving-receiver delay alone (for the closed-form pins): tau for one (x, tx, rx, v). */
+double oracle_delay_moving(const double* x, const double* tx, const double* rx, const double* v, double c) {
+  return delay_moving(x, tx, rx, v, c);
 }
 
 /*

@@ -52,7 +52,7 @@ def _load():
         lib.synth_echoes.argtypes = [ctypes.POINTER(ctypes.c_float), ctypes.c_int32, ctypes.c_int32,
                                      ctypes.c_int32, f64p, f64p, f64p, f64p, ctypes.c_double,
                                      ctypes.c_double, ctypes.c_double, ctypes.c_double,
-                                     ctypes.c_int32, f64p, f64p, ctypes.c_int64, ctypes.c_double]
+                                     ctypes.c_int32, f64p, f64p, ctypes.c_int64, ctypes.c_double, f64p]
         lib.synth_echoes.restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -93,6 +93,7 @@ class Scenario:
     body_rot: Optional[np.ndarray] = None  # [P][3][3]
     half_support: int = 16
     nav_nominal: Optional[tuple] = None   # (tx, rx) unperturbed nav (cfg 3)
+    vel: Optional[np.ndarray] = None      # [P][3] platform velocity during reception (None = stop-and-hop)
 
     @property
     def P(self):
@@ -119,11 +120,12 @@ class Scenario:
         tx, rx, t0, scat = f64(self.tx), f64(self.rx), f64(self.t0), f64(self.scat)
         sig = f64(np.stack([self.sigma.real, self.sigma.imag], axis=1))
         rot = f64(self.body_rot.reshape(P, 9)) if self.body_rot is not None else None
+        vel = f64(self.vel.reshape(P, 3)) if self.vel is not None else None
         ptr = lambda a: a.ctypes.data_as(ctypes.POINTER(ctypes.c_double)) if a is not None else None
         rc = lib.synth_echoes(out.ctypes.data_as(ctypes.POINTER(ctypes.c_float)), P, E, Ns, ptr(tx),
                               ptr(rx), ptr(t0), ptr(rot), self.fc, self.bandwidth, self.fs, self.c,
                               self.half_support, ptr(scat), ptr(sig), scat.shape[0],
-                              self.sin_half_beam)
+                              self.sin_half_beam, ptr(vel))
         if rc != 0:
             raise ValueError("synth_echoes failed")
         return out.view(np.complex64).reshape(P, E, Ns)
@@ -134,6 +136,7 @@ class Scenario:
         return dataclasses.replace(self, name=f"{self.name}[{len(idx)} pings]", tx=self.tx[idx], rx=self.rx[idx],
                                    t0=self.t0[idx],
                                    body_rot=None if self.body_rot is None else self.body_rot[idx],
+                                   vel=None if self.vel is None else self.vel[idx],
                                    nav_nominal=None if self.nav_nominal is None else
                                    (self.nav_nominal[0][idx], self.nav_nominal[1][idx]))
 

@@ -34,7 +34,7 @@
 int synth_echoes(float* echoes, int32_t P, int32_t E, int32_t Ns, const double* tx, const double* rx,
                  const double* t0, const double* body_rot, double fc, double B, double fs, double c,
                  int32_t half_support, const double* scat, const double* sigma, int64_t S,
-                 double sin_half_beam) {
+                 double sin_half_beam, const double* vel) {
   if (P < 1 || E < 1 || Ns < 1 || S < 0 || !(fs > 0) || !(c > 0) || !(B > 0)) return -1;
   const double step = SYN_PI * B / fs; /* sinc argument increment (radians of pi x) */
   const double cst = cos(step), snt = sin(step);
@@ -58,6 +58,14 @@ int synth_echoes(float* echoes, int32_t P, int32_t E, int32_t Ns, const double* 
         double rrx = sqrt(wx * wx + wy * wy + wz * wz);
         if (rrx <= 0) continue;
         double tau = (rtx + rrx) / c;
+        if (vel) {  /* receiver moving with the platform during reception: tau = (R_tx + |x - rx - v tau|)/c */
+          const double* V = vel + 3 * p;
+          for (int it = 0; it < 8; ++it) {
+            double qx = wx - V[0] * tau, qy = wy - V[1] * tau, qz = wz - V[2] * tau;
+            rrx = sqrt(qx * qx + qy * qy + qz * qz);
+            tau = (rtx + rrx) / c;
+          }
+        }
         double amp_r = sigma[2 * s] / (rtx * rrx), amp_i = sigma[2 * s + 1] / (rtx * rrx);
         /* carrier exp(-j 2 pi fc tau), phase reduced in cycles first */
         double cyc = fc * tau;
