@@ -135,6 +135,7 @@ SASBP_API sas_status sas_bp_count_terms(sas_bp_t h, uint64_t* dense, uint64_t* i
  *   tma       1 = windows staged by TMA tensor loads, 0 = cp.async fallback (odd Ns, unaligned
  *             device echoes, or SASBP_NO_TMA=1 in the environment at set_pings time)
  *   batch     channels (ping x element) staged per pipeline step
+ *   ctas_per_sm  resident CTAs per SM of the last form's kernel (0 before the first form)
  * Errors: SAS_E_INVALID for NULL; rx_mode / tma are -1 before the first set_pings. */
 typedef struct {
   int32_t tile[3];
@@ -142,6 +143,7 @@ typedef struct {
   int32_t rx_mode;
   int32_t tma;
   int32_t batch;
+  int32_t ctas_per_sm;
 } sas_bp_plan;
 SASBP_API sas_status sas_bp_get_plan(sas_bp_t h, sas_bp_plan* out);
 
@@ -166,6 +168,18 @@ typedef struct {
   int32_t cull;
 } sas_beam;
 SASBP_API sas_status sas_bp_set_beam(sas_bp_t h, const sas_beam* beam, const double* axes, int32_t P);
+
+/* Continuous receiver motion (the paper's motion model assumes continual
+ * motion; reading R16): with velocities set, each ping's receivers move with the platform
+ * velocity v_p during reception, the transmitter being stationary during the instantaneous
+ * transmit, so the delay solves
+ *   tau = ( |x - tx_p| + |x - rx_{p,e} - v_p tau| ) / c .
+ * The kernel takes the exact reference solution per (tile, channel) in fp64 and the per-pixel
+ * deviation to first order in the pixel offset (relative error ~ (|v|/c)(|d|/R)^2).
+ *   vel  fp64 [P][3] NED m/s (|v| <= c/100), copied; NULL = stop-and-hop (R5).  P must match the
+ *        ping set at form time (else SAS_E_STATE).
+ * Errors: SAS_E_INVALID (non-finite or too fast), SAS_E_NOMEM, SAS_E_CUDA. */
+SASBP_API sas_status sas_bp_set_motion(sas_bp_t h, const double* vel, int32_t P);
 
 /* Bytes of device memory the handle owns (image + workspace + owned ping copy). */
 SASBP_API size_t sas_bp_workspace_bytes(sas_bp_t h);

@@ -33,6 +33,7 @@
 namespace {
 
 thread_local char g_err[512] = "";
+thread_local int g_last_occ = 0;   // resident CTAs per SM of the last K2 launch on this thread
 
 sas_status fail(sas_status st, const char* fmt, ...) {
   va_list ap;
@@ -75,11 +76,15 @@ struct sas_bp_s {
   // TMA descriptor of the current echoes (row staging), rebuilt when the ping set changes
   sasbp::TmaDesc tmap{};
   bool use_tma = false;
+  int ctas_per_sm = 0;   // measured occupancy of the last form
   // field-of-view gating (sas_bp_set_beam; NEXT-1)
   int gate = 0, cull = 0, az_on = 0, el_on = 0;
   double half_az = 0, sin_half_az = 0, half_el = 0, tan_half_el = 0;
   double* axes = nullptr;
   int axes_P = 0;
+  // continuous receiver motion (sas_bp_set_motion; NEXT-2)
+  double* vel = nullptr;
+  int vel_P = 0;
   bool has_pings = false;
   bool broken = false;
   size_t bytes = 0;
@@ -136,10 +141,12 @@ cudaError_t launch_k(Kern kern, int threads, const sasbp::TdbpParams& prm_in, co
   }
   sasbp::TdbpParams prm = prm_in;
   int per_sm = 0, dev = 0, sms = 0;
+  g_last_occ = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem) == cudaSuccess &&
       cudaGetDevice(&dev) == cudaSuccess &&
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess)
     prm.resident = per_sm * sms;
+  g_last_occ = per_sm;
 #if !SASBP_ROTATE
   prm.resident = 0;
 #endif
@@ -147,22 +154,25 @@ cudaError_t launch_k(Kern kern, int threads, const sasbp::TdbpParams& prm_in, co
   return cudaGetLastError();
 }
 
-template <int KX, int KY, int KZ, int WY, int WZ, bool DZ, bool TMA, bool GATE>
+template <int KX, int KY, int KZ, int WY, int WZ, bool DZ, bool TMA, bool GATE, bool MOTION>
 cudaError_t launch_gate(const sasbp::TdbpParams& prm, const sasbp::TmaDesc& tmap, int mode, cudaStream_t st) {
   using namespace sasbp;
   const size_t smem = smem_bytes(prm.W);
   const int nt = 32 * WY * WZ;
   switch (mode) {
-    case kSeries3: return launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kSeries3, TMA, GATE>, nt, prm, tmap, smem, st);
-    case kSeries4: return launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kSeries4, TMA, GATE>, nt, prm, tmap, smem, st);
-    default: return launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kExact, TMA, GATE>, nt, prm, tmap, smem, st);
+    case kSeries3: return launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kSeries3, TMA, GATE, MOTION>, nt, prm, tmap, smem, st);
+    case kSeries4: return launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kSeries4, TMA, GATE, MOTION>, nt, prm, tmap, smem, st);
+    default: return launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kExact, TMA, GATE, MOTION>, nt, prm, tmap, smem, st);
   }
 }
 
 template <int KX, int KY, int KZ, int WY, int WZ, bool DZ, bool TMA>
 cudaError_t launch_mode(const sasbp::TdbpParams& prm, const sasbp::TmaDesc& tmap, int mode, cudaStream_t st) {
-  return prm.gate ? launch_gate<KX, KY, KZ, WY, WZ, DZ, TMA, true>(prm, tmap, mode, st)
-                  : launch_gate<KX, KY, KZ, WY, WZ, DZ, TMA, false>(prm, tmap, mode, st);
+  if (prm.vel)
+    return prm.gate ? launch_gate<KX, KY, KZ, WY, WZ, DZ, TMA, true, true>(prm, tmap, mode, st)
+                    : launch_gate<KX, KY, KZ, WY, WZ, DZ, TMA, false, true>(prm, tmap, mode, st);
+  return prm.gate ? launch_gate<KX, KY, KZ, WY, WZ, DZ, TMA, true, false>(prm, tmap, mode, st)
+                  : launch_gate<KX, KY, KZ, WY, WZ, DZ, TMA, false, false>(prm, tmap, mode, st);
 }
 
 template <int KX, int KY, int KZ, int WY, int WZ, bool DZ>
@@ -235,6 +245,7 @@ cudaError_t launch_tdbp(sas_bp_t h, float2* image, unsigned long long* counter, 
   prm.sin_half_az = h->sin_half_az; prm.half_az = h->half_az;
   prm.tan_half_el = h->tan_half_el; prm.half_el = h->half_el;
   prm.d_max = h->d_max;
+  prm.vel = h->vel;
   switch (h->variant) {
 #if SASBP_K4
     case V2D: return launch_variant<4, 1, 1, 8, 1, false>(prm, h->tmap, h->use_tma, h->mode, count, st);
@@ -399,6 +410,7 @@ void sas_bp_destroy(sas_bp_t h) {
   cudaFree(h->geo);
   cudaFree(h->counter);
   cudaFree(h->axes);
+  cudaFree(h->vel);
   if (h->stream) cudaStreamDestroy(h->stream);
   if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
   if (prev >= 0) cudaSetDevice(prev);
@@ -460,9 +472,11 @@ sas_status sas_bp_form_device(sas_bp_t h, void* image_dev, void* cuda_stream, in
   if (flags & ~SAS_FORM_ACCUMULATE) return fail(SAS_E_INVALID, "unknown flags 0x%x", flags);
   if (!h->has_pings) return fail(SAS_E_STATE, "sas_bp_form before sas_bp_set_pings");
   if (h->gate && h->axes && h->axes_P != h->P) return fail(SAS_E_STATE, "beam axes were given for %d pings, the ping set has %d", h->axes_P, h->P);
+  if (h->vel && h->vel_P != h->P) return fail(SAS_E_STATE, "velocities were given for %d pings, the ping set has %d", h->vel_P, h->P);
   CK_H(h, cudaSetDevice(h->device));
   CK_H(h, launch_tdbp(h, (float2*)image_dev, h->counter, (flags & SAS_FORM_ACCUMULATE) ? 1 : 0, false,
                       (cudaStream_t)cuda_stream));
+  h->ctas_per_sm = g_last_occ;
   return SAS_OK;
 }
 
@@ -473,8 +487,10 @@ sas_status sas_bp_form(sas_bp_t h, float* image_out) {
   if (!image_out) return fail(SAS_E_INVALID, "image_out must not be NULL");
   if (!h->has_pings) return fail(SAS_E_STATE, "sas_bp_form before sas_bp_set_pings");
   if (h->gate && h->axes && h->axes_P != h->P) return fail(SAS_E_STATE, "beam axes were given for %d pings, the ping set has %d", h->axes_P, h->P);
+  if (h->vel && h->vel_P != h->P) return fail(SAS_E_STATE, "velocities were given for %d pings, the ping set has %d", h->vel_P, h->P);
   CK_H(h, cudaSetDevice(h->device));
   CK_H(h, launch_tdbp(h, h->image, h->counter, 0, false, h->stream));
+  h->ctas_per_sm = g_last_occ;
   const size_t npx = (size_t)h->grid.nx * h->grid.ny * h->grid.nz;
   CK_H(h, cudaMemcpyAsync(image_out, h->image, npx * sizeof(float2), cudaMemcpyDeviceToHost, h->stream));
   CK_H(h, cudaStreamSynchronize(h->stream));
@@ -507,6 +523,7 @@ sas_status sas_bp_form_streamed(sas_bp_t h, const float* echoes, int32_t P, int3
   h->use_tma = encode_tma(h);
   h->has_pings = true;
   if (h->gate && h->axes && h->axes_P != h->P) return fail(SAS_E_STATE, "beam axes were given for %d pings, the ping set has %d", h->axes_P, h->P);
+  if (h->vel && h->vel_P != h->P) return fail(SAS_E_STATE, "velocities were given for %d pings, the ping set has %d", h->vel_P, h->P);
   const int nch = P * E;
   int nchunk = chunks > 0 ? chunks : 8;
   nchunk = std::max(1, std::min(nchunk, (nch + 63) / 64));   // >= 64 channels per chunk
@@ -536,6 +553,7 @@ sas_status sas_bp_count_terms(sas_bp_t h, uint64_t* dense, uint64_t* in_win) {
   if (h->broken) return fail(SAS_E_CUDA, "handle is in a failed CUDA state; destroy it");
   if (!h->has_pings) return fail(SAS_E_STATE, "sas_bp_count_terms before sas_bp_set_pings");
   if (h->gate && h->axes && h->axes_P != h->P) return fail(SAS_E_STATE, "beam axes were given for %d pings, the ping set has %d", h->axes_P, h->P);
+  if (h->vel && h->vel_P != h->P) return fail(SAS_E_STATE, "velocities were given for %d pings, the ping set has %d", h->vel_P, h->P);
   const uint64_t npx = (uint64_t)h->grid.nx * h->grid.ny * h->grid.nz;
   if (dense) *dense = npx * (uint64_t)h->P * (uint64_t)h->E;
   if (in_win) {
@@ -601,6 +619,33 @@ sas_status sas_bp_set_beam(sas_bp_t h, const sas_beam* beam, const double* axes,
   return SAS_OK;
 }
 
+sas_status sas_bp_set_motion(sas_bp_t h, const double* vel, int32_t P) {
+  g_err[0] = 0;
+  if (!h) return fail(SAS_E_INVALID, "handle is NULL");
+  if (h->broken) return fail(SAS_E_CUDA, "handle is in a failed CUDA state; destroy it");
+  if (!vel) {   // stop-and-hop
+    if (h->vel) { cudaFree(h->vel); h->bytes -= (size_t)h->vel_P * 3 * sizeof(double); }
+    h->vel = nullptr; h->vel_P = 0;
+    return SAS_OK;
+  }
+  if (P < 1) return fail(SAS_E_INVALID, "P must be >= 1");
+  for (int32_t p = 0; p < P; ++p) {
+    const double* v = vel + 3 * (size_t)p;
+    if (!finite3(v)) return fail(SAS_E_INVALID, "non-finite velocity of ping %d", p);
+    if (norm3(v) > 0.01 * h->c) return fail(SAS_E_INVALID, "velocity of ping %d exceeds c/100", p);
+  }
+  CK_H(h, cudaSetDevice(h->device));
+  if (h->vel_P != P || !h->vel) {
+    if (h->vel) { cudaFree(h->vel); h->bytes -= (size_t)h->vel_P * 3 * sizeof(double); h->vel = nullptr; }
+    cudaError_t e = cudaMalloc(&h->vel, (size_t)P * 3 * sizeof(double));
+    if (e != cudaSuccess) { h->vel = nullptr; h->vel_P = 0; return fail(SAS_E_NOMEM, "cudaMalloc(vel)"); }
+    h->bytes += (size_t)P * 3 * sizeof(double);
+  }
+  CK_H(h, cudaMemcpy(h->vel, vel, (size_t)P * 3 * sizeof(double), cudaMemcpyHostToDevice));
+  h->vel_P = P;
+  return SAS_OK;
+}
+
 sas_status sas_bp_get_plan(sas_bp_t h, sas_bp_plan* out) {
   g_err[0] = 0;
   if (!h || !out) return fail(SAS_E_INVALID, "NULL argument");
@@ -609,6 +654,7 @@ sas_status sas_bp_get_plan(sas_bp_t h, sas_bp_plan* out) {
   out->rx_mode = h->has_pings ? h->mode : -1;
   out->tma = h->has_pings ? (h->use_tma ? 1 : 0) : -1;
   out->batch = sasbp::kNB;
+  out->ctas_per_sm = h->ctas_per_sm;
   return SAS_OK;
 }
 

@@ -86,15 +86,17 @@ struct TdbpParams {
   const double* axes;     // [P][2][3] per-ping along-track axis a, boresight b; NULL = (+x, +y)
   double sin_half_az, half_az, tan_half_el, half_el;
   double d_max;           // tile sphere radius (m)
+  // continuous receiver motion (NEXT-2, reading R16): per-ping velocity [P][3] or NULL
+  const double* vel;
 };
 
 // per-channel constants in shared memory (fp64 prologue output)
 struct __align__(16) ChanConst {
-  float ux2, uy2, uz2, ir2;     // rx leg: 2 (c_T - rx), 1 / r_r^2
+  float ux2, uy2, uz2, kap0;    // rx leg: 2 (c_T - rx'); moving receiver scale (1 for stop-and-hop)
   float a0, a1, a2, a3;         // rx leg series in q: dU = q (a0 + a1 q + a2 q^2 + a3 q^3), see prologue
   float urr, phi0, r_r, r2_r;   // centred window coordinate offset; phase offset (rad); r_r; r_r^2
   float tx2x, tx2y, tx2z, r2_t; // tx leg: 2 (c_T - tx), r_t^2
-  float r_t, kfs, klo_f, pad1;  // r_t, fs/c, (float) k_lo
+  float r_t, kgx, kgy, kgz;     // r_t; moving receiver: U = dU (kap0 + kg.d) + urr (kg = 0 stop-and-hop)
   int ping, woff, klo, gate;    // ping index; LDS byte offset of cell Wh minus MAGIC*16; window start;
                                 // gate classes: bits 0-1 tx, 2-3 rx (kGIn/kGEdge/kGOut), bit 4 = culled
 };
@@ -198,7 +200,7 @@ __device__ __forceinline__ void pixel_centre64(const TdbpParams& prm, int ix, in
 
 // fp64 prologue for one channel (row a2): reference geometry at the tile centre ct (and, for
 // gated kernels, the tile's cone classes).
-template <bool GATE>
+template <bool GATE, bool MOTION = false>
 __device__ __forceinline__ ChanConst chan_prologue(const TdbpParams& prm, int ch, const double ct[3], int slot,
                                                    uint32_t win_base) {
   const int p = (int)(((double)ch + 0.5) * prm.inv_e);   // ch / E, exact for ch < 2^40
@@ -227,7 +229,27 @@ __device__ __forceinline__ ChanConst chan_prologue(const TdbpParams& prm, int ch
     gate_bits = (ct_cls == kGOut ? kGEdge : ct_cls) | ((cr_cls == kGOut ? kGEdge : cr_cls) << 2);
   }
   const double r_t = sqrt(utx * utx + uty * uty + utz * utz);
-  const double r_r = sqrt(urx * urx + ury * ury + urz * urz);
+  double urx_m = urx, ury_m = ury, urz_m = urz;   // centre minus the receiver at its reception time
+  double r_r = sqrt(urx * urx + ury * ury + urz * urz);
+  double kap0 = 1.0, kg[3] = {0.0, 0.0, 0.0};
+  if (MOTION && prm.vel) {
+    // reference delay with the receiver moving at v during reception: c tau = r_t + |c_T - rx - v tau|
+    // (fixed point from stop-and-hop, contraction |v|/c); the rx leg below is then taken w.r.t.
+    // rx' = rx + v tau_ref, and per pixel tau - tau_ref = (dR_t + dR_r') / (c + w.v), w = unit(x - rx'),
+    // i.e. U = dU / (1 + g), g = w.v / c = g0 + g1.d to first order in the pixel offset d.
+    const double* V = prm.vel + 3 * p;
+    double tau = (r_t + r_r) / prm.c;
+    for (int it = 0; it < 6; ++it) {
+      urx_m = urx - V[0] * tau; ury_m = ury - V[1] * tau; urz_m = urz - V[2] * tau;
+      r_r = sqrt(urx_m * urx_m + ury_m * ury_m + urz_m * urz_m);
+      tau = (r_t + r_r) / prm.c;
+    }
+    const double ux = urx_m / r_r, uy = ury_m / r_r, uz = urz_m / r_r;
+    const double uv = ux * V[0] + uy * V[1] + uz * V[2];
+    kap0 = 1.0 / (1.0 + uv / prm.c);
+    const double s1 = -kap0 * kap0 / (prm.c * r_r);   // d kappa = -kap0^2 g1.d, g1 = (v - (u.v) u) / (c r)
+    kg[0] = s1 * (V[0] - uv * ux); kg[1] = s1 * (V[1] - uv * uy); kg[2] = s1 * (V[2] - uv * uz);
+  }
   const double S = r_t + r_r;
   const double Uref = fma(S, prm.k_s, -prm.t0[p] * prm.fs);   // absolute sample index at tile centre
   const double klo_d = floor(Uref - prm.hw) - 2.0;
@@ -240,11 +262,11 @@ __device__ __forceinline__ ChanConst chan_prologue(const TdbpParams& prm, int ch
   double ph = fma(-urr, prm.k_r, S * prm.k_c);                // reference phase (cycles) at U = 0
   ph -= floor(ph);
   ChanConst k;
-  k.ux2 = (float)(2.0 * urx); k.uy2 = (float)(2.0 * ury); k.uz2 = (float)(2.0 * urz);
+  k.ux2 = (float)(2.0 * urx_m); k.uy2 = (float)(2.0 * ury_m); k.uz2 = (float)(2.0 * urz_m);
+  k.kap0 = (float)kap0; k.kgx = (float)kg[0]; k.kgy = (float)kg[1]; k.kgz = (float)kg[2];
   // series coefficients only need fp32 relative accuracy
   const float ir = 1.0f / (float)r_r;
   const float ir2 = ir * ir;
-  k.ir2 = ir2;
   // (sqrt(1+e)-1)/e = 1/2 - e/8 + e^2/16 - 5e^3/128 + ..., e = q / r^2; folded into a polynomial
   // in q so the kernel needs no e = q / r^2 multiply: a_n = c_n (fs/c) / r^(2n+1)
   const float g = (float)prm.k_s * ir;
@@ -253,8 +275,7 @@ __device__ __forceinline__ ChanConst chan_prologue(const TdbpParams& prm, int ch
   k.phi0 = (float)(6.283185307179586 * ph);
   k.r_r = (float)r_r; k.r2_r = (float)(r_r * r_r);
   k.tx2x = (float)(2.0 * utx); k.tx2y = (float)(2.0 * uty); k.tx2z = (float)(2.0 * utz);
-  k.r2_t = (float)(r_t * r_t); k.r_t = (float)r_t; k.kfs = (float)prm.k_s;
-  k.klo_f = (float)klo; k.pad1 = 0.f;
+  k.r2_t = (float)(r_t * r_t); k.r_t = (float)r_t;
   k.ping = p;
   k.woff = (int)(win_base + (uint32_t)(slot * prm.W + Wh) * 16u - (uint32_t)kMagicBits * 16u);
   k.klo = klo;
@@ -353,7 +374,7 @@ struct __align__(64) TmaDesc { unsigned char bytes[128]; };
 // HAS_DZ = false means the grid is a z-level plane (step_x, step_y have no z component); then
 // both pixels of an x-pair share their y offset whenever step_x has no y component (AXIS).
 template <int KX, int KY, int KZ, int WY, int WZ, bool HAS_DZ, int MODE, bool USE_TMA, bool GATE = false,
-          bool AXIS = false>
+          bool MOTION = false, bool AXIS = false>
 __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp_kernel(const TdbpParams prm,
                                                                           const __grid_constant__ TmaDesc tmap) {
   using TM = TileMap<KX, KY, KZ, WY, WZ>;
@@ -395,6 +416,7 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
   }
 
   const float kph = (float)(6.283185307179586 * prm.k_r);
+  const float kfs = (float)prm.k_s;
   const int nch = prm.ch_hi - prm.ch_lo;
   const int nbatch = (nch + kNB - 1) / kNB;
   // Channel order: every tile visits all batches, starting at a batch offset proportional to
@@ -434,7 +456,7 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
     if (sub < kBPW && bb < nbatch) {
       const int nbb = min(kNB, nch - bat(bb) * kNB);
       if (cl < nbb) {
-        const ChanConst k = chan_prologue<GATE>(prm, prm.ch_lo + bat(bb) * kNB + cl, ct, cl, win_base);
+        const ChanConst k = chan_prologue<GATE, MOTION>(prm, prm.ch_lo + bat(bb) * kNB + cl, ct, cl, win_base);
         cc[(bb % kRing) * kNB + cl] = k;
         live = !(k.gate & 16);
       }
@@ -576,7 +598,7 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
           const float2 r2 = __fadd2_rn(q, f2(kc.r2_t));
           const float den0 = fmaf(r2.x, rsqrt_approx(r2.x), kc.r_t);
           const float den1 = fmaf(r2.y, rsqrt_approx(r2.y), kc.r_t);
-          BT[p] = __fmul2_rn(__fmul2_rn(q, make_float2(rcp_approx(den0), rcp_approx(den1))), f2(kc.kfs));
+          BT[p] = __fmul2_rn(__fmul2_rn(q, make_float2(rcp_approx(den0), rcp_approx(den1))), f2(kfs));
         }
       }
       uint32_t msk = 0xFFu;
@@ -605,7 +627,7 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
           const float2 r2 = __fadd2_rn(q, f2(kc.r2_r));
           const float den0 = fmaf(r2.x, rsqrt_approx(r2.x), kc.r_r);
           const float den1 = fmaf(r2.y, rsqrt_approx(r2.y), kc.r_r);
-          U = __ffma2_rn(__fmul2_rn(q, make_float2(rcp_approx(den0), rcp_approx(den1))), f2(kc.kfs), BT[p]);
+          U = __ffma2_rn(__fmul2_rn(q, make_float2(rcp_approx(den0), rcp_approx(den1))), f2(kfs), BT[p]);
         } else {
           float2 h;
           if (MODE == kSeries4) {
@@ -617,7 +639,14 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
           h = __ffma2_rn(h, q, f2(kc.a0));
           U = __ffma2_rn(q, h, BT[p]);
         }
-        U = __fadd2_rn(U, f2(kc.urr));                       // centred window coordinate
+        if (MOTION) {   // moving receiver: U = dU / (1 + w.v/c) ~ dU (kap0 + kg.d) + urr
+          float2 kap = __ffma2_rn(f2(kc.kgy), DY[p], f2(kc.kap0));
+          kap = __ffma2_rn(f2(kc.kgx), DX[p], kap);
+          if (HAS_DZ) kap = __ffma2_rn(f2(kc.kgz), DZ[p], kap);
+          U = __ffma2_rn(U, kap, f2(kc.urr));
+        } else {
+          U = __fadd2_rn(U, f2(kc.urr));                     // centred window coordinate
+        }
         const float2 T = __fadd2_rn(U, f2(kMagic));          // rn(U) in the mantissa
         const float2 ph = __ffma2_rn(U, f2(kph), f2(kc.phi0));
 #pragma unroll
@@ -677,7 +706,7 @@ __global__ void __launch_bounds__(32 * WY * WZ) count_kernel(const TdbpParams pr
   for (int ch0 = prm.ch_lo; ch0 < prm.ch_hi; ch0 += kNB) {
     const int nb = min(kNB, prm.ch_hi - ch0);
     __syncthreads();
-    if (tid < nb) cc[tid] = chan_prologue<false>(prm, ch0 + tid, ct, tid, 0u);
+    if (tid < nb) cc[tid] = chan_prologue<false, true>(prm, ch0 + tid, ct, tid, 0u);
     __syncthreads();
     for (int c = 0; c < nb; ++c) {
       const ChanConst kc = cc[c];
@@ -686,9 +715,10 @@ __global__ void __launch_bounds__(32 * WY * WZ) count_kernel(const TdbpParams pr
         const float qt = fmaf(kc.tx2x, dx[k], fmaf(kc.tx2y, dy[k], fmaf(kc.tx2z, dz[k], dd[k])));
         const float qr = fmaf(kc.ux2, dx[k], fmaf(kc.uy2, dy[k], fmaf(kc.uz2, dz[k], dd[k])));
         const float rt = sqrtf(kc.r2_t + qt), rr = sqrtf(kc.r2_r + qr);
-        const float du = (qt / (rt + kc.r_t) + qr / (rr + kc.r_r)) * kc.kfs;
+        const float kap = kc.kap0 + kc.kgx * dx[k] + kc.kgy * dy[k] + kc.kgz * dz[k];
+        const float du = (qt / (rt + kc.r_t) + qr / (rr + kc.r_r)) * (float)prm.k_s * kap;
         // absolute u = k_lo + 0.5 + Wh + (du + urr)
-        const float ua = kc.klo_f + 0.5f + (float)(prm.W >> 1) + (du + kc.urr);
+        const float ua = (float)kc.klo + 0.5f + (float)(prm.W >> 1) + (du + kc.urr);
         bool admit = ok[k] && ua > -1.f && ua < Nsf;
         if (prm.gate && admit) {   // gated metric: count only terms inside the cone(s), fp64 decision
           double a[3], bb[3], x[3];

@@ -96,6 +96,7 @@ def test_null_handle_calls(lib):
     assert lib.sas_bp_form_streamed(None, f32, 1, 1, 4, f64, f64, None, f32, 0) == sasbp.SAS_E_INVALID
     assert lib.sas_bp_get_plan(None, None) == sasbp.SAS_E_INVALID
     assert lib.sas_bp_set_beam(None, None, None, 0) == sasbp.SAS_E_INVALID
+    assert lib.sas_bp_set_motion(None, None, 0) == sasbp.SAS_E_INVALID
     assert lib.sas_bp_workspace_bytes(None) == 0
 
 

@@ -301,8 +301,10 @@ def test_plan_selection(bpmod):
     s = synth.scenario(2, reduced=True)
     with bpmod.Backprojector(s.fc, s.bandwidth, s.fs, s.c, s.grid) as bp:
         bp.set_pings(s.echoes(), s.tx, s.rx, s.t0)
+        bp.form()
         pl = bp.plan()
     assert pl["tile"] == (32, 32, 1) and pl["tma"] is True and pl["rx_mode"] == "series3", pl
+    assert pl["ctas_per_sm"] == 4, pl   # 126 registers and the shared-memory budget give 4 CTAs
     s4 = synth.scenario(4, reduced=True)
     with bpmod.Backprojector(s4.fc, s4.bandwidth, s4.fs, s4.c, s4.grid) as bp:
         bp.set_pings(s4.echoes(), s4.tx + [0, 0, 1.8], s4.rx + [0, 0, 1.8], s4.t0 - 3.6 / s4.c)
@@ -481,3 +483,83 @@ def test_gated_full_size_cfg2_sampled(bpmod):
     idx = s.sample_pixels(2048, window=7, seed=7)
     ref = _gated_ref(s, e, s.grid, az, idx=idx)
     _check(_at(got, idx), ref, label="gated cfg2 full")
+
+
+# ------------------------------------------------------------------ NEXT-2: moving receiver
+
+def _motion_form(bpmod, s, e, vel, beam=None):
+    with bpmod.Backprojector(s.fc, s.bandwidth, s.fs, s.c, s.grid) as bp:
+        bp.set_pings(e, s.tx, s.rx, s.t0)
+        bp.set_motion(vel)
+        if beam:
+            bp.set_beam(*beam)
+        return bp.form()
+
+
+def test_motion_cfg1_vs_oracle(bpmod):
+    """Config 1 recorded at 2 m/s along track: GPU moving-receiver image vs the oracle's exact
+    delay root (R16), full grid; peak at the target with phase ~ 0."""
+    s = synth.scenario(1)
+    s.vel = np.tile([2.0, 0.0, 0.0], (s.P, 1))
+    e = s.echoes()
+    got = _motion_form(bpmod, s, e, s.vel)
+    ref = oracle.tdbp_points_motion(e, s.tx, s.rx, s.t0, s.vel, s.fc, s.fs, s.c,
+                                    oracle.grid_points(s.grid)).reshape(got.shape)
+    pk = s.target_pixels
+    _check(got, ref, _at(got, pk), _at(ref, pk), label="motion cfg1")
+    iy, ix = np.unravel_index(np.argmax(np.abs(got[0])), got[0].shape)
+    assert (ix, iy) == tuple(pk[0][:2])
+
+
+@pytest.mark.parametrize("cid", [3, 4])
+def test_motion_random_velocities(bpmod, cid):
+    """Per-ping velocities with sway / heave components (reduced configs 3 and 4; config 4 runs
+    the near-field exact receive leg)."""
+    s = synth.scenario(cid, reduced=True)
+    rng = np.random.default_rng(cid)
+    s.vel = np.stack([1.5 + 0.2 * rng.normal(size=s.P), 0.3 * rng.normal(size=s.P), 0.1 * rng.normal(size=s.P)], 1)
+    e = s.echoes()
+    got = _motion_form(bpmod, s, e, s.vel)
+    ref = oracle.tdbp_points_motion(e, s.tx, s.rx, s.t0, s.vel, s.fc, s.fs, s.c,
+                                    oracle.grid_points(s.grid)).reshape(got.shape)
+    pk = s.target_pixels
+    _check(got, ref, _at(got, pk), _at(ref, pk), label=f"motion cfg{cid}r")
+
+
+def test_motion_zero_velocity_bitwise(bpmod):
+    s = synth.scenario(2, reduced=True)
+    e = s.echoes()
+    a = _form(bpmod, s, e)
+    b = _motion_form(bpmod, s, e, np.zeros((s.P, 3)))
+    assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+
+
+def test_motion_with_gating(bpmod):
+    """Moving receiver and FOV gating together (gate decisions on the transmit-time positions)."""
+    s = synth.scenario(2, reduced=True)
+    s.vel = np.tile([1.8, 0.1, 0.0], (s.P, 1))
+    e = s.echoes()
+    az = 2 * np.arcsin(s.sin_half_beam)
+    got = _motion_form(bpmod, s, e, s.vel, beam=(az,))
+    # oracle: gate mask from the gated oracle with a unit echo set is not separable; compare the
+    # gated-motion image against the motion oracle restricted by the same gate, term by term,
+    # on a point subset via the identity gated(motion) = motion - (out-of-cone terms): use the
+    # open-gate limit instead for the numerics and the gate limit for the structure:
+    open_gate = _motion_form(bpmod, s, e, s.vel, beam=(np.pi,))
+    ref_open = oracle.tdbp_points_motion(e, s.tx, s.rx, s.t0, s.vel, s.fc, s.fs, s.c,
+                                         oracle.grid_points(s.grid)).reshape(got.shape)
+    _check(open_gate, ref_open, label="motion + open gate")
+    assert np.max(np.abs(got)) > 0 and not np.array_equal(got, open_gate)
+
+
+def test_set_motion_errors(bpmod):
+    s = synth.scenario(1)
+    with bpmod.Backprojector(s.fc, s.bandwidth, s.fs, s.c, s.grid) as bp:
+        bp.set_pings(s.echoes(), s.tx, s.rx, s.t0)
+        with pytest.raises(bpmod.SasError) as ei:
+            bp.set_motion(np.tile([100.0, 0, 0], (s.P, 1)))   # > c/100
+        assert ei.value.status == -1
+        bp.set_motion(np.zeros((s.P + 2, 3)))
+        with pytest.raises(bpmod.SasError) as ei:
+            bp.form()
+        assert ei.value.status == -2
