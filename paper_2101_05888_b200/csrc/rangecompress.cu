@@ -125,6 +125,12 @@ __device__ __forceinline__ void dft16(float2 v[16]) {
 #undef SL
 }
 
+#ifndef RC_TW_RECUR
+#define RC_TW_RECUR 1
+#endif
+#ifndef RC_MINB
+#define RC_MINB 2
+#endif
 // twiddle W_4096^m (forward sign) from the global table (L1 resident)
 __device__ __forceinline__ float2 twid(const float2* __restrict__ tw, int m) { return __ldg(tw + m); }
 
@@ -132,12 +138,21 @@ __device__ __forceinline__ float2 twid(const float2* __restrict__ tw, int m) { r
 template <bool INV, int NS>
 __device__ __forceinline__ void pass_store(float2 v[16], float2* sm, const float2* __restrict__ tw, int j) {
   const int k = j & (NS - 1);
+  float2 w1, wr;
+  (void)w1; (void)wr;
   if (NS > 1) {
 #pragma unroll
     for (int r = 1; r < 16; ++r) {
+#if RC_TW_RECUR
+      // w_r = w_1^r by recurrence (one table load per pass; ~r ulp of phase error)
+      if (r == 1) { w1 = twid(tw, (k * (256 / NS)) & (kL - 1)); if (INV) w1.y = -w1.y; wr = w1; }
+      else wr = cmul(wr, w1);
+      v[r] = cmul(v[r], wr);
+#else
       float2 w = twid(tw, (r * k * (256 / NS)) & (kL - 1));
       if (INV) w.y = -w.y;
       v[r] = cmul(v[r], w);
+#endif
     }
   }
   dft16<INV, false>(v);
@@ -150,11 +165,19 @@ __device__ __forceinline__ void pass_store(float2 v[16], float2* sm, const float
 template <bool INV, int NS>
 __device__ __forceinline__ void pass_regs(float2 v[16], const float2* __restrict__ tw, int j) {
   const int k = j & (NS - 1);
+  float2 w1, wr;
+  (void)w1; (void)wr;
 #pragma unroll
   for (int r = 1; r < 16; ++r) {
+#if RC_TW_RECUR
+    if (r == 1) { w1 = twid(tw, (k * (256 / NS)) & (kL - 1)); if (INV) w1.y = -w1.y; wr = w1; }
+    else wr = cmul(wr, w1);
+    v[r] = cmul(v[r], wr);
+#else
     float2 w = twid(tw, (r * k * (256 / NS)) & (kL - 1));
     if (INV) w.y = -w.y;
     v[r] = cmul(v[r], w);
+#endif
   }
   dft16<INV, false>(v);
 }
@@ -203,7 +226,7 @@ __global__ void __launch_bounds__(kFT) rc_prep_kernel(const float2* __restrict__
   for (int r = 0; r < 16; ++r) H[j + r * kFT] = make_float2(v[sig(r)].x * sc, -v[sig(r)].y * sc);
 }
 
-__global__ void __launch_bounds__(kFT, 2) rc_fft_kernel(const float2* __restrict__ raw, int Ns, int V,
+__global__ void __launch_bounds__(kFT, RC_MINB) rc_fft_kernel(const float2* __restrict__ raw, int Ns, int V,
                                                         const float2* __restrict__ H, const float2* __restrict__ tw_g,
                                                         float2* __restrict__ out) {
   __shared__ float2 sm[kPad];

@@ -14,14 +14,14 @@ t = np.arange(nr) / fs - Tp / 2
 rep = torch.from_numpy((np.exp(1j * np.pi * (B / Tp) * t ** 2) / np.sqrt(nr)).astype(np.complex64)).cuda()
 x = torch.randn(P, E, Ns, dtype=torch.complex64, device="cuda")
 y = torch.empty_like(x)
-for _ in range(3):
+for _ in range(50):   # warm the clocks up
     pkg.rangecompress_device(x, rep, y)
 torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record()
-for _ in range(10):
+for _ in range(50):
     pkg.rangecompress_device(x, rep, y)
 e1.record()
 torch.cuda.synchronize()
-ms = e0.elapsed_time(e1) / 10
+ms = e0.elapsed_time(e1) / 50
 print(os.environ.get("SASBP_LIB", "default"), f"{ms:.3f} ms", f"{16 * P * E * Ns / ms / 1e6:.0f} GB/s")
