@@ -134,6 +134,18 @@ def cpu_oracle_rate(s, echoes, seconds: float, seed: int = 123):
                       f"({terms:.3e} terms, {dt:.1f} s, fp64 C + OpenMP)"}
 
 
+def _profile_traffic(name, config):
+    """dram bytes per launch from a committed ncu summary (profiles/), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", name)) as f:
+            pj = json.load(f)
+        if config is not None and pj.get("config") != config:
+            return None
+        return pj.get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
 def _measured_hbm():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -355,7 +367,8 @@ def run_sasbp(args):
         k1 = {"kernel": "rc_fft_kernel (overlap-save, L=4096)", "Nr": nr, "ms": k1_ms,
               "achieved": k1_bytes / (k1_ms * 1e-3) / 1e9, "unit": "GB/s", "bound": "hbm", "peak": hbm[0],
               "peak_source": hbm[1], "frac": k1_bytes / (k1_ms * 1e-3) / 1e9 / hbm[0],
-              "algorithmic_bytes": k1_bytes, "note": "16 B per sample: read raw + write compressed once"}
+              "algorithmic_bytes": k1_bytes, "note": "16 B per sample: read raw + write compressed once",
+              "traffic": _profile_traffic("ncu_k1_r01.json", None)}
         del out_d
 
     cpu = None
@@ -364,16 +377,7 @@ def run_sasbp(args):
         cpu["cpu_model"] = host_cpu_model()
 
     if rank == 0:
-        traffic = None
-        prof = os.path.join(ROOT, "profiles", "ncu_tdbp_latest.json")
-        if os.path.exists(prof):
-            try:
-                with open(prof) as f:
-                    pj = json.load(f)
-                if pj.get("config") == args.config:
-                    traffic = pj.get("dram_bytes_per_launch")
-            except Exception:
-                traffic = None
+        traffic = _profile_traffic("ncu_tdbp_latest.json", args.config)
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
