@@ -68,6 +68,13 @@ def _load():
         lib.oracle_tdbp_points_motion.restype = ctypes.c_int
         lib.oracle_delay_moving.argtypes = [f64p, f64p, f64p, f64p, ctypes.c_double]
         lib.oracle_delay_moving.restype = ctypes.c_double
+        lib.oracle_tdbp_points_refracted.argtypes = [f32p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                                     f64p, f64p, f64p, ctypes.c_double, ctypes.c_double,
+                                                     ctypes.c_double, ctypes.c_double, ctypes.c_double, f64p,
+                                                     ctypes.c_int64, f64p, i64p]
+        lib.oracle_tdbp_points_refracted.restype = ctypes.c_int
+        lib.oracle_travel_refracted.argtypes = [f64p, f64p, ctypes.c_double, ctypes.c_double, ctypes.c_double]
+        lib.oracle_travel_refracted.restype = ctypes.c_double
         lib.oracle_rangecompress.argtypes = [f32p, ctypes.c_int64, ctypes.c_int32, f32p,
                                              ctypes.c_int32, f64p]
         lib.oracle_rangecompress.restype = ctypes.c_int
@@ -150,6 +157,31 @@ def tdbp_points_motion(echoes, tx, rx, t0, vel, fc, fs, c, pts, with_count=False
         raise ValueError("oracle_tdbp_points_motion: invalid arguments")
     res = out[:, 0] + 1j * out[:, 1]
     return (res, cnt) if with_count else res
+
+
+def tdbp_points_refracted(echoes, tx, rx, t0, zb, c2, fc, fs, c, pts, with_count=False):
+    """TDBP through a flat sediment-water interface z = zb (sediment speed c2, water speed c)."""
+    lib = _load()
+    echoes, P, E, Ns, tx, rx, t0 = _echo_arrays(echoes, tx, rx, t0)
+    pts = np.ascontiguousarray(pts, dtype=np.float64).reshape(-1, 3)
+    N = pts.shape[0]
+    out = np.zeros((N, 2), dtype=np.float64)
+    cnt = np.zeros(N, dtype=np.int64) if with_count else None
+    rc = lib.oracle_tdbp_points_refracted(_p(echoes, ctypes.c_float), P, E, Ns, _p(tx, ctypes.c_double),
+                                          _p(rx, ctypes.c_double), _p(t0, ctypes.c_double), float(zb), float(c2),
+                                          float(fc), float(fs), float(c), _p(pts, ctypes.c_double), N,
+                                          _p(out, ctypes.c_double), _p(cnt, ctypes.c_int64))
+    if rc != 0:
+        raise ValueError("oracle_tdbp_points_refracted: invalid arguments")
+    res = out[:, 0] + 1j * out[:, 1]
+    return (res, cnt) if with_count else res
+
+
+def travel_refracted(x, s, zb, c1, c2):
+    lib = _load()
+    a = [np.ascontiguousarray(q, dtype=np.float64).reshape(3) for q in (x, s)]
+    return float(lib.oracle_travel_refracted(_p(a[0], ctypes.c_double), _p(a[1], ctypes.c_double), float(zb),
+                                             float(c1), float(c2)))
 
 
 def delay_moving(x, tx, rx, v, c):

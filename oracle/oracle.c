@@ -210,6 +210,73 @@ int oracle_tdbp_points_gated(const float* echoes, int32_t P, int32_t E, int32_t 
 }
 
 /*
+ * One-way travel time from a sensor s in the water to x across a flat sediment-water
+ * interface (NEXT-3, reading R17; "include a sediment-water interface refraction model in
+ * determining propagation time"): interface the horizontal plane z = zb (NED,
+ * z down), sound speed c1 above (water) and c2 below (sediment).  For x above the interface the
+ * path is straight; for x below, Fermat's principle gives
+ *     t = min_xi  sqrt(xi^2 + h1^2)/c1 + sqrt((D - xi)^2 + h2^2)/c2,
+ * D = horizontal distance s -> x, h1 = zb - s_z, h2 = x_z - zb (Snell's law at the minimum);
+ * solved by Newton's method on the convex objective from the straight-line crossing, to
+ * |d xi| < 1e-14 (D + h1 + h2).
+ */
+static double travel_refracted(const double* x, const double* s, double zb, double c1, double c2) {
+  const double h2 = x[2] - zb;
+  if (h2 <= 0.0) return dist3(x, s) / c1;
+  const double h1 = zb - s[2];
+  const double dx = x[0] - s[0], dy = x[1] - s[1];
+  const double D = sqrt(dx * dx + dy * dy);
+  double xi = D * h1 / (h1 + h2);
+  for (int it = 0; it < 100; ++it) {
+    const double L1 = sqrt(xi * xi + h1 * h1), L2 = sqrt((D - xi) * (D - xi) + h2 * h2);
+    const double f1 = xi / (c1 * L1) - (D - xi) / (c2 * L2);
+    const double f2 = h1 * h1 / (c1 * L1 * L1 * L1) + h2 * h2 / (c2 * L2 * L2 * L2);
+    double nx = xi - f1 / f2;
+    if (nx < 0.0) nx = 0.5 * xi;
+    if (nx > D) nx = 0.5 * (xi + D);
+    const double step = fabs(nx - xi);
+    xi = nx;
+    if (step <= 1e-14 * (D + h1 + h2)) break;
+  }
+  return sqrt(xi * xi + h1 * h1) / c1 + sqrt((D - xi) * (D - xi) + h2 * h2) / c2;
+}
+
+/*
+ * TDBP through a flat sediment-water interface (NEXT-3): the definition with the straight-path
+ * delay replaced by tau = travel_refracted(x, tx) + travel_refracted(x, rx).  Sensors must be in
+ * the water (tx_z, rx_z < zb); c is the water sound speed c1.
+ */
+int oracle_tdbp_points_refracted(const float* echoes, int32_t P, int32_t E, int32_t Ns, const double* tx,
+                                 const double* rx, const double* t0, double zb, double c2, double fc, double fs,
+                                 double c, const double* pts, int64_t N, double* out, int64_t* n_in) {
+  if (P < 1 || E < 1 || Ns < 1 || N < 0 || !(c > 0) || !(fs > 0) || !(c2 > 0)) return -1;
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int64_t i = 0; i < N; ++i) {
+    const double* x = pts + 3 * i;
+    double ar = 0.0, ai = 0.0;
+    int64_t cnt = 0;
+    for (int32_t p = 0; p < P; ++p) {
+      double t0p = t0 ? t0[p] : 0.0;
+      const double tt = travel_refracted(x, tx + 3 * p, zb, c, c2);
+      for (int32_t e = 0; e < E; ++e) {
+        const float* ch = echoes + 2 * ((int64_t)p * E + e) * (int64_t)Ns;
+        const double tau = tt + travel_refracted(x, rx + 3 * ((int64_t)p * E + e), zb, c, c2);
+        cnt += one_term_tau(x, ch, Ns, tau, t0p, fc, fs, &ar, &ai);
+      }
+    }
+    out[2 * i] = ar;
+    out[2 * i + 1] = ai;
+    if (n_in) n_in[i] = cnt;
+  }
+  return 0;
+}
+
+/* One-way refracted travel time alone (for the pins). */
+double oracle_travel_refracted(const double* x, const double* s, double zb, double c1, double c2) {
+  return travel_refracted(x, s, zb, c1, c2);
+}
+
+/*
  * TDBP with continuous receiver motion at explicit points (NEXT-2): the definition with the
  * stop-and-hop delay replaced by delay_moving (per-ping velocity vel[P][3], NED m/s).
  */

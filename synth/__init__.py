@@ -52,7 +52,8 @@ def _load():
         lib.synth_echoes.argtypes = [ctypes.POINTER(ctypes.c_float), ctypes.c_int32, ctypes.c_int32,
                                      ctypes.c_int32, f64p, f64p, f64p, f64p, ctypes.c_double,
                                      ctypes.c_double, ctypes.c_double, ctypes.c_double,
-                                     ctypes.c_int32, f64p, f64p, ctypes.c_int64, ctypes.c_double, f64p]
+                                     ctypes.c_int32, f64p, f64p, ctypes.c_int64, ctypes.c_double, f64p,
+                                     ctypes.c_int32, ctypes.c_double, ctypes.c_double]
         lib.synth_echoes.restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -94,6 +95,7 @@ class Scenario:
     half_support: int = 16
     nav_nominal: Optional[tuple] = None   # (tx, rx) unperturbed nav (cfg 3)
     vel: Optional[np.ndarray] = None      # [P][3] platform velocity during reception (None = stop-and-hop)
+    medium: Optional[tuple] = None        # (zb, c2): flat sediment interface z = zb, sediment speed c2
 
     @property
     def P(self):
@@ -125,7 +127,9 @@ class Scenario:
         rc = lib.synth_echoes(out.ctypes.data_as(ctypes.POINTER(ctypes.c_float)), P, E, Ns, ptr(tx),
                               ptr(rx), ptr(t0), ptr(rot), self.fc, self.bandwidth, self.fs, self.c,
                               self.half_support, ptr(scat), ptr(sig), scat.shape[0],
-                              self.sin_half_beam, ptr(vel))
+                              self.sin_half_beam, ptr(vel), 1 if self.medium else 0,
+                              float(self.medium[0]) if self.medium else 0.0,
+                              float(self.medium[1]) if self.medium else 0.0)
         if rc != 0:
             raise ValueError("synth_echoes failed")
         return out.view(np.complex64).reshape(P, E, Ns)

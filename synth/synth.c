@@ -24,6 +24,28 @@
 
 #define SYN_PI 3.14159265358979323846264338328
 
+/* Forward-model one-way time from a sensor s (in water) to a scatterer x across the flat
+ * interface z = zb (c1 above, c2 below), Fermat path; also returns the geometric path length. */
+static double syn_travel(const double* x, const double* s, double zb, double c1, double c2, double* len) {
+  double dx = x[0] - s[0], dy = x[1] - s[1], dz = x[2] - s[2];
+  double h2 = x[2] - zb;
+  if (h2 <= 0.0) {
+    *len = sqrt(dx * dx + dy * dy + dz * dz);
+    return *len / c1;
+  }
+  double h1 = zb - s[2], D = sqrt(dx * dx + dy * dy);
+  double lo = 0.0, hi = D;   /* bisection on the derivative of the convex objective (robust) */
+  for (int it = 0; it < 200 && hi - lo > 1e-15 * (D + 1.0); ++it) {
+    double m = 0.5 * (lo + hi);
+    double g = m / (c1 * sqrt(m * m + h1 * h1)) - (D - m) / (c2 * sqrt((D - m) * (D - m) + h2 * h2));
+    if (g > 0) hi = m; else lo = m;
+  }
+  double xi = 0.5 * (lo + hi);
+  double L1 = sqrt(xi * xi + h1 * h1), L2 = sqrt((D - xi) * (D - xi) + h2 * h2);
+  *len = L1 + L2;
+  return L1 / c1 + L2 / c2;
+}
+
 /*
  * echoes   : float32 [P][E][Ns][2], accumulated into (caller zeroes it)
  * tx       : [P][3]; rx : [P][E][3]; t0 : [P]
@@ -34,7 +56,7 @@
 int synth_echoes(float* echoes, int32_t P, int32_t E, int32_t Ns, const double* tx, const double* rx,
                  const double* t0, const double* body_rot, double fc, double B, double fs, double c,
                  int32_t half_support, const double* scat, const double* sigma, int64_t S,
-                 double sin_half_beam, const double* vel) {
+                 double sin_half_beam, const double* vel, int32_t refract, double zb, double c2) {
   if (P < 1 || E < 1 || Ns < 1 || S < 0 || !(fs > 0) || !(c > 0) || !(B > 0)) return -1;
   const double step = SYN_PI * B / fs; /* sinc argument increment (radians of pi x) */
   const double cst = cos(step), snt = sin(step);
@@ -58,7 +80,12 @@ int synth_echoes(float* echoes, int32_t P, int32_t E, int32_t Ns, const double* 
         double rrx = sqrt(wx * wx + wy * wy + wz * wz);
         if (rrx <= 0) continue;
         double tau = (rtx + rrx) / c;
-        if (vel) {  /* receiver moving with the platform during reception: tau = (R_tx + |x - rx - v tau|)/c */
+        if (refract) {   /* sediment-water interface: both legs follow Fermat paths */
+          double lt, lr;
+          tau = syn_travel(X, T, zb, c, c2, &lt) + syn_travel(X, Rx, zb, c, c2, &lr);
+          rrx = lr;
+          (void)lt;
+        } else if (vel) {  /* receiver moving with the platform during reception: tau = (R_tx + |x - rx - v tau|)/c */
           const double* V = vel + 3 * p;
           for (int it = 0; it < 8; ++it) {
             double qx = wx - V[0] * tau, qy = wy - V[1] * tau, qz = wz - V[2] * tau;

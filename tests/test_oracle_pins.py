@@ -488,3 +488,61 @@ def test_moving_receiver_focus_cfg1():
     assert 0.96 <= abs(img[k]) / bound <= 1.01
     sh = oracle.tdbp_points(e, s.tx, s.rx, s.t0, s.fc, s.fs, s.c, x[None])[0]
     assert 20 * np.log10(abs(img[k]) / abs(sh)) >= 6.0
+
+
+# ---------------------------------------------------------------- sediment refraction (NEXT-3, reading R17)
+
+def test_refraction_normal_incidence_closed_form():
+    """Sensor straight above the voxel: t = h1/c1 + h2/c2 (Snell at normal incidence)."""
+    t = oracle.travel_refracted([0.3, -0.2, 0.5], [0.3, -0.2, -2.0], 0.0, 1500.0, 1700.0)
+    assert abs(t - (2.0 / 1500.0 + 0.5 / 1700.0)) <= 1e-17
+
+
+def test_refraction_reduces_to_straight_path():
+    """Equal sound speeds, or a voxel above the interface, give the straight path |x - s| / c1."""
+    rng = np.random.default_rng(1)
+    for _ in range(20):
+        s = np.array([*rng.uniform(-2, 2, 2), rng.uniform(-3, -0.5)])
+        x = np.array([*rng.uniform(-2, 2, 2), rng.uniform(0.01, 1.5)])
+        assert abs(oracle.travel_refracted(x, s, 0.0, 1500.0, 1500.0) - np.linalg.norm(x - s) / 1500.0) <= 1e-15
+        xa = np.array([x[0], x[1], -0.3])
+        t = oracle.travel_refracted(xa, s, 0.0, 1500.0, 1700.0)
+        assert abs(t - np.linalg.norm(xa - s) / 1500.0) <= 1e-15 * t
+
+
+def test_refraction_is_fermat_minimum_and_snell():
+    """Brute force over interface points: the oracle time is the minimum (Fermat), and at the
+    minimiser sin(theta1)/c1 = sin(theta2)/c2 (Snell)."""
+    c1, c2 = 1500.0, 1650.0
+    s = np.array([0.2, -0.4, -1.8])
+    x = np.array([1.7, 0.9, 0.45])
+    D = np.hypot(*(x[:2] - s[:2]))
+    h1, h2 = -s[2], x[2]
+    xi = np.linspace(0, D, 200001)
+    tt = np.sqrt(xi ** 2 + h1 ** 2) / c1 + np.sqrt((D - xi) ** 2 + h2 ** 2) / c2
+    k = np.argmin(tt)
+    t = oracle.travel_refracted(x, s, 0.0, c1, c2)
+    assert t <= tt.min() + 1e-15 and tt.min() - t <= 1e-12
+    xs = xi[k]
+    s1, s2 = xs / np.hypot(xs, h1), (D - xs) / np.hypot(D - xs, h2)
+    assert abs(s1 / c1 - s2 / c2) <= 1e-3 * s1 / c1
+
+
+def test_refraction_focuses_buried_target():
+    """A target 0.20 m below the seabed in fast sediment (c2 = 1700 m/s): imaging with the
+    refracted delay focuses it at its true voxel; straight water-speed rays place it shallower
+    (apparent depth ~ h c1/c2), the P:317 motivation for the interface model."""
+    s = synth.scenario(4, reduced=True)
+    g = dict(s.grid)
+    tgt = np.array([[3.0, 3.1, 0.20]])
+    pos, pix = synth._snap(g, tgt)
+    s.scat, s.sigma = pos, np.ones(1, dtype=np.complex128)      # the target alone (no speckle)
+    s.targets, s.target_pixels = pos, pix
+    s.medium = (0.0, 1700.0)
+    e = s.echoes()
+    idx = s.sample_pixels(0, window=11)
+    pts = oracle.grid_points(g, idx)
+    a = np.abs(oracle.tdbp_points_refracted(e, s.tx, s.rx, s.t0, 0.0, 1700.0, s.fc, s.fs, s.c, pts))
+    b = np.abs(oracle.tdbp_points(e, s.tx, s.rx, s.t0, s.fc, s.fs, s.c, pts))
+    assert tuple(idx[np.argmax(a)]) == tuple(pix[0])
+    assert idx[np.argmax(b)][2] < pix[0][2] - 1          # straight rays: shallower by > 1 voxel
