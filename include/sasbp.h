@@ -131,7 +131,7 @@ SASBP_API sas_status sas_bp_count_terms(sas_bp_t h, uint64_t* dense, uint64_t* i
  *   tile      pixels per CTA tile (x, y, z)
  *   window    samples staged per (tile, channel): cells of the interpolation window
  *   rx_mode   0 = 3-term series, 1 = 4-term series, 2 = exact receive-leg delay (chosen from
- *             the series truncation bound)
+ *             the series truncation bound), 3 = refracted (sas_bp_set_medium)
  *   tma       1 = windows staged by TMA tensor loads, 0 = cp.async fallback (odd Ns, unaligned
  *             device echoes, or SASBP_NO_TMA=1 in the environment at set_pings time)
  *   batch     channels (ping x element) staged per pipeline step
@@ -180,6 +180,17 @@ SASBP_API sas_status sas_bp_set_beam(sas_bp_t h, const sas_beam* beam, const dou
  *        ping set at form time (else SAS_E_STATE).
  * Errors: SAS_E_INVALID (non-finite or too fast), SAS_E_NOMEM, SAS_E_CUDA. */
 SASBP_API sas_status sas_bp_set_motion(sas_bp_t h, const double* vel, int32_t P);
+
+/* Sediment-water refraction (reading R17): a flat interface
+ * at z = zb (NED, z down) with sound speed c (create) above and c2 below; each leg's travel time
+ * follows Fermat's principle (Snell's law), straight in the water for points above the
+ * interface.  The kernel takes fp64 reference times per (tile, channel) and solves the
+ * refraction point per term in fp32 (3 Newton steps; the time is stationary at the solution).
+ *   c2 <= 0 -> back to isovelocity (R9).  Every sensor must be above the interface at form time
+ *   (else SAS_E_INVALID); cannot be combined with sas_bp_set_motion (SAS_E_UNSUPPORTED).
+ * Errors: SAS_E_INVALID for non-finite values; SAS_E_UNSUPPORTED if the window for a slow
+ * sediment would not fit shared memory. */
+SASBP_API sas_status sas_bp_set_medium(sas_bp_t h, double zb, double c2);
 
 /* Bytes of device memory the handle owns (image + workspace + owned ping copy). */
 SASBP_API size_t sas_bp_workspace_bytes(sas_bp_t h);

@@ -85,6 +85,10 @@ struct sas_bp_s {
   // continuous receiver motion (sas_bp_set_motion; NEXT-2)
   double* vel = nullptr;
   int vel_P = 0;
+  // sediment-water interface (sas_bp_set_medium; NEXT-3)
+  int refract = 0;
+  double zb = 0, c2 = 0;
+  double max_sensor_z = -INFINITY;   // of the current ping set
   bool has_pings = false;
   bool broken = false;
   size_t bytes = 0;
@@ -159,6 +163,10 @@ cudaError_t launch_gate(const sasbp::TdbpParams& prm, const sasbp::TmaDesc& tmap
   using namespace sasbp;
   const size_t smem = smem_bytes(prm.W);
   const int nt = 32 * WY * WZ;
+  if (prm.refract) {
+    if (MOTION) return cudaErrorNotSupported;   // rejected on the host before launch
+    return launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kRefract, TMA, GATE, false>, nt, prm, tmap, smem, st);
+  }
   switch (mode) {
     case kSeries3: return launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kSeries3, TMA, GATE, MOTION>, nt, prm, tmap, smem, st);
     case kSeries4: return launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kSeries4, TMA, GATE, MOTION>, nt, prm, tmap, smem, st);
@@ -246,6 +254,11 @@ cudaError_t launch_tdbp(sas_bp_t h, float2* image, unsigned long long* counter, 
   prm.tan_half_el = h->tan_half_el; prm.half_el = h->half_el;
   prm.d_max = h->d_max;
   prm.vel = h->vel;
+  prm.refract = h->refract; prm.zb = h->zb; prm.c2 = h->c2;
+  if (h->refract) {   // the window must cover the slowest medium: |grad tau| <= 2 / min(c, c2)
+    prm.hw = 2.0 * h->d_max * h->fs / std::min(h->c, h->c2);
+    prm.W = (int)std::ceil(2.0 * prm.hw + 4.0) + 3;
+  }
   switch (h->variant) {
 #if SASBP_K4
     case V2D: return launch_variant<4, 1, 1, 8, 1, false>(prm, h->tmap, h->use_tma, h->mode, count, st);
@@ -300,6 +313,9 @@ sas_status upload_geo(sas_bp_t h, int32_t P, int32_t E, int32_t Ns, const double
   }
   double rmin = INFINITY;
   for (size_t i = 0; i < (size_t)P * E; ++i) rmin = std::fmin(rmin, dist_to_box(rx + 3 * i, lo, hi));
+  h->max_sensor_z = -INFINITY;
+  for (int32_t p = 0; p < P; ++p) h->max_sensor_z = std::fmax(h->max_sensor_z, tx[3 * (size_t)p + 2]);
+  for (size_t i = 0; i < (size_t)P * E; ++i) h->max_sensor_z = std::fmax(h->max_sensor_z, rx[3 * i + 2]);
   h->mode = choose_mode(h->d_max, rmin, h->c / h->fc);
   h->P = P; h->E = E; h->Ns = Ns;
   return SAS_OK;
@@ -473,6 +489,8 @@ sas_status sas_bp_form_device(sas_bp_t h, void* image_dev, void* cuda_stream, in
   if (!h->has_pings) return fail(SAS_E_STATE, "sas_bp_form before sas_bp_set_pings");
   if (h->gate && h->axes && h->axes_P != h->P) return fail(SAS_E_STATE, "beam axes were given for %d pings, the ping set has %d", h->axes_P, h->P);
   if (h->vel && h->vel_P != h->P) return fail(SAS_E_STATE, "velocities were given for %d pings, the ping set has %d", h->vel_P, h->P);
+  if (h->refract && h->vel) return fail(SAS_E_UNSUPPORTED, "refraction and receiver motion cannot be combined");
+  if (h->refract && !(h->max_sensor_z < h->zb)) return fail(SAS_E_INVALID, "with an interface every sensor must be in the water (z < zb)");
   CK_H(h, cudaSetDevice(h->device));
   CK_H(h, launch_tdbp(h, (float2*)image_dev, h->counter, (flags & SAS_FORM_ACCUMULATE) ? 1 : 0, false,
                       (cudaStream_t)cuda_stream));
@@ -488,6 +506,8 @@ sas_status sas_bp_form(sas_bp_t h, float* image_out) {
   if (!h->has_pings) return fail(SAS_E_STATE, "sas_bp_form before sas_bp_set_pings");
   if (h->gate && h->axes && h->axes_P != h->P) return fail(SAS_E_STATE, "beam axes were given for %d pings, the ping set has %d", h->axes_P, h->P);
   if (h->vel && h->vel_P != h->P) return fail(SAS_E_STATE, "velocities were given for %d pings, the ping set has %d", h->vel_P, h->P);
+  if (h->refract && h->vel) return fail(SAS_E_UNSUPPORTED, "refraction and receiver motion cannot be combined");
+  if (h->refract && !(h->max_sensor_z < h->zb)) return fail(SAS_E_INVALID, "with an interface every sensor must be in the water (z < zb)");
   CK_H(h, cudaSetDevice(h->device));
   CK_H(h, launch_tdbp(h, h->image, h->counter, 0, false, h->stream));
   h->ctas_per_sm = g_last_occ;
@@ -524,6 +544,8 @@ sas_status sas_bp_form_streamed(sas_bp_t h, const float* echoes, int32_t P, int3
   h->has_pings = true;
   if (h->gate && h->axes && h->axes_P != h->P) return fail(SAS_E_STATE, "beam axes were given for %d pings, the ping set has %d", h->axes_P, h->P);
   if (h->vel && h->vel_P != h->P) return fail(SAS_E_STATE, "velocities were given for %d pings, the ping set has %d", h->vel_P, h->P);
+  if (h->refract && h->vel) return fail(SAS_E_UNSUPPORTED, "refraction and receiver motion cannot be combined");
+  if (h->refract && !(h->max_sensor_z < h->zb)) return fail(SAS_E_INVALID, "with an interface every sensor must be in the water (z < zb)");
   const int nch = P * E;
   int nchunk = chunks > 0 ? chunks : 8;
   nchunk = std::max(1, std::min(nchunk, (nch + 63) / 64));   // >= 64 channels per chunk
@@ -554,6 +576,8 @@ sas_status sas_bp_count_terms(sas_bp_t h, uint64_t* dense, uint64_t* in_win) {
   if (!h->has_pings) return fail(SAS_E_STATE, "sas_bp_count_terms before sas_bp_set_pings");
   if (h->gate && h->axes && h->axes_P != h->P) return fail(SAS_E_STATE, "beam axes were given for %d pings, the ping set has %d", h->axes_P, h->P);
   if (h->vel && h->vel_P != h->P) return fail(SAS_E_STATE, "velocities were given for %d pings, the ping set has %d", h->vel_P, h->P);
+  if (h->refract && h->vel) return fail(SAS_E_UNSUPPORTED, "refraction and receiver motion cannot be combined");
+  if (h->refract && !(h->max_sensor_z < h->zb)) return fail(SAS_E_INVALID, "with an interface every sensor must be in the water (z < zb)");
   const uint64_t npx = (uint64_t)h->grid.nx * h->grid.ny * h->grid.nz;
   if (dense) *dense = npx * (uint64_t)h->P * (uint64_t)h->E;
   if (in_win) {
@@ -646,12 +670,23 @@ sas_status sas_bp_set_motion(sas_bp_t h, const double* vel, int32_t P) {
   return SAS_OK;
 }
 
+sas_status sas_bp_set_medium(sas_bp_t h, double zb, double c2) {
+  g_err[0] = 0;
+  if (!h) return fail(SAS_E_INVALID, "handle is NULL");
+  if (!std::isfinite(zb) || !std::isfinite(c2)) return fail(SAS_E_INVALID, "zb and c2 must be finite");
+  if (c2 <= 0) { h->refract = 0; return SAS_OK; }   // isovelocity (R9)
+  const double Wn = std::ceil(2.0 * (2.0 * h->d_max * h->fs / std::min(h->c, c2)) + 4.0) + 3;
+  if (smem_bytes((int)Wn) > 200 * 1024) return fail(SAS_E_UNSUPPORTED, "sediment speed too low for the tile window");
+  h->refract = 1; h->zb = zb; h->c2 = c2;
+  return SAS_OK;
+}
+
 sas_status sas_bp_get_plan(sas_bp_t h, sas_bp_plan* out) {
   g_err[0] = 0;
   if (!h || !out) return fail(SAS_E_INVALID, "NULL argument");
   out->tile[0] = h->TX; out->tile[1] = h->TY; out->tile[2] = h->TZ;
   out->window = h->W;
-  out->rx_mode = h->has_pings ? h->mode : -1;
+  out->rx_mode = h->has_pings ? (h->refract ? 3 : h->mode) : -1;
   out->tma = h->has_pings ? (h->use_tma ? 1 : 0) : -1;
   out->batch = sasbp::kNB;
   out->ctas_per_sm = h->ctas_per_sm;

@@ -57,6 +57,7 @@ constexpr int kNB = SASBP_NB;   // channels per batch
 constexpr int kSeries3 = 0;     // 3-term series in eps
 constexpr int kSeries4 = 1;     // 4-term series in eps
 constexpr int kExact = 2;       // q / (sqrt(r^2 + q) + r)
+constexpr int kRefract = 3;     // Fermat path through a flat sediment interface (NEXT-3), per-term Newton
 
 struct TdbpParams {
   const float2* echoes;   // [P*E][Ns]
@@ -88,6 +89,9 @@ struct TdbpParams {
   double d_max;           // tile sphere radius (m)
   // continuous receiver motion (NEXT-2, reading R16): per-ping velocity [P][3] or NULL
   const double* vel;
+  // sediment-water interface (NEXT-3, reading R17): z = zb, sediment speed c2 (refract != 0)
+  int refract;
+  double zb, c2;
 };
 
 // per-channel constants in shared memory (fp64 prologue output)
@@ -127,6 +131,51 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 __device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
+
+// ---------------------------------------------------------------- refraction (NEXT-3, R17)
+// One-way Fermat time through the interface, fp64 (prologue reference): same definition as the
+// test-side reference, Newton from the straight-line crossing with bisection-style safeguards.
+__device__ double refr_time64(const double x[3], const double s[3], double zb, double c1, double c2) {
+  const double h2 = x[2] - zb;
+  const double dx = x[0] - s[0], dy = x[1] - s[1];
+  if (h2 <= 0.0) return sqrt(dx * dx + dy * dy + (x[2] - s[2]) * (x[2] - s[2])) / c1;
+  const double h1 = zb - s[2];
+  const double D = sqrt(dx * dx + dy * dy);
+  double xi = D * h1 / (h1 + h2);
+  for (int it = 0; it < 60; ++it) {
+    const double L1 = sqrt(xi * xi + h1 * h1), L2 = sqrt((D - xi) * (D - xi) + h2 * h2);
+    const double f1 = xi / (c1 * L1) - (D - xi) / (c2 * L2);
+    const double f2 = h1 * h1 / (c1 * L1 * L1 * L1) + h2 * h2 / (c2 * L2 * L2 * L2);
+    double nx = xi - f1 / f2;
+    if (nx < 0.0) nx = 0.5 * xi;
+    if (nx > D) nx = 0.5 * (xi + D);
+    const double st = fabs(nx - xi);
+    xi = nx;
+    if (st <= 1e-14 * (D + h1 + h2)) break;
+  }
+  return sqrt(xi * xi + h1 * h1) / c1 + sqrt((D - xi) * (D - xi) + h2 * h2) / c2;
+}
+
+// Per-term fp32 version in SAMPLES (k1 = fs/c1, k2 = fs/c2), tile-relative coordinates: voxel
+// offset e = d - s from the sensor, depth below the interface h2 = d_z - zbr, sensor height above
+// it h1 = zbr - s_z.  Newton on the convex objective (3 steps from the straight-line crossing,
+// each clamped to [0, D]); the time is stationary at the minimum, so the residual refraction-
+// point error enters only at second order.
+__device__ __forceinline__ float refr_time32(float ex, float ey, float ez, float h1, float h2, float k1, float k2) {
+  if (h2 <= 0.f) return sqrtf(fmaf(ex, ex, fmaf(ey, ey, ez * ez))) * k1;
+  const float D = sqrtf(fmaf(ex, ex, ey * ey));
+  float xi = D * h1 * rcp_approx(h1 + h2);
+#pragma unroll
+  for (int it = 0; it < 3; ++it) {
+    const float a = xi, b = D - xi;
+    const float i1 = rsqrt_approx(fmaf(a, a, h1 * h1)), i2 = rsqrt_approx(fmaf(b, b, h2 * h2));
+    const float f1 = a * k1 * i1 - b * k2 * i2;
+    const float f2 = h1 * h1 * k1 * i1 * i1 * i1 + h2 * h2 * k2 * i2 * i2 * i2;
+    xi = fminf(fmaxf(xi - f1 * rcp_approx(f2), 0.f), D);
+  }
+  const float a = xi, b = D - xi;
+  return sqrtf(fmaf(a, a, h1 * h1)) * k1 + sqrtf(fmaf(b, b, h2 * h2)) * k2;
+}
 
 // ---------------------------------------------------------------- FOV gate (NEXT-1, R15)
 constexpr int kGIn = 0, kGEdge = 1, kGOut = 2;
@@ -200,7 +249,7 @@ __device__ __forceinline__ void pixel_centre64(const TdbpParams& prm, int ix, in
 
 // fp64 prologue for one channel (row a2): reference geometry at the tile centre ct (and, for
 // gated kernels, the tile's cone classes).
-template <bool GATE, bool MOTION = false>
+template <bool GATE, bool MOTION = false, bool REFRACT = false>
 __device__ __forceinline__ ChanConst chan_prologue(const TdbpParams& prm, int ch, const double ct[3], int slot,
                                                    uint32_t win_base) {
   const int p = (int)(((double)ch + 0.5) * prm.inv_e);   // ch / E, exact for ch < 2^40
@@ -250,7 +299,15 @@ __device__ __forceinline__ ChanConst chan_prologue(const TdbpParams& prm, int ch
     const double s1 = -kap0 * kap0 / (prm.c * r_r);   // d kappa = -kap0^2 g1.d, g1 = (v - (u.v) u) / (c r)
     kg[0] = s1 * (V[0] - uv * ux); kg[1] = s1 * (V[1] - uv * uy); kg[2] = s1 * (V[2] - uv * uz);
   }
-  const double S = r_t + r_r;
+  double S = r_t + r_r;
+  double At = 0.0, Ar = 0.0;   // refraction: reference one-way times in samples
+  if (REFRACT) {
+    const double ctr[3] = {ct[0], ct[1], ct[2]};
+    const double tt = refr_time64(ctr, T, prm.zb, prm.c, prm.c2);
+    const double tr = refr_time64(ctr, R, prm.zb, prm.c, prm.c2);
+    S = prm.c * (tt + tr);          // c tau_ref: Uref and the reference phase below follow
+    At = tt * prm.fs; Ar = tr * prm.fs;
+  }
   const double Uref = fma(S, prm.k_s, -prm.t0[p] * prm.fs);   // absolute sample index at tile centre
   const double klo_d = floor(Uref - prm.hw) - 2.0;
   // even window start: a TMA box must start 16-B aligned (2 samples); the plan's W has one
@@ -276,6 +333,11 @@ __device__ __forceinline__ ChanConst chan_prologue(const TdbpParams& prm, int ch
   k.r_r = (float)r_r; k.r2_r = (float)(r_r * r_r);
   k.tx2x = (float)(2.0 * utx); k.tx2y = (float)(2.0 * uty); k.tx2z = (float)(2.0 * utz);
   k.r2_t = (float)(r_t * r_t); k.r_t = (float)r_t;
+  if (REFRACT) {   // sensor positions relative to the tile centre and reference times (samples)
+    k.ux2 = (float)(R[0] - ct[0]); k.uy2 = (float)(R[1] - ct[1]); k.uz2 = (float)(R[2] - ct[2]);
+    k.tx2x = (float)(T[0] - ct[0]); k.tx2y = (float)(T[1] - ct[1]); k.tx2z = (float)(T[2] - ct[2]);
+    k.a1 = (float)Ar; k.r_t = (float)At;
+  }
   k.ping = p;
   k.woff = (int)(win_base + (uint32_t)(slot * prm.W + Wh) * 16u - (uint32_t)kMagicBits * 16u);
   k.klo = klo;
@@ -417,6 +479,9 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
 
   const float kph = (float)(6.283185307179586 * prm.k_r);
   const float kfs = (float)prm.k_s;
+  // refraction: interface height relative to the tile centre, slownesses in samples per metre
+  const float zbr = MODE == kRefract ? (float)(prm.zb - ct[2]) : 0.f;
+  const float k1r = (float)(prm.fs / prm.c), k2r = MODE == kRefract ? (float)(prm.fs / prm.c2) : 0.f;
   const int nch = prm.ch_hi - prm.ch_lo;
   const int nbatch = (nch + kNB - 1) / kNB;
   // Channel order: every tile visits all batches, starting at a batch offset proportional to
@@ -456,7 +521,8 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
     if (sub < kBPW && bb < nbatch) {
       const int nbb = min(kNB, nch - bat(bb) * kNB);
       if (cl < nbb) {
-        const ChanConst k = chan_prologue<GATE, MOTION>(prm, prm.ch_lo + bat(bb) * kNB + cl, ct, cl, win_base);
+        const ChanConst k = chan_prologue<GATE, MOTION, MODE == kRefract>(prm, prm.ch_lo + bat(bb) * kNB + cl, ct, cl,
+                                                                         win_base);
         cc[(bb % kRing) * kNB + cl] = k;
         live = !(k.gate & 16);
       }
@@ -592,6 +658,14 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
         // transmit leg, exact range-relative form: dR = q / (sqrt(r^2 + q) + r), in samples
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
+          if (MODE == kRefract) {   // Fermat time through the interface minus the tile reference
+            const float t0v = refr_time32(DX[p].x - kc.tx2x, DY[p].x - kc.tx2y, DZ[p].x - kc.tx2z, zbr - kc.tx2z,
+                                          DZ[p].x - zbr, k1r, k2r);
+            const float t1v = refr_time32(DX[p].y - kc.tx2x, DY[p].y - kc.tx2y, DZ[p].y - kc.tx2z, zbr - kc.tx2z,
+                                          DZ[p].y - zbr, k1r, k2r);
+            BT[p] = make_float2(t0v - kc.r_t, t1v - kc.r_t);
+            continue;
+          }
           float2 q = __ffma2_rn(f2(kc.tx2y), AXIS ? f2(DYS[p]) : DY[p], DD[p]);
           q = __ffma2_rn(f2(kc.tx2x), DX[p], q);
           if (HAS_DZ) q = __ffma2_rn(f2(kc.tx2z), DZ[p], q);
@@ -623,7 +697,13 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
         q = __ffma2_rn(f2(kc.ux2), DX[p], q);
         if (HAS_DZ) q = __ffma2_rn(f2(kc.uz2), DZ[p], q);
         float2 U;
-        if (MODE == kExact) {
+        if (MODE == kRefract) {
+          const float r0 = refr_time32(DX[p].x - kc.ux2, DY[p].x - kc.uy2, DZ[p].x - kc.uz2, zbr - kc.uz2,
+                                       DZ[p].x - zbr, k1r, k2r);
+          const float r1 = refr_time32(DX[p].y - kc.ux2, DY[p].y - kc.uy2, DZ[p].y - kc.uz2, zbr - kc.uz2,
+                                       DZ[p].y - zbr, k1r, k2r);
+          U = __fadd2_rn(make_float2(r0 - kc.a1, r1 - kc.a1), BT[p]);
+        } else if (MODE == kExact) {
           const float2 r2 = __fadd2_rn(q, f2(kc.r2_r));
           const float den0 = fmaf(r2.x, rsqrt_approx(r2.x), kc.r_r);
           const float den1 = fmaf(r2.y, rsqrt_approx(r2.y), kc.r_r);
@@ -712,6 +792,15 @@ __global__ void __launch_bounds__(32 * WY * WZ) count_kernel(const TdbpParams pr
       const ChanConst kc = cc[c];
 #pragma unroll
       for (int k = 0; k < K; ++k) {
+        if (prm.refract) {   // counted with the fp64 refracted delay (off the clock)
+          double x[3];
+          pixel_centre64(prm, tm.ix(k), tm.iy(k), tm.iz(k), x);
+          const double tau = refr_time64(x, prm.tx + 3 * kc.ping, prm.zb, prm.c, prm.c2) +
+                             refr_time64(x, prm.rx + 3 * (size_t)(ch0 + c), prm.zb, prm.c, prm.c2);
+          const double ua = (tau - prm.t0[kc.ping]) * prm.fs;
+          cnt += (ok[k] && ua > -1.0 && ua < (double)prm.Ns) ? 1u : 0u;
+          continue;
+        }
         const float qt = fmaf(kc.tx2x, dx[k], fmaf(kc.tx2y, dy[k], fmaf(kc.tx2z, dz[k], dd[k])));
         const float qr = fmaf(kc.ux2, dx[k], fmaf(kc.uy2, dy[k], fmaf(kc.uz2, dz[k], dd[k])));
         const float rt = sqrtf(kc.r2_t + qt), rr = sqrtf(kc.r2_r + qr);

@@ -22,7 +22,7 @@ _NAMES = {0: "SAS_OK", -1: "SAS_E_INVALID", -2: "SAS_E_STATE", -3: "SAS_E_NOMEM"
 
 EXPORTS = ("sas_bp_create", "sas_bp_destroy", "sas_bp_set_pings", "sas_bp_set_pings_device", "sas_bp_form",
            "sas_bp_form_device", "sas_bp_count_terms", "sas_bp_workspace_bytes", "sas_rangecompress",
-           "sas_rangecompress_device", "sas_last_error", "sas_version", "sas_bp_get_plan", "sas_bp_form_streamed", "sas_bp_set_beam", "sas_bp_set_motion")
+           "sas_rangecompress_device", "sas_last_error", "sas_version", "sas_bp_get_plan", "sas_bp_form_streamed", "sas_bp_set_beam", "sas_bp_set_motion", "sas_bp_set_medium")
 
 
 class SasError(RuntimeError):
@@ -79,6 +79,7 @@ def load_library(path: Optional[str] = None):
         "sas_bp_form_streamed": ([vp, f32p, i32, i32, i32, f64p, f64p, f64p, f32p, i32], ctypes.c_int),
         "sas_bp_set_beam": ([vp, ctypes.POINTER(sas_beam), f64p, i32], ctypes.c_int),
         "sas_bp_set_motion": ([vp, f64p, i32], ctypes.c_int),
+        "sas_bp_set_medium": ([vp, ctypes.c_double, ctypes.c_double], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name, None)
@@ -280,11 +281,16 @@ class Backprojector:
         v = np.ascontiguousarray(vel, dtype=np.float64).reshape(-1, 3)
         _check(_lib.sas_bp_set_motion(self._h, _ptr(v, ctypes.c_double), v.shape[0]))
 
+    def set_medium(self, zb: float = 0.0, c2: float = 0.0):
+        """Flat sediment-water interface z = zb with sediment sound speed c2 (NEXT-3); c2 <= 0 =
+        isovelocity."""
+        _check(_lib.sas_bp_set_medium(self._h, float(zb), float(c2)))
+
     def plan(self) -> dict:
         """The execution plan (tile, window, rx_mode, tma, batch) -- sas_bp_get_plan."""
         p = sas_bp_plan()
         _check(_lib.sas_bp_get_plan(self._h, ctypes.byref(p)))
-        return {"tile": tuple(p.tile), "window": p.window, "rx_mode": ("series3", "series4", "exact")[p.rx_mode]
+        return {"tile": tuple(p.tile), "window": p.window, "rx_mode": ("series3", "series4", "exact", "refracted")[p.rx_mode]
                 if p.rx_mode >= 0 else None, "tma": None if p.tma < 0 else bool(p.tma), "batch": p.batch,
                 "ctas_per_sm": p.ctas_per_sm}
 

@@ -97,6 +97,7 @@ def test_null_handle_calls(lib):
     assert lib.sas_bp_get_plan(None, None) == sasbp.SAS_E_INVALID
     assert lib.sas_bp_set_beam(None, None, None, 0) == sasbp.SAS_E_INVALID
     assert lib.sas_bp_set_motion(None, None, 0) == sasbp.SAS_E_INVALID
+    assert lib.sas_bp_set_medium(None, 0.0, 1700.0) == sasbp.SAS_E_INVALID
     assert lib.sas_bp_workspace_bytes(None) == 0
 
 

@@ -563,3 +563,70 @@ def test_set_motion_errors(bpmod):
         with pytest.raises(bpmod.SasError) as ei:
             bp.form()
         assert ei.value.status == -2
+
+
+# ------------------------------------------------------------------ NEXT-3: sediment refraction
+
+def _refr_form(bpmod, s, e, zb, c2, counts=False):
+    with bpmod.Backprojector(s.fc, s.bandwidth, s.fs, s.c, s.grid) as bp:
+        bp.set_pings(e, s.tx, s.rx, s.t0)
+        bp.set_medium(zb, c2)
+        img = bp.form()
+        assert bp.plan()["rx_mode"] == "refracted"
+        return (img, bp.count_terms()) if counts else img
+
+
+@pytest.mark.parametrize("c2", [1700.0, 1560.0, 1450.0])
+def test_refracted_3d_vs_oracle(bpmod, c2):
+    """Reduced config 4 recorded through a sediment interface at z = 0 (fast and slow sediment):
+    GPU Fermat delays vs the oracle's exact refracted delays, full volume, and the in-window
+    term count."""
+    s = synth.scenario(4, reduced=True)
+    s.medium = (0.0, c2)
+    e = s.echoes()
+    (got, (dense, inwin)) = _refr_form(bpmod, s, e, 0.0, c2, counts=True)
+    ref, cnt = oracle.tdbp_points_refracted(e, s.tx, s.rx, s.t0, 0.0, c2, s.fc, s.fs, s.c,
+                                            oracle.grid_points(s.grid), with_count=True)
+    ref = ref.reshape(got.shape)
+    pk = s.target_pixels
+    _check(got, ref, _at(got, pk), _at(ref, pk), label=f"refracted c2={c2}")
+    assert abs(inwin - int(cnt.sum())) <= max(1, 1e-4 * cnt.sum())
+
+
+def test_refracted_interface_inside_volume(bpmod):
+    """Interface through the middle of the voxel grid: voxels above it take the straight water
+    path, those below the Fermat path."""
+    s = synth.scenario(4, reduced=True)
+    zb = 0.15
+    s.medium = (zb, 1650.0)
+    e = s.echoes()
+    got = _refr_form(bpmod, s, e, zb, 1650.0)
+    ref = oracle.tdbp_points_refracted(e, s.tx, s.rx, s.t0, zb, 1650.0, s.fc, s.fs, s.c,
+                                       oracle.grid_points(s.grid)).reshape(got.shape)
+    _check(got, ref, label="interface inside the volume")
+
+
+def test_refracted_equal_speed_is_dense(bpmod):
+    s = synth.scenario(4, reduced=True)
+    e = s.echoes()
+    got = _refr_form(bpmod, s, e, 0.0, s.c)
+    ref = oracle.tdbp_grid(e, s.tx, s.rx, s.t0, s.fc, s.fs, s.c, s.grid)
+    _check(got, ref, label="c2 = c")
+
+
+def test_set_medium_errors(bpmod):
+    s = synth.scenario(4, reduced=True)
+    e = s.echoes()
+    with bpmod.Backprojector(s.fc, s.bandwidth, s.fs, s.c, s.grid) as bp:
+        bp.set_pings(e, s.tx, s.rx, s.t0)
+        bp.set_medium(-2.5, 1700.0)                 # interface above the sensors (z = -2)
+        with pytest.raises(bpmod.SasError) as ei:
+            bp.form()
+        assert ei.value.status == -1
+        bp.set_medium(0.0, 1700.0)
+        bp.set_motion(np.zeros((s.P, 3)))
+        with pytest.raises(bpmod.SasError) as ei:
+            bp.form()
+        assert ei.value.status == -5
+        bp.set_motion(None)
+        bp.form()
