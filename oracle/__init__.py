@@ -14,7 +14,9 @@ delays, zero-extension values, point-target physics and invariants;
 ``rangecompress`` by the autocorrelation-peak, shift and mainlobe pins;
 ``tdbp_points_gated`` (NEXT-1, reading R15) by the wide-open special case (= dense),
 the azimuth / elevation boundary examples, monotonicity in the beamwidth, rigid-rotation
-invariance and the config-1 target under the generator's own beam.
+invariance and the config-1 target under the generator's own beam; the NEXT-4 variants
+``tdbp_points_weighted`` (R18), ``upsample`` / ``lanczos4`` (R19) and ``baseband`` (R20) by
+closed forms, interpolating / band-limited reproduction properties and config-1 physics.
 """
 from __future__ import annotations
 
@@ -78,6 +80,16 @@ def _load():
         lib.oracle_rangecompress.argtypes = [f32p, ctypes.c_int64, ctypes.c_int32, f32p,
                                              ctypes.c_int32, f64p]
         lib.oracle_rangecompress.restype = ctypes.c_int
+        lib.oracle_tdbp_points_weighted.argtypes = lib.oracle_tdbp_points.argtypes
+        lib.oracle_tdbp_points_weighted.restype = ctypes.c_int
+        lib.oracle_lanczos4.argtypes = [ctypes.c_double]
+        lib.oracle_lanczos4.restype = ctypes.c_double
+        lib.oracle_upsample.argtypes = [f32p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, f64p]
+        lib.oracle_upsample.restype = ctypes.c_int
+        lib.oracle_baseband.argtypes = [f32p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_double,
+                                        ctypes.c_double, f64p, f32p, ctypes.c_int32, ctypes.c_int32,
+                                        ctypes.c_int32, f64p]
+        lib.oracle_baseband.restype = ctypes.c_int
         lib.oracle_num_threads.restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -250,6 +262,62 @@ def rangecompress(raw, replica):
     if rc != 0:
         raise ValueError("oracle_rangecompress: invalid arguments")
     return (out[..., 0] + 1j * out[..., 1]).reshape(shape)
+
+
+def tdbp_points_weighted(echoes, tx, rx, t0, fc, fs, c, pts, with_count=False):
+    """Spreading-compensated TDBP (NEXT-4, R18): every term times R_tx * R_rx."""
+    lib = _load()
+    echoes, P, E, Ns, tx, rx, t0 = _echo_arrays(echoes, tx, rx, t0)
+    pts = np.ascontiguousarray(pts, dtype=np.float64).reshape(-1, 3)
+    N = pts.shape[0]
+    out = np.zeros((N, 2), dtype=np.float64)
+    cnt = np.zeros(N, dtype=np.int64) if with_count else None
+    rc = lib.oracle_tdbp_points_weighted(_p(echoes, ctypes.c_float), P, E, Ns, _p(tx, ctypes.c_double),
+                                         _p(rx, ctypes.c_double), _p(t0, ctypes.c_double), float(fc),
+                                         float(fs), float(c), _p(pts, ctypes.c_double), N,
+                                         _p(out, ctypes.c_double), _p(cnt, ctypes.c_int64))
+    if rc != 0:
+        raise ValueError("oracle_tdbp_points_weighted: invalid arguments")
+    res = out[:, 0] + 1j * out[:, 1]
+    return (res, cnt) if with_count else res
+
+
+def lanczos4(s) -> float:
+    """The 8-tap interpolation kernel L(s) = sinc(s) sinc(s/4), |s| < 4 (R19)."""
+    return float(_load().oracle_lanczos4(float(s)))
+
+
+def upsample(x, U):
+    """xU band-limited upsampling by the 8-tap kernel (R19); x complex64 [..., Ns] ->
+    complex128 [..., U*Ns] at rate U*fs, same t0."""
+    lib = _load()
+    x = np.ascontiguousarray(x, dtype=np.complex64)
+    shape = x.shape
+    Ns = shape[-1]
+    nch = int(np.prod(shape[:-1])) if len(shape) > 1 else 1
+    out = np.zeros((nch, U * Ns, 2), dtype=np.float64)
+    rc = lib.oracle_upsample(_p(x.view(np.float32), ctypes.c_float), nch, Ns, int(U), _p(out, ctypes.c_double))
+    if rc != 0:
+        raise ValueError("oracle_upsample: invalid arguments")
+    return (out[..., 0] + 1j * out[..., 1]).reshape(shape[:-1] + (U * Ns,))
+
+
+def baseband(x, fs_in, fc, t0, h, D, Nout):
+    """Real passband [P][E][Nin] -> complex baseband [P][E][Nout] (R20): mix by
+    exp(-j 2 pi fc (t0_p + n/fs_in)), centred FIR h (odd length), keep every D-th sample."""
+    lib = _load()
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    if x.ndim != 3:
+        raise ValueError("x must be float32 [P][E][Nin]")
+    P, E, Nin = x.shape
+    h = np.ascontiguousarray(h, dtype=np.float32).ravel()
+    t0 = None if t0 is None else np.ascontiguousarray(t0, dtype=np.float64).reshape(P)
+    out = np.zeros((P, E, Nout, 2), dtype=np.float64)
+    rc = lib.oracle_baseband(_p(x, ctypes.c_float), P, E, Nin, float(fs_in), float(fc), _p(t0, ctypes.c_double),
+                             _p(h, ctypes.c_float), h.size, int(D), int(Nout), _p(out, ctypes.c_double))
+    if rc != 0:
+        raise ValueError("oracle_baseband: invalid arguments")
+    return out[..., 0] + 1j * out[..., 1]
 
 
 def num_threads() -> int:

@@ -33,6 +33,10 @@
  * Range compression (the paper presumes compressed data,
  * S:195):  y[n] = sum_{m=0}^{Nr-1} x[n+m] * conj(r[m]),  x[k] = 0 for k >= Ns,
  * the direct O(Ns*Nr) correlation in fp64.
+ *
+ * NEXT rows: gating (R15), moving receiver (R16), sediment refraction (R17),
+ * and the NEXT-4 interpolation / conditioning variants -- spreading weight R_tx R_rx (R18),
+ * 8-tap windowed-sinc xU upsampling (R19) and passband basebanding (R20).
  */
 #include <math.h>
 #include <stdint.h>
@@ -357,6 +361,121 @@ int oracle_rangecompress(const float* raw, int64_t nch, int32_t Ns, const float*
       }
       y[2 * n] = yr;
       y[2 * n + 1] = yi;
+    }
+  }
+  return 0;
+}
+
+/*
+ * Spreading-compensated TDBP at explicit points (NEXT-4, reading R18): every term of the
+ * definition multiplied by w = |x - tx_p| |x - rx_{p,e}|, the inverse of the spherical-spreading
+ * amplitude 1/(|x_TX - x| |x_RX - x|) of Eq. (eqn:backprojection) ("spreading
+ * compensation (multiplying by R_tx R_rx)").
+ */
+int oracle_tdbp_points_weighted(const float* echoes, int32_t P, int32_t E, int32_t Ns, const double* tx,
+                                const double* rx, const double* t0, double fc, double fs, double c,
+                                const double* pts, int64_t N, double* out, int64_t* n_in) {
+  if (P < 1 || E < 1 || Ns < 1 || N < 0 || !(c > 0) || !(fs > 0)) return -1;
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int64_t i = 0; i < N; ++i) {
+    const double* x = pts + 3 * i;
+    double ar = 0.0, ai = 0.0;
+    int64_t cnt = 0;
+    for (int32_t p = 0; p < P; ++p) {
+      double t0p = t0 ? t0[p] : 0.0;
+      const double rt = dist3(x, tx + 3 * p);
+      for (int32_t e = 0; e < E; ++e) {
+        const float* ch = echoes + 2 * ((int64_t)p * E + e) * (int64_t)Ns;
+        const double rr = dist3(x, rx + 3 * ((int64_t)p * E + e));
+        double tr = 0.0, ti = 0.0;
+        cnt += one_term_tau(x, ch, Ns, (rt + rr) / c, t0p, fc, fs, &tr, &ti);
+        ar += rt * rr * tr;                                    /* w = R_tx R_rx (R18) */
+        ai += rt * rr * ti;
+      }
+    }
+    out[2 * i] = ar;
+    out[2 * i + 1] = ai;
+    if (n_in) n_in[i] = cnt;
+  }
+  return 0;
+}
+
+/*
+ * The 8-tap windowed-sinc interpolation kernel (NEXT-4, reading R19; "band-limited
+ * via 8-tap windowed-sinc"; the paper is silent on interpolation): the Lanczos window of
+ * order 4,
+ *     L(s) = sinc(s) sinc(s/4)  for |s| < 4,   0 otherwise,   sinc(s) = sin(pi s)/(pi s), sinc(0) = 1.
+ */
+static double lanczos4(double s) {
+  const double PI = 3.141592653589793238462643383279;
+  if (s == 0.0) return 1.0;
+  if (fabs(s) >= 4.0) return 0.0;
+  return (sin(PI * s) / (PI * s)) * (sin(PI * s / 4.0) / (PI * s / 4.0));
+}
+
+double oracle_lanczos4(double s) { return lanczos4(s); }
+
+/*
+ * Band-limited xU upsampling of complex channels by the 8-tap kernel (NEXT-4, R19):
+ *     y[U n + r] = sum_{m=-3}^{4} x[n + m] L(r/U - m),   r = 0..U-1,  n = 0..Ns-1,
+ * x zero-extended outside 0..Ns-1 (reading R2).  Output sample j = U n + r sits at the input
+ * time n + r/U, so the upsampled series has rate U fs and the same t0.
+ *   x : complex64 [nch][Ns], out : complex128 [nch][U Ns].
+ */
+int oracle_upsample(const float* x, int64_t nch, int32_t Ns, int32_t U, double* out) {
+  if (nch < 0 || Ns < 1 || U < 1) return -1;
+#pragma omp parallel for schedule(static)
+  for (int64_t ch = 0; ch < nch; ++ch) {
+    const float* xc = x + 2 * ch * (int64_t)Ns;
+    double* y = out + 2 * ch * (int64_t)Ns * U;
+    for (int32_t n = 0; n < Ns; ++n) {
+      for (int32_t r = 0; r < U; ++r) {
+        double yr = 0.0, yi = 0.0;
+        for (int32_t m = -3; m <= 4; ++m) {
+          double dr, di;
+          sample_at(xc, Ns, (int64_t)n + m, &dr, &di);
+          const double w = lanczos4((double)r / (double)U - (double)m);
+          yr += w * dr;
+          yi += w * di;
+        }
+        y[2 * ((int64_t)U * n + r)] = yr;
+        y[2 * ((int64_t)U * n + r) + 1] = yi;
+      }
+    }
+  }
+  return 0;
+}
+
+/*
+ * Basebanding of real passband channels (the optional input; reading
+ * R20): mix down by the carrier measured from the ping's transmit instant (R3, R4), low-pass
+ * with the caller's FIR taps h[0..Nh-1] (Nh odd, centred) and keep every D-th sample:
+ *     z[n] = x[n] exp(-j 2 pi fc (t0_p + n / fs_in)),       z[n] = 0 outside 0..Nin-1
+ *     y[m] = sum_{k=0}^{Nh-1} h[k] z[m D + (Nh-1)/2 - k],     m = 0..Nout-1
+ * Output sample m is taken at t0_p + m D / fs_in: rate fs_in / D, same t0.
+ *   x : float [P][E][Nin], t0 : [P] or NULL (= 0), out : complex128 [P][E][Nout].
+ */
+int oracle_baseband(const float* x, int32_t P, int32_t E, int32_t Nin, double fs_in, double fc,
+                    const double* t0, const float* h, int32_t Nh, int32_t D, int32_t Nout, double* out) {
+  if (P < 1 || E < 1 || Nin < 1 || Nh < 1 || (Nh % 2) == 0 || D < 1 || Nout < 1 || !(fs_in > 0)) return -1;
+  const int64_t nch = (int64_t)P * E;
+  const int32_t half = (Nh - 1) / 2;
+#pragma omp parallel for schedule(static)
+  for (int64_t ch = 0; ch < nch; ++ch) {
+    const float* xc = x + ch * (int64_t)Nin;
+    const double t0p = t0 ? t0[ch / E] : 0.0;
+    double* y = out + 2 * ch * (int64_t)Nout;
+    for (int32_t m = 0; m < Nout; ++m) {
+      double yr = 0.0, yi = 0.0;
+      for (int32_t k = 0; k < Nh; ++k) {
+        const int64_t n = (int64_t)m * D + half - k;
+        if (n < 0 || n >= Nin) continue;
+        const double ph = -ORACLE_TWO_PI * fc * (t0p + (double)n / fs_in);
+        yr += (double)h[k] * (double)xc[n] * cos(ph);
+        yi += (double)h[k] * (double)xc[n] * sin(ph);
+      }
+      y[2 * m] = yr;
+      y[2 * m + 1] = yi;
     }
   }
   return 0;
