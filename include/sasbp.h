@@ -192,6 +192,14 @@ SASBP_API sas_status sas_bp_set_motion(sas_bp_t h, const double* vel, int32_t P)
  * sediment would not fit shared memory. */
 SASBP_API sas_status sas_bp_set_medium(sas_bp_t h, double zb, double c2);
 
+/* Spreading compensation (reading R18): with spreading = 1 every term is
+ * multiplied by w = |x - tx_p| |x - rx_{p,e}|, the inverse of the spherical-spreading amplitude
+ * 1/(|x_TX - x| |x_RX - x|) of Eq. (eqn:backprojection).  spreading = 0 (the
+ * default) is the unweighted sum (R6).  Defined for stop-and-hop straight rays: form returns
+ * SAS_E_UNSUPPORTED when combined with sas_bp_set_motion or sas_bp_set_medium.
+ * Errors: SAS_E_INVALID for a NULL handle or spreading not in {0, 1}. */
+SASBP_API sas_status sas_bp_set_weighting(sas_bp_t h, int32_t spreading);
+
 /* Bytes of device memory the handle owns (image + workspace + owned ping copy). */
 SASBP_API size_t sas_bp_workspace_bytes(sas_bp_t h);
 
@@ -207,6 +215,44 @@ SASBP_API sas_status sas_rangecompress(const float* raw, int32_t P, int32_t E, i
 SASBP_API sas_status sas_rangecompress_device(const void* raw_dev, int32_t P, int32_t E, int32_t Ns,
                                     const void* replica_dev, int32_t Nr, void* out_dev,
                                     void* cuda_stream);
+
+/* Band-limited xU upsampling by the 8-tap windowed sinc (SPEC S:396
+ * "8-tap windowed-sinc on the upsampled (x4) compressed series"; reading R19):
+ *   out[ch][U n + r] = sum_{m=-3}^{4} in[ch][n + m] L(r/U - m),  L(s) = sinc(s) sinc(s/4), |s| < 4,
+ * in zero outside 0..Ns-1, ch = 0..nch-1, n = 0..Ns-1, r = 0..U-1.  The output is the same record
+ * at rate U fs (same t0): feed it to sas_bp_create(..., U * fs, ...) for linear TDBP on the
+ * upsampled series.  in: complex64 [nch][Ns]; out: complex64 [nch][U Ns] (caller-owned, must not
+ * overlap in).  Host buffers; runs on the current device.
+ * Errors: SAS_E_INVALID for nch|Ns < 1, U not in 1..16, NULL pointers or size overflow;
+ * SAS_E_NOMEM; SAS_E_CUDA. */
+SASBP_API sas_status sas_upsample(const float* in, int32_t nch, int32_t Ns, int32_t U, float* out);
+
+/* Device-pointer variant of sas_upsample, asynchronous on cuda_stream (8-byte aligned). */
+SASBP_API sas_status sas_upsample_device(const void* in_dev, int32_t nch, int32_t Ns, int32_t U, void* out_dev,
+                                         void* cuda_stream);
+
+/* Basebanding of real passband channels ("range compression +
+ * basebanding"; reading R20): mix down by the carrier measured from each ping's transmit
+ * instant (R3, R4), low-pass with the caller's FIR and keep every D-th sample:
+ *   z[n] = x[n] exp(-j 2 pi fc (t0_p + n / fs_in)),             x zero outside 0..Nin-1
+ *   out[ch][m] = sum_{k=0}^{Nh-1} h[k] z[m D + (Nh-1)/2 - k],    m = 0..Nout-1
+ * channel ch = p E + e.  Output sample m is at t0_p + m D / fs_in: rate fs_in / D, same t0.
+ *   x   float [P][E][Nin] real passband samples at fs_in
+ *   t0  fp64 [P] seconds after transmit of sample 0, or NULL (= 0); host, copied
+ *   h   float [Nh] FIR taps, Nh odd, 1..1023; host, copied (scale by 2 to keep the passband
+ *       amplitude: a cos(2 pi f t + th) -> a exp(j ...) when sum(h) = 2)
+ *   out complex64 [P][E][Nout]
+ * Errors: SAS_E_INVALID for P|E|Nin|Nout|D < 1, even or out-of-range Nh, fs_in or fc not finite
+ * and > 0, non-finite t0, NULL pointers; SAS_E_NOMEM; SAS_E_CUDA. */
+SASBP_API sas_status sas_baseband(const float* x, int32_t P, int32_t E, int32_t Nin, double fs_in, double fc,
+                                  const double* t0, const float* h, int32_t Nh, int32_t D, int32_t Nout,
+                                  float* out);
+
+/* Device-pointer variant of sas_baseband (x_dev, out_dev on the device; t0 and h stay HOST
+ * arrays, copied), asynchronous on cuda_stream. */
+SASBP_API sas_status sas_baseband_device(const void* x_dev, int32_t P, int32_t E, int32_t Nin, double fs_in,
+                                         double fc, const double* t0, const float* h, int32_t Nh, int32_t D,
+                                         int32_t Nout, void* out_dev, void* cuda_stream);
 
 /* Thread-local message describing the last failure on this thread ("" if none). */
 SASBP_API const char* sas_last_error(void);

@@ -27,15 +27,27 @@ def _stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False, out: str = None, defines=()) -> str:
-    """Build libsasbp.so (or an A/B variant at `out` with extra -D defines)."""
+    """Build libsasbp.so (or an A/B variant at `out` with extra -D defines).  Every .cu is compiled
+    to an object in parallel (the K2 instantiation families live in separate translation units),
+    then linked."""
     target = out or LIB
     if out is None and not force and not _stale():
         return LIB
-    tmp = target + f".tmp{os.getpid()}"
-    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
-           "-Xcompiler", "-fvisibility=hidden", "-cudart", "static", "-I", os.path.join(ROOT, "include"),
-           "-Xptxas", "-v" if verbose else "-O3", *[f"-D{d}" for d in defines], "-o", tmp, *sources()]
-    subprocess.check_call(cmd)
+    import concurrent.futures
+    import tempfile
+    common = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+              "-Xcompiler", "-fvisibility=hidden", "-I", os.path.join(ROOT, "include"),
+              "-Xptxas", "-v" if verbose else "-O3", *[f"-D{d}" for d in defines]]
+    with tempfile.TemporaryDirectory(prefix="sasbp_build_") as tmpd:
+        def one(src):
+            obj = os.path.join(tmpd, os.path.basename(src) + ".o")
+            subprocess.check_call(common + ["-c", "-o", obj, src])
+            return obj
+        srcs = sources()
+        with concurrent.futures.ThreadPoolExecutor(max_workers=min(len(srcs), os.cpu_count() or 4)) as ex:
+            objs = list(ex.map(one, srcs))
+        tmp = target + f".tmp{os.getpid()}"
+        subprocess.check_call([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs])
     os.replace(tmp, target)
     return target
 

@@ -1,0 +1,314 @@
+// conditioning.cu -- the input-conditioning kernels around K1/K2 (SURVEY §8(a) row a1 option and
+// §8(f) NEXT-4):
+//
+//  * K1b sas_upsample (reading R19): band-limited xU upsampling by the 8-tap windowed sinc
+//      out[U n + r] = sum_{m=-3}^{4} in[n + m] L(r/U - m),  L(s) = sinc(s) sinc(s/4), |s| < 4
+//    ("8-tap windowed-sinc on the upsampled (x4) compressed series"; the paper is
+//    silent on interpolation).  HBM-bound: 8 B read + 8U B written per input sample.  One CTA
+//    stages a segment of 1024 input samples (+7 halo, zero-extended, R2) in shared memory; each
+//    thread owns one input position, keeps its 8 taps in registers and writes its U outputs as
+//    one contiguous 8U-byte run (a warp stores 256U contiguous bytes).  The U x 8 weights are
+//    evaluated on the host in double precision from the definition and passed by value.
+//
+//  * K0 sas_baseband (reading R20): real passband -> complex baseband,
+//      z[n] = x[n] exp(-j 2 pi fc (t0_p + n / fs_in)),  out[m] = sum_k h[k] z[m D + (Nh-1)/2 - k]
+//    One CTA per (channel, run of MO outputs): the input span is mixed once into shared memory,
+//    stored POLYPHASE (z_q[i] = z[i D + q]) so that, for a fixed tap, consecutive threads
+//    (consecutive outputs) read consecutive words -- no bank conflicts for any decimation D.  The
+//    carrier phase is reduced in fp64 (fc t0_p mod 1 on the host, n (fc / fs_in) mod 1 per
+//    sample), so the ~1e4-cycle carrier phase never passes through fp32.
+#include "sasbp.h"
+
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <vector>
+#include <cuda_runtime.h>
+
+extern "C" void sasbp_set_error(const char* msg);  // sasbp.cu: the thread-local sas_last_error buffer
+
+namespace {
+
+sas_status cond_fail(sas_status st, const char* what, cudaError_t e = cudaSuccess) {
+  char buf[256];
+  if (e != cudaSuccess) snprintf(buf, sizeof(buf), "%s: %s", what, cudaGetErrorString(e));
+  else snprintf(buf, sizeof(buf), "%s", what);
+  sasbp_set_error(buf);
+  return st;
+}
+
+// ---------------------------------------------------------------- K1b: 8-tap xU upsampling
+
+constexpr int kUpThreads = 256;
+constexpr int kUpSeg = 1024;          // input samples per CTA
+constexpr int kUpMax = 16;
+
+struct UpWeights { float w[kUpMax][8]; };   // w[r][m + 3] = L(r/U - m)
+
+__device__ __forceinline__ void st_cs_v4(float2* p, float2 a, float2 b) {
+  // streaming store: the upsampled series is written once and read later by another kernel
+  asm volatile("st.global.cs.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y)
+               : "memory");
+}
+
+template <int UT>   // UT = U at compile time (1, 2, 4, 8), 0 = runtime U
+__global__ void __launch_bounds__(kUpThreads) upsample_kernel(const float2* __restrict__ in, int Ns, int U_rt,
+                                                              long long segs, const __grid_constant__ UpWeights W,
+                                                              float2* __restrict__ out) {
+  __shared__ float2 sx[kUpSeg + 8];
+  const int U = UT ? UT : U_rt;
+  const long long b = blockIdx.x;
+  const long long ch = b / segs;
+  const int n0 = (int)(b - ch * segs) * kUpSeg;
+  const float2* x = in + ch * (long long)Ns;
+  for (int i = threadIdx.x; i < kUpSeg + 7; i += kUpThreads) {   // x[n0 - 3 .. n0 + kUpSeg + 3]
+    const int n = n0 - 3 + i;
+    sx[i] = (n >= 0 && n < Ns) ? __ldcs(x + n) : make_float2(0.f, 0.f);
+  }
+  __syncthreads();
+  float2* y = out + ch * (long long)Ns * U;
+  for (int t = threadIdx.x; t < kUpSeg; t += kUpThreads) {
+    const int n = n0 + t;
+    if (n >= Ns) break;
+    float2 tap[8];
+#pragma unroll
+    for (int m = 0; m < 8; ++m) tap[m] = sx[t + m];
+    float2* yo = y + (long long)n * U;
+    if (UT >= 2) {
+#pragma unroll
+      for (int r = 0; r < (UT ? UT : 2); r += 2) {
+        float2 a = make_float2(0.f, 0.f), c = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+          a.x = fmaf(W.w[r][m], tap[m].x, a.x); a.y = fmaf(W.w[r][m], tap[m].y, a.y);
+          c.x = fmaf(W.w[r + 1][m], tap[m].x, c.x); c.y = fmaf(W.w[r + 1][m], tap[m].y, c.y);
+        }
+        st_cs_v4(yo + r, a, c);
+      }
+    } else {
+      for (int r = 0; r < U; ++r) {
+        float2 a = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int m = 0; m < 8; ++m) { a.x = fmaf(W.w[r][m], tap[m].x, a.x); a.y = fmaf(W.w[r][m], tap[m].y, a.y); }
+        __stcs(yo + r, a);
+      }
+    }
+  }
+}
+
+// L(s) = sinc(s) sinc(s/4) for |s| < 4 (R19), in double precision
+double lanczos4_host(double s) {
+  const double pi = 3.141592653589793238462643383279;
+  if (s == 0.0) return 1.0;
+  if (std::fabs(s) >= 4.0) return 0.0;
+  const double a = pi * s, b = pi * s * 0.25;
+  return (std::sin(a) / a) * (std::sin(b) / b);
+}
+
+// ---------------------------------------------------------------- K0: basebanding
+
+constexpr int kBbThreads = 256;
+constexpr int kBbSmem = 48 * 1024;    // bytes of mixed input per CTA
+constexpr int kBbMaxNh = 1023;
+
+__global__ void __launch_bounds__(kBbThreads) baseband_kernel(const float* __restrict__ x, int E, int Nin, double kr,
+                                                              const double* __restrict__ base, const float* __restrict__ h,
+                                                              int Nh, int D, int Nout, int MO, long long runs,
+                                                              float2* __restrict__ out) {
+  extern __shared__ __align__(16) unsigned char bb_smem[];
+  float* sh = reinterpret_cast<float*>(bb_smem);                            // taps [Nh] (padded to 4)
+  float2* sz = reinterpret_cast<float2*>(bb_smem + ((Nh + 3) & ~3) * 4);     // polyphase z [D][Lq]
+  const long long b = blockIdx.x;
+  const long long ch = b / runs;
+  const int m0 = (int)(b - ch * runs) * MO;
+  const int half = (Nh - 1) >> 1;
+  // span of input indices: n = m D + half - k, m in [m0, m0 + MO), k in [0, Nh)
+  const int nlo = m0 * D + half - (Nh - 1);
+  const int span = (MO - 1) * D + Nh;
+  const int Lq = (span + D - 1) / D;          // samples per phase
+  const float* xc = x + ch * (long long)Nin;
+  const double bp = base[ch / E];             // fc t0_p mod 1 (cycles)
+  for (int k = threadIdx.x; k < Nh; k += kBbThreads) sh[k] = h[k];
+  for (int i = threadIdx.x; i < span; i += kBbThreads) {
+    const int n = nlo + i;
+    float2 z = make_float2(0.f, 0.f);
+    if (n >= 0 && n < Nin) {
+      const float v = __ldcs(xc + n);
+      double ph = fma((double)n, kr, bp);     // fc (t0_p + n / fs_in) mod 1, fp64
+      ph -= rint(ph);                         // [-1/2, 1/2]
+      float sn, cs;
+      __sincosf(-6.283185307179586f * (float)ph, &sn, &cs);
+      z = make_float2(v * cs, v * sn);
+    }
+    const int q = i % D;                      // polyphase: z_q[i / D]
+    sz[q * Lq + i / D] = z;
+  }
+  __syncthreads();
+  float2* yo = out + ch * (long long)Nout;
+  for (int t = threadIdx.x; t < MO; t += kBbThreads) {
+    const int m = m0 + t;
+    if (m >= Nout) break;
+    // tap k reads local input i = t D + j, j = Nh - 1 - k; with j = a D + q that is z_q[t + a]
+    float ar = 0.f, ai = 0.f;
+    for (int q = 0; q < D && q < Nh; ++q) {
+      const float2* zq = sz + q * Lq + t;
+#pragma unroll 4
+      for (int j = q, a = 0; j < Nh; j += D, ++a) {
+        const float2 z = zq[a];
+        const float hk = sh[Nh - 1 - j];
+        ar = fmaf(hk, z.x, ar);
+        ai = fmaf(hk, z.y, ai);
+      }
+    }
+    __stcs(yo + m, make_float2(ar, ai));
+  }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- C ABI
+
+extern "C" sas_status sas_upsample_device(const void* in_dev, int32_t nch, int32_t Ns, int32_t U, void* out_dev,
+                                          void* cuda_stream) {
+  sasbp_set_error("");
+  if (nch < 1 || Ns < 1) return cond_fail(SAS_E_INVALID, "nch and Ns must be >= 1");
+  if (U < 1 || U > kUpMax) return cond_fail(SAS_E_INVALID, "U must be in 1..16");
+  if (!in_dev || !out_dev) return cond_fail(SAS_E_INVALID, "NULL pointer");
+  if ((((uintptr_t)in_dev) & 7) || (((uintptr_t)out_dev) & 15))
+    return cond_fail(SAS_E_INVALID, "in_dev must be 8-byte and out_dev 16-byte aligned");
+  if ((long double)nch * Ns * U > 4.0e15L) return cond_fail(SAS_E_INVALID, "nch*Ns*U too large");
+  UpWeights W{};
+  for (int r = 0; r < U; ++r)
+    for (int m = -3; m <= 4; ++m) W.w[r][m + 3] = (float)lanczos4_host((double)r / U - m);
+  const long long segs = (Ns + kUpSeg - 1) / kUpSeg;
+  const long long blocks = segs * nch;
+  if (blocks > 2147483647LL) return cond_fail(SAS_E_INVALID, "too many channels for one launch");
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  const float2* in = (const float2*)in_dev;
+  float2* out = (float2*)out_dev;
+  switch (U) {
+    case 2: upsample_kernel<2><<<(unsigned)blocks, kUpThreads, 0, st>>>(in, Ns, U, segs, W, out); break;
+    case 4: upsample_kernel<4><<<(unsigned)blocks, kUpThreads, 0, st>>>(in, Ns, U, segs, W, out); break;
+    case 8: upsample_kernel<8><<<(unsigned)blocks, kUpThreads, 0, st>>>(in, Ns, U, segs, W, out); break;
+    default: upsample_kernel<0><<<(unsigned)blocks, kUpThreads, 0, st>>>(in, Ns, U, segs, W, out); break;
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cond_fail(SAS_E_CUDA, "upsample_kernel launch", e);
+  return SAS_OK;
+}
+
+extern "C" sas_status sas_upsample(const float* in, int32_t nch, int32_t Ns, int32_t U, float* out) {
+  sasbp_set_error("");
+  if (!in || !out) return cond_fail(SAS_E_INVALID, "NULL pointer");
+  if (nch < 1 || Ns < 1 || U < 1 || U > kUpMax) return cond_fail(SAS_E_INVALID, "nch, Ns >= 1 and U in 1..16 required");
+  const size_t n = (size_t)nch * Ns;
+  cudaStream_t st = nullptr;
+  cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  if (e != cudaSuccess) return cond_fail(SAS_E_CUDA, "cudaStreamCreate", e);
+  float2 *din = nullptr, *dout = nullptr;
+  sas_status rs = SAS_OK;
+  if (cudaMalloc(&din, n * sizeof(float2)) != cudaSuccess || cudaMalloc(&dout, n * U * sizeof(float2)) != cudaSuccess)
+    rs = cond_fail(SAS_E_NOMEM, "cudaMalloc failed in sas_upsample");
+  if (rs == SAS_OK && (e = cudaMemcpyAsync(din, in, n * sizeof(float2), cudaMemcpyHostToDevice, st)) != cudaSuccess)
+    rs = cond_fail(SAS_E_CUDA, "H2D copy", e);
+  if (rs == SAS_OK) rs = sas_upsample_device(din, nch, Ns, U, dout, st);
+  if (rs == SAS_OK) {
+    e = cudaMemcpyAsync(out, dout, n * U * sizeof(float2), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) rs = cond_fail(SAS_E_CUDA, "D2H copy", e);
+  }
+  cudaStreamSynchronize(st);
+  cudaFree(din);
+  cudaFree(dout);
+  cudaStreamDestroy(st);
+  return rs;
+}
+
+extern "C" sas_status sas_baseband_device(const void* x_dev, int32_t P, int32_t E, int32_t Nin, double fs_in,
+                                          double fc, const double* t0, const float* h, int32_t Nh, int32_t D,
+                                          int32_t Nout, void* out_dev, void* cuda_stream) {
+  sasbp_set_error("");
+  if (P < 1 || E < 1 || Nin < 1 || Nout < 1 || D < 1) return cond_fail(SAS_E_INVALID, "P, E, Nin, Nout, D must be >= 1");
+  if (Nh < 1 || Nh > kBbMaxNh || (Nh % 2) == 0) return cond_fail(SAS_E_INVALID, "Nh must be odd and in 1..1023");
+  if (!(std::isfinite(fs_in) && fs_in > 0) || !(std::isfinite(fc) && fc > 0))
+    return cond_fail(SAS_E_INVALID, "fs_in and fc must be finite and > 0");
+  if (!x_dev || !h || !out_dev) return cond_fail(SAS_E_INVALID, "NULL pointer");
+  if ((((uintptr_t)x_dev) & 3) || (((uintptr_t)out_dev) & 7)) return cond_fail(SAS_E_INVALID, "misaligned pointer");
+  if ((long double)P * E * ((long double)Nin + Nout) > 4.0e15L) return cond_fail(SAS_E_INVALID, "sizes too large");
+  std::vector<double> base(P);
+  for (int32_t p = 0; p < P; ++p) {
+    const double tp = t0 ? t0[p] : 0.0;
+    if (!std::isfinite(tp)) return cond_fail(SAS_E_INVALID, "non-finite t0");
+    const double v = fc * tp;                 // carrier cycles at sample 0, reduced mod 1 in fp64
+    base[p] = v - std::floor(v);
+  }
+  for (int32_t k = 0; k < Nh; ++k)
+    if (!std::isfinite(h[k])) return cond_fail(SAS_E_INVALID, "non-finite FIR tap");
+  double kr = fc / fs_in;                     // cycles per input sample, mod 1
+  kr -= std::floor(kr);
+  // outputs per CTA: the mixed span (MO - 1) D + Nh fits kBbSmem bytes next to the taps
+  const int tap_bytes = ((Nh + 3) & ~3) * 4;
+  const long long cap = (kBbSmem - tap_bytes) / 8;                      // complex samples
+  long long MO = (cap - Nh) / D + 1;
+  if (MO < 1) return cond_fail(SAS_E_UNSUPPORTED, "decimation too large for one CTA's staging buffer");
+  MO = std::min<long long>(MO, 2048);
+  MO = std::min<long long>(MO, Nout);
+  const long long span = (MO - 1) * D + Nh;
+  const long long Lq = (span + D - 1) / D;
+  const size_t smem = (size_t)tap_bytes + (size_t)D * Lq * 8;
+  const long long runs = (Nout + MO - 1) / MO;
+  const long long blocks = runs * (long long)P * E;
+  if (blocks > 2147483647LL) return cond_fail(SAS_E_INVALID, "too many channels for one launch");
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  double* dbase = nullptr;
+  float* dh = nullptr;
+  cudaError_t e = cudaMallocAsync(&dbase, P * sizeof(double), st);
+  if (e == cudaSuccess) e = cudaMallocAsync(&dh, Nh * sizeof(float), st);
+  if (e != cudaSuccess) {
+    if (dbase) cudaFreeAsync(dbase, st);
+    return cond_fail(SAS_E_NOMEM, "cudaMallocAsync(baseband tables)", e);
+  }
+  e = cudaMemcpyAsync(dbase, base.data(), P * sizeof(double), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dh, h, Nh * sizeof(float), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess && smem > 48 * 1024)
+    e = cudaFuncSetAttribute(baseband_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess) {
+    baseband_kernel<<<(unsigned)blocks, kBbThreads, smem, st>>>((const float*)x_dev, E, Nin, kr, dbase, dh, Nh, D, Nout,
+                                                                (int)MO, runs, (float2*)out_dev);
+    e = cudaGetLastError();
+  }
+  // (pageable-source cudaMemcpyAsync has consumed the host vectors when it returns)
+  cudaFreeAsync(dbase, st);
+  cudaFreeAsync(dh, st);
+  if (e != cudaSuccess) return cond_fail(SAS_E_CUDA, "baseband_kernel", e);
+  return SAS_OK;
+}
+
+extern "C" sas_status sas_baseband(const float* x, int32_t P, int32_t E, int32_t Nin, double fs_in, double fc,
+                                   const double* t0, const float* h, int32_t Nh, int32_t D, int32_t Nout, float* out) {
+  sasbp_set_error("");
+  if (!x || !h || !out) return cond_fail(SAS_E_INVALID, "NULL pointer");
+  if (P < 1 || E < 1 || Nin < 1 || Nout < 1) return cond_fail(SAS_E_INVALID, "P, E, Nin, Nout must be >= 1");
+  const size_t nin = (size_t)P * E * Nin, nout = (size_t)P * E * Nout;
+  cudaStream_t st = nullptr;
+  cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  if (e != cudaSuccess) return cond_fail(SAS_E_CUDA, "cudaStreamCreate", e);
+  float* dx = nullptr;
+  float2* dout = nullptr;
+  sas_status rs = SAS_OK;
+  if (cudaMalloc(&dx, nin * sizeof(float)) != cudaSuccess || cudaMalloc(&dout, nout * sizeof(float2)) != cudaSuccess)
+    rs = cond_fail(SAS_E_NOMEM, "cudaMalloc failed in sas_baseband");
+  if (rs == SAS_OK && (e = cudaMemcpyAsync(dx, x, nin * sizeof(float), cudaMemcpyHostToDevice, st)) != cudaSuccess)
+    rs = cond_fail(SAS_E_CUDA, "H2D copy", e);
+  if (rs == SAS_OK) rs = sas_baseband_device(dx, P, E, Nin, fs_in, fc, t0, h, Nh, D, Nout, dout, st);
+  if (rs == SAS_OK) {
+    e = cudaMemcpyAsync(out, dout, nout * sizeof(float2), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) rs = cond_fail(SAS_E_CUDA, "D2H copy", e);
+  }
+  cudaStreamSynchronize(st);
+  cudaFree(dx);
+  cudaFree(dout);
+  cudaStreamDestroy(st);
+  return rs;
+}

@@ -1,0 +1,10 @@
+// k2_2d.cu -- one K2 instantiation family (see k2_launch.cuh).
+#include <type_traits>
+
+#include "k2_launch.cuh"
+
+namespace sasbp {
+cudaError_t k2_launch_2d(const TdbpParams& prm, const TmaDesc& tmap, const K2Launch& L) {
+  return launch_family<SASBP_T2D, false, false, false>(prm, tmap, L);
+}
+}  // namespace sasbp

@@ -1,0 +1,118 @@
+// k2_launch.cuh -- host-side launch templates of K2 (TDBP) and K3 (term counter).
+//
+// The kernel instantiations are spread over several translation units (k2_*.cu), one per
+// (tile variant, gating, weighting) family, so nvcc builds them in parallel; sasbp.cu only sees
+// the plain entry points declared at the bottom.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "tdbp_kernel.cuh"
+
+#ifndef SASBP_ROTATE
+#define SASBP_ROTATE 0
+#endif
+
+namespace sasbp {
+
+// tile variants: 2D z-level plane, 2D with z components in the steps, 3D volume
+enum K2Variant { kV2D = 0, kV2D_DZ = 1, kV3D = 2 };
+
+struct K2Launch {
+  bool tma;          // TMA row staging (else cp.async)
+  int mode;          // receive-leg mode (kSeries3 / kSeries4 / kExact); prm.refract selects kRefract
+  bool count;        // K3 instead of K2
+  cudaStream_t st;
+  int* occ;          // out: resident CTAs per SM of the launched kernel
+};
+
+template <typename Kern>
+cudaError_t launch_k(Kern kern, int threads, const TdbpParams& prm_in, const TmaDesc& tmap, size_t smem,
+                     const K2Launch& L) {
+  const unsigned blocks = (unsigned)prm_in.tiles_x * prm_in.tiles_y * prm_in.tiles_z;
+  if (smem > 0) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  TdbpParams prm = prm_in;
+  int per_sm = 0, dev = 0, sms = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem) == cudaSuccess &&
+      cudaGetDevice(&dev) == cudaSuccess &&
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess)
+    prm.resident = per_sm * sms;
+  if (L.occ) *L.occ = per_sm;
+#if !SASBP_ROTATE
+  prm.resident = 0;
+#endif
+  kern<<<blocks, threads, smem, L.st>>>(prm, tmap);
+  return cudaGetLastError();
+}
+
+// one (tile shape, gating, weighting) family: TMA / cp.async x receive-leg modes x motion
+template <int KX, int KY, int KZ, int WY, int WZ, bool DZ, bool GATE, bool WEIGHT>
+cudaError_t launch_family(const TdbpParams& prm, const TmaDesc& tmap, const K2Launch& L) {
+  const size_t smem = k2_smem_bytes(prm.W);
+  const int nt = 32 * WY * WZ;
+  if (L.count) {
+    if (GATE || WEIGHT) return cudaErrorInvalidValue;   // counting lives in the dense family
+    const unsigned blocks = (unsigned)prm.tiles_x * prm.tiles_y * prm.tiles_z;
+    count_kernel<KX, KY, KZ, WY, WZ><<<blocks, nt, 0, L.st>>>(prm);
+    return cudaGetLastError();
+  }
+  if (WEIGHT) {   // spreading weight (R18): stop-and-hop, straight rays only (checked on the host)
+    if (prm.vel || prm.refract) return cudaErrorNotSupported;
+    auto go = [&](auto kern) { return launch_k(kern, nt, prm, tmap, smem, L); };
+    if (L.tma) {
+      switch (L.mode) {
+        case kSeries3: return go(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kSeries3, true, GATE, false, false, WEIGHT>);
+        case kSeries4: return go(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kSeries4, true, GATE, false, false, WEIGHT>);
+        default: return go(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kExact, true, GATE, false, false, WEIGHT>);
+      }
+    }
+    switch (L.mode) {
+      case kSeries3: return go(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kSeries3, false, GATE, false, false, WEIGHT>);
+      case kSeries4: return go(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kSeries4, false, GATE, false, false, WEIGHT>);
+      default: return go(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kExact, false, GATE, false, false, WEIGHT>);
+    }
+  }
+  auto pick = [&](auto tma_tag, auto motion_tag) -> cudaError_t {
+    constexpr bool T = decltype(tma_tag)::value;
+    constexpr bool M = decltype(motion_tag)::value;
+    if (prm.refract) {
+      if (M) return cudaErrorNotSupported;   // rejected on the host before launch
+      return launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kRefract, T, GATE, false>, nt, prm, tmap, smem, L);
+    }
+    switch (L.mode) {
+      case kSeries3: return launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kSeries3, T, GATE, M>, nt, prm, tmap, smem, L);
+      case kSeries4: return launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kSeries4, T, GATE, M>, nt, prm, tmap, smem, L);
+      default: return launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kExact, T, GATE, M>, nt, prm, tmap, smem, L);
+    }
+  };
+  using TT = std::true_type;
+  using FF = std::false_type;
+  if (L.tma) return prm.vel ? pick(TT{}, TT{}) : pick(TT{}, FF{});
+  return prm.vel ? pick(FF{}, TT{}) : pick(FF{}, FF{});
+}
+
+// entry points, one per translation unit (k2_*.cu)
+cudaError_t k2_launch_2d(const TdbpParams& prm, const TmaDesc& tmap, const K2Launch& L);        // dense + count
+cudaError_t k2_launch_2d_gate(const TdbpParams& prm, const TmaDesc& tmap, const K2Launch& L);
+cudaError_t k2_launch_2ddz(const TdbpParams& prm, const TmaDesc& tmap, const K2Launch& L);
+cudaError_t k2_launch_2ddz_gate(const TdbpParams& prm, const TmaDesc& tmap, const K2Launch& L);
+cudaError_t k2_launch_3d(const TdbpParams& prm, const TmaDesc& tmap, const K2Launch& L);
+cudaError_t k2_launch_3d_gate(const TdbpParams& prm, const TmaDesc& tmap, const K2Launch& L);
+cudaError_t k2_launch_2d_w(const TdbpParams& prm, const TmaDesc& tmap, const K2Launch& L);     // weighted (R18)
+cudaError_t k2_launch_2ddz_w(const TdbpParams& prm, const TmaDesc& tmap, const K2Launch& L);
+cudaError_t k2_launch_3d_w(const TdbpParams& prm, const TmaDesc& tmap, const K2Launch& L);
+
+}  // namespace sasbp
+
+// tile shapes of the variants (KX, KY, KZ, WY, WZ): 2D = 32 x 8*WY pixels, 3D = 16 x 8 x 8 voxels
+#ifndef SASBP_WY2D
+#define SASBP_WY2D 4
+#endif
+#if SASBP_K4
+#define SASBP_T2D 4, 1, 1, 8, 1
+#else
+#define SASBP_T2D 4, 2, 1, SASBP_WY2D, 1
+#endif
+#define SASBP_T3D 2, 2, 2, 1, 4

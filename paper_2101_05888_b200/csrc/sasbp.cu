@@ -18,17 +18,8 @@
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
-#include "tdbp_kernel.cuh"
+#include "k2_launch.cuh"
 
-#ifndef SASBP_ROTATE
-#define SASBP_ROTATE 0
-#endif
-#ifndef SASBP_K4
-#define SASBP_K4 0
-#endif
-#ifndef SASBP_AXIS
-#define SASBP_AXIS 0
-#endif
 
 namespace {
 
@@ -46,7 +37,8 @@ sas_status fail(sas_status st, const char* fmt, ...) {
 bool finite3(const double* v) { return std::isfinite(v[0]) && std::isfinite(v[1]) && std::isfinite(v[2]); }
 double norm3(const double* v) { return std::sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]); }
 
-enum Variant { V2D = 0, V2D_DZ = 1, V3D = 2 };
+using Variant = sasbp::K2Variant;
+constexpr Variant V2D = sasbp::kV2D, V2D_DZ = sasbp::kV2D_DZ, V3D = sasbp::kV3D;
 
 }  // namespace
 
@@ -88,6 +80,8 @@ struct sas_bp_s {
   // sediment-water interface (sas_bp_set_medium; NEXT-3)
   int refract = 0;
   double zb = 0, c2 = 0;
+  // spreading weight R_tx R_rx (sas_bp_set_weighting; NEXT-4, R18)
+  int weight = 0;
   double max_sensor_z = -INFINITY;   // of the current ping set
   bool has_pings = false;
   bool broken = false;
@@ -133,67 +127,6 @@ double dist_to_box(const double* p, const double lo[3], const double hi[3]) {
     s += d * d;
   }
   return std::sqrt(s);
-}
-
-template <typename Kern>
-cudaError_t launch_k(Kern kern, int threads, const sasbp::TdbpParams& prm_in, const sasbp::TmaDesc& tmap,
-                     size_t smem, cudaStream_t st) {
-  const unsigned blocks = (unsigned)prm_in.tiles_x * prm_in.tiles_y * prm_in.tiles_z;
-  if (smem > 0) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-  }
-  sasbp::TdbpParams prm = prm_in;
-  int per_sm = 0, dev = 0, sms = 0;
-  g_last_occ = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem) == cudaSuccess &&
-      cudaGetDevice(&dev) == cudaSuccess &&
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess)
-    prm.resident = per_sm * sms;
-  g_last_occ = per_sm;
-#if !SASBP_ROTATE
-  prm.resident = 0;
-#endif
-  kern<<<blocks, threads, smem, st>>>(prm, tmap);
-  return cudaGetLastError();
-}
-
-template <int KX, int KY, int KZ, int WY, int WZ, bool DZ, bool TMA, bool GATE, bool MOTION>
-cudaError_t launch_gate(const sasbp::TdbpParams& prm, const sasbp::TmaDesc& tmap, int mode, cudaStream_t st) {
-  using namespace sasbp;
-  const size_t smem = smem_bytes(prm.W);
-  const int nt = 32 * WY * WZ;
-  if (prm.refract) {
-    if (MOTION) return cudaErrorNotSupported;   // rejected on the host before launch
-    return launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kRefract, TMA, GATE, false>, nt, prm, tmap, smem, st);
-  }
-  switch (mode) {
-    case kSeries3: return launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kSeries3, TMA, GATE, MOTION>, nt, prm, tmap, smem, st);
-    case kSeries4: return launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kSeries4, TMA, GATE, MOTION>, nt, prm, tmap, smem, st);
-    default: return launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kExact, TMA, GATE, MOTION>, nt, prm, tmap, smem, st);
-  }
-}
-
-template <int KX, int KY, int KZ, int WY, int WZ, bool DZ, bool TMA>
-cudaError_t launch_mode(const sasbp::TdbpParams& prm, const sasbp::TmaDesc& tmap, int mode, cudaStream_t st) {
-  if (prm.vel)
-    return prm.gate ? launch_gate<KX, KY, KZ, WY, WZ, DZ, TMA, true, true>(prm, tmap, mode, st)
-                    : launch_gate<KX, KY, KZ, WY, WZ, DZ, TMA, false, true>(prm, tmap, mode, st);
-  return prm.gate ? launch_gate<KX, KY, KZ, WY, WZ, DZ, TMA, true, false>(prm, tmap, mode, st)
-                  : launch_gate<KX, KY, KZ, WY, WZ, DZ, TMA, false, false>(prm, tmap, mode, st);
-}
-
-template <int KX, int KY, int KZ, int WY, int WZ, bool DZ>
-cudaError_t launch_variant(const sasbp::TdbpParams& prm, const sasbp::TmaDesc& tmap, bool tma, int mode, bool count,
-                           cudaStream_t st) {
-  using namespace sasbp;
-  if (count) {
-    const unsigned blocks = (unsigned)prm.tiles_x * prm.tiles_y * prm.tiles_z;
-    count_kernel<KX, KY, KZ, WY, WZ><<<blocks, 32 * WY * WZ, 0, st>>>(prm);
-    return cudaGetLastError();
-  }
-  return tma ? launch_mode<KX, KY, KZ, WY, WZ, DZ, true>(prm, tmap, mode, st)
-             : launch_mode<KX, KY, KZ, WY, WZ, DZ, false>(prm, tmap, mode, st);
 }
 
 // Encode the TMA descriptor for the echo array [P*E][Ns] of 8-byte samples, box = one window
@@ -259,15 +192,20 @@ cudaError_t launch_tdbp(sas_bp_t h, float2* image, unsigned long long* counter, 
     prm.hw = 2.0 * h->d_max * h->fs / std::min(h->c, h->c2);
     prm.W = (int)std::ceil(2.0 * prm.hw + 4.0) + 3;
   }
+  sasbp::K2Launch L{h->use_tma, h->mode, count, st, &g_last_occ};
+  g_last_occ = 0;
+  const bool g = prm.gate && !count;
+  if (h->weight && !count) {
+    switch (h->variant) {
+      case V2D: return sasbp::k2_launch_2d_w(prm, h->tmap, L);
+      case V2D_DZ: return sasbp::k2_launch_2ddz_w(prm, h->tmap, L);
+      default: return sasbp::k2_launch_3d_w(prm, h->tmap, L);
+    }
+  }
   switch (h->variant) {
-#if SASBP_K4
-    case V2D: return launch_variant<4, 1, 1, 8, 1, false>(prm, h->tmap, h->use_tma, h->mode, count, st);
-    case V2D_DZ: return launch_variant<4, 1, 1, 8, 1, true>(prm, h->tmap, h->use_tma, h->mode, count, st);
-#else
-    case V2D: return launch_variant<4, 2, 1, SASBP_WY2D, 1, false>(prm, h->tmap, h->use_tma, h->mode, count, st);
-    case V2D_DZ: return launch_variant<4, 2, 1, SASBP_WY2D, 1, true>(prm, h->tmap, h->use_tma, h->mode, count, st);
-#endif
-    default: return launch_variant<2, 2, 2, 1, 4, true>(prm, h->tmap, h->use_tma, h->mode, count, st);
+    case V2D: return g ? sasbp::k2_launch_2d_gate(prm, h->tmap, L) : sasbp::k2_launch_2d(prm, h->tmap, L);
+    case V2D_DZ: return g ? sasbp::k2_launch_2ddz_gate(prm, h->tmap, L) : sasbp::k2_launch_2ddz(prm, h->tmap, L);
+    default: return g ? sasbp::k2_launch_3d_gate(prm, h->tmap, L) : sasbp::k2_launch_3d(prm, h->tmap, L);
   }
 }
 
@@ -491,6 +429,7 @@ sas_status sas_bp_form_device(sas_bp_t h, void* image_dev, void* cuda_stream, in
   if (h->vel && h->vel_P != h->P) return fail(SAS_E_STATE, "velocities were given for %d pings, the ping set has %d", h->vel_P, h->P);
   if (h->refract && h->vel) return fail(SAS_E_UNSUPPORTED, "refraction and receiver motion cannot be combined");
   if (h->refract && !(h->max_sensor_z < h->zb)) return fail(SAS_E_INVALID, "with an interface every sensor must be in the water (z < zb)");
+  if (h->weight && (h->vel || h->refract)) return fail(SAS_E_UNSUPPORTED, "the spreading weight is defined for stop-and-hop straight rays only");
   CK_H(h, cudaSetDevice(h->device));
   CK_H(h, launch_tdbp(h, (float2*)image_dev, h->counter, (flags & SAS_FORM_ACCUMULATE) ? 1 : 0, false,
                       (cudaStream_t)cuda_stream));
@@ -508,6 +447,7 @@ sas_status sas_bp_form(sas_bp_t h, float* image_out) {
   if (h->vel && h->vel_P != h->P) return fail(SAS_E_STATE, "velocities were given for %d pings, the ping set has %d", h->vel_P, h->P);
   if (h->refract && h->vel) return fail(SAS_E_UNSUPPORTED, "refraction and receiver motion cannot be combined");
   if (h->refract && !(h->max_sensor_z < h->zb)) return fail(SAS_E_INVALID, "with an interface every sensor must be in the water (z < zb)");
+  if (h->weight && (h->vel || h->refract)) return fail(SAS_E_UNSUPPORTED, "the spreading weight is defined for stop-and-hop straight rays only");
   CK_H(h, cudaSetDevice(h->device));
   CK_H(h, launch_tdbp(h, h->image, h->counter, 0, false, h->stream));
   h->ctas_per_sm = g_last_occ;
@@ -546,6 +486,7 @@ sas_status sas_bp_form_streamed(sas_bp_t h, const float* echoes, int32_t P, int3
   if (h->vel && h->vel_P != h->P) return fail(SAS_E_STATE, "velocities were given for %d pings, the ping set has %d", h->vel_P, h->P);
   if (h->refract && h->vel) return fail(SAS_E_UNSUPPORTED, "refraction and receiver motion cannot be combined");
   if (h->refract && !(h->max_sensor_z < h->zb)) return fail(SAS_E_INVALID, "with an interface every sensor must be in the water (z < zb)");
+  if (h->weight && (h->vel || h->refract)) return fail(SAS_E_UNSUPPORTED, "the spreading weight is defined for stop-and-hop straight rays only");
   const int nch = P * E;
   int nchunk = chunks > 0 ? chunks : 8;
   nchunk = std::max(1, std::min(nchunk, (nch + 63) / 64));   // >= 64 channels per chunk
@@ -578,6 +519,7 @@ sas_status sas_bp_count_terms(sas_bp_t h, uint64_t* dense, uint64_t* in_win) {
   if (h->vel && h->vel_P != h->P) return fail(SAS_E_STATE, "velocities were given for %d pings, the ping set has %d", h->vel_P, h->P);
   if (h->refract && h->vel) return fail(SAS_E_UNSUPPORTED, "refraction and receiver motion cannot be combined");
   if (h->refract && !(h->max_sensor_z < h->zb)) return fail(SAS_E_INVALID, "with an interface every sensor must be in the water (z < zb)");
+  if (h->weight && (h->vel || h->refract)) return fail(SAS_E_UNSUPPORTED, "the spreading weight is defined for stop-and-hop straight rays only");
   const uint64_t npx = (uint64_t)h->grid.nx * h->grid.ny * h->grid.nz;
   if (dense) *dense = npx * (uint64_t)h->P * (uint64_t)h->E;
   if (in_win) {
@@ -678,6 +620,14 @@ sas_status sas_bp_set_medium(sas_bp_t h, double zb, double c2) {
   const double Wn = std::ceil(2.0 * (2.0 * h->d_max * h->fs / std::min(h->c, c2)) + 4.0) + 3;
   if (smem_bytes((int)Wn) > 200 * 1024) return fail(SAS_E_UNSUPPORTED, "sediment speed too low for the tile window");
   h->refract = 1; h->zb = zb; h->c2 = c2;
+  return SAS_OK;
+}
+
+sas_status sas_bp_set_weighting(sas_bp_t h, int32_t spreading) {
+  g_err[0] = 0;
+  if (!h) return fail(SAS_E_INVALID, "handle is NULL");
+  if (spreading != 0 && spreading != 1) return fail(SAS_E_INVALID, "spreading must be 0 or 1");
+  h->weight = spreading;
   return SAS_OK;
 }
 

@@ -135,7 +135,7 @@ __device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
 // ---------------------------------------------------------------- refraction (NEXT-3, R17)
 // One-way Fermat time through the interface, fp64 (prologue reference): same definition as the
 // test-side reference, Newton from the straight-line crossing with bisection-style safeguards.
-__device__ double refr_time64(const double x[3], const double s[3], double zb, double c1, double c2) {
+__device__ inline double refr_time64(const double x[3], const double s[3], double zb, double c1, double c2) {
   const double h2 = x[2] - zb;
   const double dx = x[0] - s[0], dy = x[1] - s[1];
   if (h2 <= 0.0) return sqrt(dx * dx + dy * dy + (x[2] - s[2]) * (x[2] - s[2])) / c1;
@@ -193,7 +193,7 @@ __device__ __forceinline__ void ping_axes(const TdbpParams& prm, int p, double a
 // one sensor's cone: kGIn (every point inside), kGOut (every point outside) or kGEdge.  Exact
 // spherical bounds: the angle to the plane perpendicular to a ranges over alpha -/+ beta; the
 // elevation condition depends only on the projection onto span(b, c), a disk of radius d_max.
-__device__ int cone_class(const TdbpParams& prm, const double v[3], const double a[3], const double b[3]) {
+__device__ inline int cone_class(const TdbpParams& prm, const double v[3], const double a[3], const double b[3]) {
   const double rho = prm.d_max, eps = 1e-9;
   const double nv = sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
   if (!(nv > rho)) return kGEdge;
@@ -219,7 +219,7 @@ __device__ int cone_class(const TdbpParams& prm, const double v[3], const double
 
 // Per-point test, evaluated in fp64 in the definition's order of operations (no contraction),
 // so the decision is the plain fp64 one the test-side reference takes (R15).
-__device__ bool in_fov_px(const TdbpParams& prm, const double x[3], const double* s, const double a[3],
+__device__ inline bool in_fov_px(const TdbpParams& prm, const double x[3], const double* s, const double a[3],
                           const double b[3]) {
   const double v0 = __dsub_rn(x[0], s[0]), v1 = __dsub_rn(x[1], s[1]), v2 = __dsub_rn(x[2], s[2]);
   if (prm.az_on) {
@@ -435,8 +435,9 @@ struct __align__(64) TmaDesc { unsigned char bytes[128]; };
 
 // HAS_DZ = false means the grid is a z-level plane (step_x, step_y have no z component); then
 // both pixels of an x-pair share their y offset whenever step_x has no y component (AXIS).
+// WEIGHT = true multiplies every term by the spreading weight R_tx R_rx (NEXT-4, reading R18).
 template <int KX, int KY, int KZ, int WY, int WZ, bool HAS_DZ, int MODE, bool USE_TMA, bool GATE = false,
-          bool MOTION = false, bool AXIS = false>
+          bool MOTION = false, bool AXIS = false, bool WEIGHT = false>
 __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp_kernel(const TdbpParams prm,
                                                                           const __grid_constant__ TmaDesc tmap) {
   using TM = TileMap<KX, KY, KZ, WY, WZ>;
@@ -479,6 +480,8 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
 
   const float kph = (float)(6.283185307179586 * prm.k_r);
   const float kfs = (float)prm.k_s;
+  // spreading weight (R18): w = R_tx R_rx = (r_t k_s + dU_tx)(r_r k_s + dU_rx) / k_s^2, in samples
+  const float inv_ks2 = (float)(1.0 / (prm.k_s * prm.k_s));
   // refraction: interface height relative to the tile centre, slownesses in samples per metre
   const float zbr = MODE == kRefract ? (float)(prm.zb - ct[2]) : 0.f;
   const float k1r = (float)(prm.fs / prm.c), k2r = MODE == kRefract ? (float)(prm.fs / prm.c2) : 0.f;
@@ -691,12 +694,15 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
         }
         masked = (kc.gate & 3) == kGEdge || ((kc.gate >> 2) & 3) == kGEdge;   // warp-uniform
       }
+      const float rtk = WEIGHT ? kc.r_t * kfs : 0.f;               // r_t, r_r in samples
+      const float rrk = WEIGHT ? kc.r_r * kfs * inv_ks2 : 0.f;
 #pragma unroll
       for (int p = 0; p < NP; ++p) {
         float2 q = __ffma2_rn(f2(kc.uy2), AXIS ? f2(DYS[p]) : DY[p], DD[p]);
         q = __ffma2_rn(f2(kc.ux2), DX[p], q);
         if (HAS_DZ) q = __ffma2_rn(f2(kc.uz2), DZ[p], q);
         float2 U;
+        float2 wgt = f2(1.f);
         if (MODE == kRefract) {
           const float r0 = refr_time32(DX[p].x - kc.ux2, DY[p].x - kc.uy2, DZ[p].x - kc.uz2, zbr - kc.uz2,
                                        DZ[p].x - zbr, k1r, k2r);
@@ -707,7 +713,13 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
           const float2 r2 = __fadd2_rn(q, f2(kc.r2_r));
           const float den0 = fmaf(r2.x, rsqrt_approx(r2.x), kc.r_r);
           const float den1 = fmaf(r2.y, rsqrt_approx(r2.y), kc.r_r);
-          U = __ffma2_rn(__fmul2_rn(q, make_float2(rcp_approx(den0), rcp_approx(den1))), f2(kfs), BT[p]);
+          if (WEIGHT) {
+            const float2 dU = __fmul2_rn(__fmul2_rn(q, make_float2(rcp_approx(den0), rcp_approx(den1))), f2(kfs));
+            U = __fadd2_rn(dU, BT[p]);
+            wgt = __fmul2_rn(__fadd2_rn(BT[p], f2(rtk)), __ffma2_rn(dU, f2(inv_ks2), f2(rrk)));
+          } else {
+            U = __ffma2_rn(__fmul2_rn(q, make_float2(rcp_approx(den0), rcp_approx(den1))), f2(kfs), BT[p]);
+          }
         } else {
           float2 h;
           if (MODE == kSeries4) {
@@ -717,7 +729,13 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
             h = __ffma2_rn(f2(kc.a2), q, f2(kc.a1));
           }
           h = __ffma2_rn(h, q, f2(kc.a0));
-          U = __ffma2_rn(q, h, BT[p]);
+          if (WEIGHT) {
+            const float2 dU = __fmul2_rn(q, h);
+            U = __fadd2_rn(dU, BT[p]);
+            wgt = __fmul2_rn(__fadd2_rn(BT[p], f2(rtk)), __ffma2_rn(dU, f2(inv_ks2), f2(rrk)));
+          } else {
+            U = __ffma2_rn(q, h, BT[p]);
+          }
         }
         if (MOTION) {   // moving receiver: U = dU / (1 + w.v/c) ~ dU (kap0 + kg.d) + urr
           float2 kap = __ffma2_rn(f2(kc.kgy), DY[p], f2(kc.kap0));
@@ -740,7 +758,8 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
             addr = (addr & mk) | (zcell & ~mk);
           }
           const float4 w = lds128(addr);
-          const float2 eh = __ffma2_rn(f2(Us), make_float2(w.z, w.w), make_float2(w.x, w.y));
+          float2 eh = __ffma2_rn(f2(Us), make_float2(w.z, w.w), make_float2(w.x, w.y));
+          if (WEIGHT) eh = __fmul2_rn(eh, f2(s ? wgt.y : wgt.x));
           float sn, cs;
           __sincosf(phs, &sn, &cs);
           const float2 rot = make_float2(cs, sn);

@@ -22,7 +22,8 @@ _NAMES = {0: "SAS_OK", -1: "SAS_E_INVALID", -2: "SAS_E_STATE", -3: "SAS_E_NOMEM"
 
 EXPORTS = ("sas_bp_create", "sas_bp_destroy", "sas_bp_set_pings", "sas_bp_set_pings_device", "sas_bp_form",
            "sas_bp_form_device", "sas_bp_count_terms", "sas_bp_workspace_bytes", "sas_rangecompress",
-           "sas_rangecompress_device", "sas_last_error", "sas_version", "sas_bp_get_plan", "sas_bp_form_streamed", "sas_bp_set_beam", "sas_bp_set_motion", "sas_bp_set_medium")
+           "sas_rangecompress_device", "sas_last_error", "sas_version", "sas_bp_get_plan", "sas_bp_form_streamed", "sas_bp_set_beam", "sas_bp_set_motion", "sas_bp_set_medium",
+           "sas_bp_set_weighting", "sas_upsample", "sas_upsample_device", "sas_baseband", "sas_baseband_device")
 
 
 class SasError(RuntimeError):
@@ -80,6 +81,13 @@ def load_library(path: Optional[str] = None):
         "sas_bp_set_beam": ([vp, ctypes.POINTER(sas_beam), f64p, i32], ctypes.c_int),
         "sas_bp_set_motion": ([vp, f64p, i32], ctypes.c_int),
         "sas_bp_set_medium": ([vp, ctypes.c_double, ctypes.c_double], ctypes.c_int),
+        "sas_bp_set_weighting": ([vp, i32], ctypes.c_int),
+        "sas_upsample": ([f32p, i32, i32, i32, f32p], ctypes.c_int),
+        "sas_upsample_device": ([vp, i32, i32, i32, vp, vp], ctypes.c_int),
+        "sas_baseband": ([f32p, i32, i32, i32, ctypes.c_double, ctypes.c_double, f64p, f32p, i32, i32, i32, f32p],
+                         ctypes.c_int),
+        "sas_baseband_device": ([vp, i32, i32, i32, ctypes.c_double, ctypes.c_double, f64p, f32p, i32, i32, i32, vp,
+                                 vp], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name, None)
@@ -286,6 +294,10 @@ class Backprojector:
         isovelocity."""
         _check(_lib.sas_bp_set_medium(self._h, float(zb), float(c2)))
 
+    def set_weighting(self, spreading: bool = False):
+        """Multiply every term by R_tx R_rx (NEXT-4, R18); False = unweighted sum (R6)."""
+        _check(_lib.sas_bp_set_weighting(self._h, 1 if spreading else 0))
+
     def plan(self) -> dict:
         """The execution plan (tile, window, rx_mode, tma, batch) -- sas_bp_get_plan."""
         p = sas_bp_plan()
@@ -321,4 +333,60 @@ def rangecompress_device(raw, replica, out, stream=None):
     _check(lib.sas_rangecompress_device(_dev_ptr(raw, raw.numel() * 8), nch, 1, Ns,
                                         _dev_ptr(replica, replica.numel() * 8), replica.numel(),
                                         _dev_ptr(out, raw.numel() * 8), _stream_ptr(stream)))
+    return out
+
+
+def upsample(x, U: int) -> np.ndarray:
+    """Host xU band-limited upsampling by the 8-tap windowed sinc (K1b, R19): complex64
+    [..., Ns] -> [..., U*Ns] at rate U*fs, same t0."""
+    lib = load_library()
+    x = np.ascontiguousarray(x, dtype=np.complex64)
+    shp = x.shape
+    Ns = shp[-1]
+    nch = int(np.prod(shp[:-1])) if len(shp) > 1 else 1
+    out = np.empty(shp[:-1] + (U * Ns,), dtype=np.complex64)
+    f = lambda a: a.view(np.float32).ctypes.data_as(ctypes.POINTER(ctypes.c_float))
+    _check(lib.sas_upsample(f(x), nch, Ns, int(U), f(out)))
+    return out
+
+
+def upsample_device(x, U: int, out, stream=None):
+    """CUDA-tensor xU upsampling: complex64 [..., Ns] -> out complex64 [..., U*Ns]."""
+    lib = load_library()
+    Ns = x.shape[-1]
+    nch = x.numel() // Ns
+    _check(lib.sas_upsample_device(_dev_ptr(x, x.numel() * 8), nch, Ns, int(U), _dev_ptr(out, x.numel() * 8 * U),
+                                   _stream_ptr(stream)))
+    return out
+
+
+def _bb_args(t0, h, P):
+    t = None if t0 is None else np.ascontiguousarray(t0, dtype=np.float64).reshape(P)
+    hh = np.ascontiguousarray(h, dtype=np.float32).ravel()
+    return t, hh
+
+
+def baseband(x, fs_in: float, fc: float, t0, h, D: int, Nout: int) -> np.ndarray:
+    """Host basebanding (K0, R20): real float32 [P][E][Nin] at fs_in -> complex64 [P][E][Nout]:
+    mix by exp(-j 2 pi fc (t0_p + n/fs_in)), centred FIR h (odd length), keep every D-th sample."""
+    lib = load_library()
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    P, E, Nin = x.shape
+    t, hh = _bb_args(t0, h, P)
+    out = np.empty((P, E, int(Nout)), dtype=np.complex64)
+    _check(lib.sas_baseband(_ptr(x, ctypes.c_float), P, E, Nin, float(fs_in), float(fc), _ptr(t, ctypes.c_double),
+                            _ptr(hh, ctypes.c_float), hh.size, int(D), int(Nout),
+                            out.view(np.float32).ctypes.data_as(ctypes.POINTER(ctypes.c_float))))
+    return out
+
+
+def baseband_device(x, fs_in: float, fc: float, t0, h, D: int, out, stream=None):
+    """CUDA-tensor basebanding: float32 [P][E][Nin] -> out complex64 [P][E][Nout] (t0, h host)."""
+    lib = load_library()
+    P, E, Nin = x.shape
+    Nout = out.shape[-1]
+    t, hh = _bb_args(t0, h, P)
+    _check(lib.sas_baseband_device(_dev_ptr(x, x.numel() * 4), P, E, Nin, float(fs_in), float(fc),
+                                   _ptr(t, ctypes.c_double), _ptr(hh, ctypes.c_float), hh.size, int(D), int(Nout),
+                                   _dev_ptr(out, P * E * Nout * 8), _stream_ptr(stream)))
     return out
