@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-k1", action="store_true")
     ap.add_argument("--no-gated", action="store_true")
+    ap.add_argument("--no-next4", action="store_true")
     return ap.parse_args()
 
 
@@ -371,6 +372,60 @@ def run_sasbp(args):
               "traffic": _profile_traffic("ncu_k1_r01.json", None)}
         del out_d
 
+    # ---- NEXT-4: spreading-weighted K2 on the same workload; K1b x4 upsampling and K0 basebanding
+    # on the same channel layout (cfg-2 channels recorded at fs/4, resp. real passband at 4 fs)
+    next4 = None
+    if not args.no_next4 and rank == 0 and world == 1:
+        def _time(fn, nrep):
+            for _ in range(2):
+                fn()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(nrep):
+                fn()
+            b.record(stream)
+            torch.cuda.synchronize()
+            return a.elapsed_time(b) / nrep
+        hbm = _measured_hbm()
+        bp.set_weighting(True)
+        w_ms = _time(lambda: bp.form_device(img, stream=stream), args.steps)
+        bp.set_weighting(False)
+        nch = P * E
+        ns_in = Ns // 4
+        up_in = echoes_d.view(-1)[: nch * ns_in].view(nch, ns_in)
+        up_out = torch.empty((nch, 4 * ns_in), dtype=torch.complex64, device=dev)
+        up_ms = _time(lambda: pkg.upsample_device(up_in, 4, up_out, stream=stream), 5)
+        up_bytes = 8 * nch * ns_in * (1 + 4)
+        del up_out
+        nin = 4 * Ns
+        pb = torch.randn((P, E, nin), dtype=torch.float32, device=dev)
+        bb_out = torch.empty((P, E, Ns), dtype=torch.complex64, device=dev)
+        kk = np.arange(-31, 32)
+        hbb = (2 * 0.1 * np.sinc(2 * 0.1 * kk) * (0.5 + 0.5 * np.cos(np.pi * kk / 32))).astype(np.float32)
+        hbb *= np.float32(2.0 / hbb.sum())
+        bb_ms = _time(lambda: pkg.baseband_device(pb, 4 * s.fs, s.fc, s.t0, hbb, 4, bb_out, stream=stream), 5)
+        bb_bytes = 4 * nch * nin + 8 * nch * Ns
+        del pb, bb_out
+        next4 = {
+            "weighted_k2": {"what": "TDBP with the spreading weight R_tx R_rx (R18), same workload",
+                            "ms_per_step": w_ms, "Gterm_per_s": dense / (w_ms * 1e-3) / 1e9,
+                            "frac": dense / (w_ms * 1e-3) / 1e9 / peak,
+                            "slowdown_vs_unweighted": w_ms / (total_ms / args.steps)},
+            "k1b_upsample": {"kernel": "upsample_kernel<4> (8-tap Lanczos, x4)",
+                             "shape": f"{nch} channels x {ns_in} -> {4 * ns_in} samples", "ms": up_ms,
+                             "algorithmic_bytes": up_bytes, "achieved": up_bytes / (up_ms * 1e-3) / 1e9,
+                             "unit": "GB/s", "bound": "hbm", "peak": hbm[0], "peak_source": hbm[1],
+                             "frac": up_bytes / (up_ms * 1e-3) / 1e9 / hbm[0],
+                             "note": "8 B read + 32 B written per input sample"},
+            "k0_baseband": {"kernel": "baseband_kernel (polyphase, fp64 phase reduction)",
+                            "shape": f"{nch} channels x {nin} real @ {4 * s.fs / 1e3:.0f} kHz -> {Ns} complex, D=4, "
+                                     f"Nh={hbb.size}", "ms": bb_ms, "algorithmic_bytes": bb_bytes,
+                            "achieved": bb_bytes / (bb_ms * 1e-3) / 1e9, "unit": "GB/s", "bound": "hbm",
+                            "peak": hbm[0], "peak_source": hbm[1], "frac": bb_bytes / (bb_ms * 1e-3) / 1e9 / hbm[0],
+                            "note": "4 B read per passband sample + 8 B written per baseband sample"},
+        }
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_oracle_rate(s, echoes_h, args.cpu_seconds)
@@ -400,6 +455,7 @@ def run_sasbp(args):
             "cpu_baseline": cpu,
             "k1_rangecompress": k1,
             "next1_gated": gated,
+            "next4": next4,
         }
         if cpu:
             out["gpu_over_cpu"] = value / cpu["value"]

@@ -22,6 +22,8 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
+#include <algorithm>
 #include <vector>
 #include <cuda_runtime.h>
 
@@ -164,6 +166,116 @@ __global__ void __launch_bounds__(kBbThreads) baseband_kernel(const float* __res
   }
 }
 
+// Register-blocked polyphase form (the default): each thread owns kBbR = 8 consecutive outputs.
+// With j = a D + q the sum is  out[t] = sum_q sum_a hq[q][a] zq[q][t + a],  hq[q][a] =
+// h[Nh - 1 - (a D + q)] (zero-padded to Apad taps per phase, a multiple of 8): per phase a
+// 1-D convolution whose input window slides through registers -- per block of 8 taps a thread
+// loads 8 new samples and 8 (broadcast) taps and issues 64 complex MACs as FFMA2.  The polyphase
+// arrays are padded one sample per 8 (index i + i/8) so the warp's stride-8 window loads are
+// conflict-free (stride 9 x 8 B).
+constexpr int kBbR = 8;
+
+__device__ __forceinline__ int bb_pad(int i) { return i + (i >> 3); }
+
+__device__ __forceinline__ void bb_block(float2 (&acc)[kBbR], const float2 (&wa)[kBbR], const float2 (&wb)[kBbR],
+                                         const float2* __restrict__ hq) {
+#pragma unroll
+  for (int aa = 0; aa < 8; ++aa) {
+    const float2 hh = hq[aa];   // (h, h), same address for the whole warp
+#pragma unroll
+    for (int r = 0; r < kBbR; ++r) {
+      const float2 z = (r + aa < 8) ? wa[r + aa] : wb[r + aa - 8];
+      acc[r] = __ffma2_rn(hh, z, acc[r]);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) baseband_blocked_kernel(const float* __restrict__ x, int E, int Nin, double kr,
+                                                               const double* __restrict__ base,
+                                                               const float2* __restrict__ hq_g, int Nh, int D, int Apad,
+                                                               int Nout, int MO, long long runs, float2 rot1,
+                                                               float2* __restrict__ out) {
+  extern __shared__ __align__(16) unsigned char bb_smem[];
+  float2* hs = reinterpret_cast<float2*>(bb_smem);            // [D][Apad] (h, h)
+  float2* sz = hs + (size_t)D * Apad;                          // [D][LqP] padded polyphase input
+  const long long b = blockIdx.x;
+  const long long ch = b / runs;
+  const int m0 = (int)(b - ch * runs) * MO;
+  const int half = (Nh - 1) >> 1;
+  const int nlo = m0 * D + half - (Nh - 1);    // local input i = n - nlo = t D + j
+  const int Lq = MO + Apad;                     // samples per phase (+ slack for the last block)
+  const int LqP = bb_pad(Lq) + 1;
+  const float* xc = x + ch * (long long)Nin;
+  const double bp = base[ch / E];
+  for (int k = threadIdx.x; k < D * Apad; k += blockDim.x) hs[k] = hq_g[k];
+  // Staging, phase-inner: thread k-slots k = k0 + u blockDim (8 in flight), samples n = nlo + k D + q.
+  // The carrier phasor exp(-j 2 pi fc t_n) is evaluated exactly (fp64 reduction + sincos) at
+  // q = 0 and advanced by the fp32 rotation exp(-j 2 pi fc / fs_in) for q = 1..D-1, re-anchored
+  // every 8 phases, so the error stays ~8 fp32 ulps.  No integer division anywhere.
+  constexpr int kU = 8;
+  const float2 rot = rot1;
+  for (int k0 = threadIdx.x; k0 < Lq; k0 += kU * blockDim.x) {
+    float2 w[kU];
+    for (int q = 0; q < D; ++q) {
+      float v[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int k = k0 + u * blockDim.x;
+        const int n = nlo + k * D + q;
+        v[u] = (k < Lq && n >= 0 && n < Nin) ? __ldcs(xc + n) : 0.f;
+      }
+      if ((q & 7) == 0) {
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          double ph = fma((double)(nlo + (k0 + u * (int)blockDim.x) * D + q), kr, bp);   // cycles, fp64
+          ph -= rint(ph);
+          __sincosf(-6.283185307179586f * (float)ph, &w[u].y, &w[u].x);
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < kU; ++u)
+          w[u] = make_float2(fmaf(w[u].x, rot.x, -w[u].y * rot.y), fmaf(w[u].x, rot.y, w[u].y * rot.x));
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int k = k0 + u * blockDim.x;
+        if (k < Lq) sz[q * LqP + bb_pad(k)] = make_float2(v[u] * w[u].x, v[u] * w[u].y);
+      }
+    }
+  }
+  __syncthreads();
+  const int t0 = threadIdx.x * kBbR;
+  if (m0 + t0 >= Nout) return;
+  float2 acc[kBbR];
+#pragma unroll
+  for (int r = 0; r < kBbR; ++r) acc[r] = make_float2(0.f, 0.f);
+  for (int q = 0; q < D; ++q) {
+    const float2* zq = sz + q * LqP;
+    const float2* hq = hs + q * Apad;
+    float2 wa[kBbR], wb[kBbR];
+#pragma unroll
+    for (int r = 0; r < kBbR; ++r) wa[r] = zq[bb_pad(t0 + r)];
+    for (int ab = 0; ab < Apad; ab += 16) {
+#pragma unroll
+      for (int r = 0; r < kBbR; ++r) wb[r] = zq[bb_pad(t0 + ab + 8 + r)];
+      bb_block(acc, wa, wb, hq + ab);
+      if (ab + 8 >= Apad) break;
+#pragma unroll
+      for (int r = 0; r < kBbR; ++r) wa[r] = zq[bb_pad(t0 + ab + 16 + r)];
+      bb_block(acc, wb, wa, hq + ab + 8);
+    }
+  }
+  float2* yo = out + ch * (long long)Nout + m0 + t0;
+  if (m0 + t0 + kBbR <= Nout && ((((uintptr_t)yo) & 15) == 0)) {
+#pragma unroll
+    for (int r = 0; r < kBbR; r += 2) st_cs_v4(yo + r, acc[r], acc[r + 1]);
+  } else {
+#pragma unroll
+    for (int r = 0; r < kBbR; ++r)
+      if (m0 + t0 + r < Nout) __stcs(yo + r, acc[r]);
+  }
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------- C ABI
@@ -246,7 +358,59 @@ extern "C" sas_status sas_baseband_device(const void* x_dev, int32_t P, int32_t 
     if (!std::isfinite(h[k])) return cond_fail(SAS_E_INVALID, "non-finite FIR tap");
   double kr = fc / fs_in;                     // cycles per input sample, mod 1
   kr -= std::floor(kr);
-  // outputs per CTA: the mixed span (MO - 1) D + Nh fits kBbSmem bytes next to the taps
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  // blocked polyphase kernel: 8 outputs per thread, threads = 256 / 128 / 64 / 32 so that the
+  // padded polyphase arrays fit shared memory
+  {
+    const int A = (Nh + D - 1) / D;                  // taps per phase
+    const int Apad = (A + 7) & ~7;
+    int threads = 256;
+    size_t smem = 0;
+    for (; threads >= 32; threads >>= 1) {
+      const long long MOb = (long long)threads * kBbR;
+      const long long Lq = MOb + Apad;
+      const long long LqP = Lq + (Lq >> 3) + 1;
+      smem = ((size_t)D * Apad + (size_t)D * LqP) * sizeof(float2);
+      if (smem <= 200 * 1024) break;
+    }
+    const char* force = getenv("SASBP_BB_SIMPLE");
+    if (threads >= 32 && !(force && force[0] == '1')) {
+      const int MOb = threads * kBbR;
+      const long long runs = (Nout + MOb - 1) / MOb;
+      const long long blocks = runs * (long long)P * E;
+      if (blocks > 2147483647LL) return cond_fail(SAS_E_INVALID, "too many channels for one launch");
+      std::vector<float2> hq((size_t)D * Apad, make_float2(0.f, 0.f));
+      for (int q = 0; q < D; ++q)
+        for (int a = 0; a < Apad; ++a) {
+          const int j = a * D + q;
+          if (j < Nh) hq[(size_t)q * Apad + a] = make_float2(h[Nh - 1 - j], h[Nh - 1 - j]);
+        }
+      double* dbase = nullptr;
+      float2* dhq = nullptr;
+      cudaError_t e = cudaMallocAsync(&dbase, P * sizeof(double), st);
+      if (e == cudaSuccess) e = cudaMallocAsync(&dhq, hq.size() * sizeof(float2), st);
+      if (e != cudaSuccess) {
+        if (dbase) cudaFreeAsync(dbase, st);
+        return cond_fail(SAS_E_NOMEM, "cudaMallocAsync(baseband tables)", e);
+      }
+      e = cudaMemcpyAsync(dbase, base.data(), P * sizeof(double), cudaMemcpyHostToDevice, st);
+      if (e == cudaSuccess) e = cudaMemcpyAsync(dhq, hq.data(), hq.size() * sizeof(float2), cudaMemcpyHostToDevice, st);
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(baseband_blocked_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e == cudaSuccess) {
+        baseband_blocked_kernel<<<(unsigned)blocks, threads, smem, st>>>(
+            (const float*)x_dev, E, Nin, kr, dbase, dhq, Nh, D, Apad, Nout, MOb, runs,
+            make_float2((float)std::cos(2.0 * 3.141592653589793 * kr), (float)-std::sin(2.0 * 3.141592653589793 * kr)),
+            (float2*)out_dev);
+        e = cudaGetLastError();
+      }
+      cudaFreeAsync(dbase, st);
+      cudaFreeAsync(dhq, st);
+      if (e != cudaSuccess) return cond_fail(SAS_E_CUDA, "baseband_blocked_kernel", e);
+      return SAS_OK;
+    }
+  }
+  // simple kernel (very large decimation): the mixed span (MO - 1) D + Nh fits kBbSmem bytes
   const int tap_bytes = ((Nh + 3) & ~3) * 4;
   const long long cap = (kBbSmem - tap_bytes) / 8;                      // complex samples
   long long MO = (cap - Nh) / D + 1;
@@ -259,7 +423,6 @@ extern "C" sas_status sas_baseband_device(const void* x_dev, int32_t P, int32_t 
   const long long runs = (Nout + MO - 1) / MO;
   const long long blocks = runs * (long long)P * E;
   if (blocks > 2147483647LL) return cond_fail(SAS_E_INVALID, "too many channels for one launch");
-  cudaStream_t st = (cudaStream_t)cuda_stream;
   double* dbase = nullptr;
   float* dh = nullptr;
   cudaError_t e = cudaMallocAsync(&dbase, P * sizeof(double), st);

@@ -207,8 +207,13 @@ def _lowpass(n_half, cutoff):
 
 @pytest.mark.parametrize("P,E,Nin,D,Nh,Nout", [(1, 1, 1, 1, 1, 1), (2, 3, 4096, 4, 65, 1024), (3, 2, 5000, 4, 33, 1300),
                                                (1, 4, 999, 1, 7, 999), (2, 2, 3000, 37, 255, 90),
-                                               (1, 2, 20000, 2, 1023, 10000), (2, 1, 700, 3, 1, 300)])
-def test_baseband_vs_oracle(bpmod, P, E, Nin, D, Nh, Nout):
+                                               (1, 2, 20000, 2, 1023, 10000), (2, 1, 700, 3, 1, 300), (1, 1, 3000, 64, 129, 47),
+                                               (1, 1, 70000, 300, 601, 233)])
+@pytest.mark.parametrize("path", ["blocked", "simple"])
+def test_baseband_vs_oracle(bpmod, P, E, Nin, D, Nh, Nout, path, monkeypatch):
+    """Both kernels (register-blocked polyphase default; the simple one for huge decimations)."""
+    if path == "simple":
+        monkeypatch.setenv("SASBP_BB_SIMPLE", "1")
     rng = np.random.default_rng(P * 7 + Nin + D + Nh)
     x = rng.normal(size=(P, E, Nin)).astype(np.float32)
     h = (2.0 * _lowpass((Nh - 1) // 2, 0.4 / D)) if Nh > 1 else np.array([1.0], dtype=np.float32)
