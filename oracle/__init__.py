@@ -16,7 +16,10 @@ delays, zero-extension values, point-target physics and invariants;
 the azimuth / elevation boundary examples, monotonicity in the beamwidth, rigid-rotation
 invariance and the config-1 target under the generator's own beam; the NEXT-4 variants
 ``tdbp_points_weighted`` (R18), ``upsample`` / ``lanczos4`` (R19) and ``baseband`` (R20) by
-closed forms, interpolating / band-limited reproduction properties and config-1 physics.
+closed forms, interpolating / band-limited reproduction properties and config-1 physics;
+``whitening_gain`` / ``rangecompress_whitened`` (R21) by the SPEC's hand examples (flat ->
+0 dB, P = [1, 4] -> [0, -6.02] dB), the gamma limit, G = 1 -> plain compression and spectral
+flattening of coloured noise.
 """
 from __future__ import annotations
 
@@ -90,6 +93,12 @@ def _load():
                                         ctypes.c_double, f64p, f32p, ctypes.c_int32, ctypes.c_int32,
                                         ctypes.c_int32, f64p]
         lib.oracle_baseband.restype = ctypes.c_int
+        lib.oracle_whitening_gain.argtypes = [f32p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_double,
+                                              f64p, f64p]
+        lib.oracle_whitening_gain.restype = ctypes.c_int
+        lib.oracle_rangecompress_whitened.argtypes = [f32p, ctypes.c_int64, ctypes.c_int32, f32p, ctypes.c_int32,
+                                                      f64p, ctypes.c_int32, f64p]
+        lib.oracle_rangecompress_whitened.restype = ctypes.c_int
         lib.oracle_num_threads.restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -318,6 +327,43 @@ def baseband(x, fs_in, fc, t0, h, D, Nout):
     if rc != 0:
         raise ValueError("oracle_baseband: invalid arguments")
     return out[..., 0] + 1j * out[..., 1]
+
+
+def whitening_gain(raw, M, gamma):
+    """Eq. 9 whitening gain (R21): batch-mean M-point periodogram P of complex64 [..., Ns] and
+    G = h(1/(gamma mean P + P)), max G = 1.  Returns (G, P), fp64 [M] each."""
+    lib = _load()
+    raw = np.ascontiguousarray(raw, dtype=np.complex64)
+    Ns = raw.shape[-1]
+    nch = int(np.prod(raw.shape[:-1])) if raw.ndim > 1 else 1
+    G = np.zeros(M, dtype=np.float64)
+    P = np.zeros(M, dtype=np.float64)
+    rc = lib.oracle_whitening_gain(_p(raw.view(np.float32), ctypes.c_float), nch, Ns, int(M), float(gamma),
+                                   _p(G, ctypes.c_double), _p(P, ctypes.c_double))
+    if rc == -2:
+        raise ValueError("oracle_whitening_gain: no spectrum (all-zero batch)")
+    if rc != 0:
+        raise ValueError("oracle_whitening_gain: invalid arguments")
+    return G, P
+
+
+def rangecompress_whitened(raw, replica, G):
+    """Whitening FIR (frequency sampling of G over one centred period) then the matched filter
+    (R21 + R14); complex64 [..., Ns] -> complex128 of the same shape."""
+    lib = _load()
+    raw = np.ascontiguousarray(raw, dtype=np.complex64)
+    replica = np.ascontiguousarray(replica, dtype=np.complex64).ravel()
+    G = np.ascontiguousarray(G, dtype=np.float64).ravel()
+    shape = raw.shape
+    Ns = shape[-1]
+    nch = int(np.prod(shape[:-1])) if len(shape) > 1 else 1
+    out = np.zeros((nch, Ns, 2), dtype=np.float64)
+    rc = lib.oracle_rangecompress_whitened(_p(raw.view(np.float32), ctypes.c_float), nch, Ns,
+                                           _p(replica.view(np.float32), ctypes.c_float), replica.size,
+                                           _p(G, ctypes.c_double), G.size, _p(out, ctypes.c_double))
+    if rc != 0:
+        raise ValueError("oracle_rangecompress_whitened: invalid arguments")
+    return (out[..., 0] + 1j * out[..., 1]).reshape(shape)
 
 
 def num_threads() -> int:

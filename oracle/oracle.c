@@ -36,11 +36,13 @@
  *
  * NEXT rows: gating (R15), moving receiver (R16), sediment refraction (R17),
  * and the NEXT-4 interpolation / conditioning variants -- spreading weight R_tx R_rx (R18),
- * 8-tap windowed-sinc xU upsampling (R19) and passband basebanding (R20).
+ * 8-tap windowed-sinc xU upsampling (R19), passband basebanding (R20) and spectral whitening
+ * (R21).
  */
 #include <math.h>
 #include <stdint.h>
 #include <stddef.h>
+#include <stdlib.h>
 
 #ifdef _OPENMP
 #include <omp.h>
@@ -478,6 +480,110 @@ int oracle_baseband(const float* x, int32_t P, int32_t E, int32_t Nin, double fs
       y[2 * m + 1] = yi;
     }
   }
+  return 0;
+}
+
+/*
+ * Spectral whitening (NEXT-4, reading R21; Eq. (eqn:whitening)):
+ *     G(f) = h( 1 / (gamma * mean_f P(f) + P(f)) ),   h = scaling so that max G = 1 (0 dB minimum
+ *     attenuation, "h is a normalization function ensuring the minimum attenuation is 0 dB")
+ * with the power estimate P the batch-mean periodogram on an M-point frequency grid:
+ *     P[k] = (1 / (nch B)) sum_ch sum_{b<B} | sum_{n<M} x_ch[b M + n] exp(-j 2 pi k n / M) |^2,
+ *     B = max(1, floor(Ns / M)) blocks per channel, x zero past Ns.
+ *   raw : complex64 [nch][Ns]; G, P : fp64 [M] out.  Returns -2 if gamma*mean + P[k] <= 0 for
+ *   some k (an all-zero batch has no spectrum), -1 on invalid sizes.
+ */
+int oracle_whitening_gain(const float* raw, int64_t nch, int32_t Ns, int32_t M, double gamma, double* G, double* P) {
+  const double TWO_PI = ORACLE_TWO_PI;
+  if (nch < 1 || Ns < 1 || M < 1 || !(gamma >= 0)) return -1;
+  const int32_t B = Ns / M > 0 ? Ns / M : 1;
+  for (int32_t k = 0; k < M; ++k) P[k] = 0.0;
+  for (int64_t ch = 0; ch < nch; ++ch) {
+    const float* x = raw + 2 * ch * (int64_t)Ns;
+    for (int32_t b = 0; b < B; ++b) {
+      for (int32_t k = 0; k < M; ++k) {
+        double re = 0.0, im = 0.0;
+        for (int32_t n = 0; n < M; ++n) {
+          double xr, xi;
+          sample_at(x, Ns, (int64_t)b * M + n, &xr, &xi);
+          const double a = -TWO_PI * (double)(((int64_t)k * n) % M) / (double)M;
+          re += xr * cos(a) - xi * sin(a);
+          im += xr * sin(a) + xi * cos(a);
+        }
+        P[k] += re * re + im * im;
+      }
+    }
+  }
+  double mean = 0.0;
+  for (int32_t k = 0; k < M; ++k) {
+    P[k] /= (double)nch * (double)B;
+    mean += P[k];
+  }
+  mean /= (double)M;
+  double gmax = 0.0;
+  for (int32_t k = 0; k < M; ++k) {
+    const double den = gamma * mean + P[k];
+    if (!(den > 0)) return -2;
+    G[k] = 1.0 / den;
+    if (G[k] > gmax) gmax = G[k];
+  }
+  for (int32_t k = 0; k < M; ++k) G[k] /= gmax;
+  return 0;
+}
+
+/*
+ * Whitened range compression (NEXT-4, R21): G of Eq. 9 is a POWER gain (it flattens P: with
+ * gamma = 0, G P is constant; SPEC S:208-209 gives its values in dB as 10 log10 G), so the signal
+ * is filtered with the amplitude response sqrt(G[k]) at f = k fs / M -- the M-tap
+ * frequency-sampling FIR over one centred period,
+ *     w[i] = (1/M) sum_k sqrt(G[k]) exp(+j 2 pi k i / M),   i = -M/2 .. M/2 - 1   (M even; M = 1: w = [sqrt G0])
+ * -- followed by the matched filter of R14:
+ *     x_w[n] = sum_i w[i] x[n - i]          (x zero outside 0..Ns-1, x_w not truncated)
+ *     y[n]   = sum_{m<Nr} x_w[n + m] conj(r[m]),   n = 0..Ns-1.
+ *   raw : complex64 [nch][Ns], replica complex64 [Nr], G fp64 [M], out complex128 [nch][Ns].
+ */
+int oracle_rangecompress_whitened(const float* raw, int64_t nch, int32_t Ns, const float* replica, int32_t Nr,
+                                  const double* G, int32_t M, double* out) {
+  const double TWO_PI = ORACLE_TWO_PI;
+  if (nch < 0 || Ns < 1 || Nr < 1 || M < 1 || (M > 1 && (M % 2) != 0)) return -1;
+  const int32_t i0 = -(M / 2);
+  double* w = (double*)malloc(sizeof(double) * 2 * (size_t)M);
+  if (!w) return -1;
+  for (int32_t t = 0; t < M; ++t) {
+    const int32_t i = i0 + t;
+    double re = 0.0, im = 0.0;
+    for (int32_t k = 0; k < M; ++k) {
+      const int64_t km = (((int64_t)k * i) % M + M) % M;
+      const double a = TWO_PI * (double)km / (double)M;
+      re += sqrt(G[k]) * cos(a);
+      im += sqrt(G[k]) * sin(a);
+    }
+    w[2 * t] = re / M;
+    w[2 * t + 1] = im / M;
+  }
+#pragma omp parallel for schedule(static)
+  for (int64_t ch = 0; ch < nch; ++ch) {
+    const float* x = raw + 2 * ch * (int64_t)Ns;
+    double* y = out + 2 * ch * (int64_t)Ns;
+    for (int32_t n = 0; n < Ns; ++n) {
+      double yr = 0.0, yi = 0.0;
+      for (int32_t m = 0; m < Nr; ++m) {
+        double xwr = 0.0, xwi = 0.0;                            /* x_w[n + m] */
+        for (int32_t t = 0; t < M; ++t) {
+          double xr, xi;
+          sample_at(x, Ns, (int64_t)n + m - (i0 + t), &xr, &xi);
+          xwr += w[2 * t] * xr - w[2 * t + 1] * xi;
+          xwi += w[2 * t] * xi + w[2 * t + 1] * xr;
+        }
+        const double rr = replica[2 * m], ri = -(double)replica[2 * m + 1];   /* conj(r[m]) */
+        yr += xwr * rr - xwi * ri;
+        yi += xwr * ri + xwi * rr;
+      }
+      y[2 * n] = yr;
+      y[2 * n + 1] = yi;
+    }
+  }
+  free(w);
   return 0;
 }
 

@@ -219,3 +219,64 @@ def test_baseband_channel_layout_and_t0_per_ping():
     y = oracle.baseband(x, fs, fc, t0, h, 2, 128)
     assert np.max(np.abs(y[0] - y[0, :1])) == 0.0
     assert np.max(np.abs(y[1] - y[0] * np.exp(-2j * np.pi / 8))) <= 1e-9 * np.max(np.abs(y))
+
+
+# ---------------------------------------------------------------- R21 spectral whitening
+
+def test_whitening_gain_hand_values():
+    g = _load("next4.json")["whitening"]
+    # (a) unit impulse at every block start: flat periodogram -> 0 dB everywhere
+    M, B = 16, 5
+    x = np.zeros((3, M * B), dtype=np.complex64)
+    x[:, ::M] = 1.0
+    G, P = oracle.whitening_gain(x, M, 0.0)
+    assert np.max(np.abs(P - 1.0)) <= 1e-12 and np.max(np.abs(G - 1.0)) <= 1e-12
+    # (b) P = [1, 4], gamma = 0 -> G = [1, 1/4] = [0, -6.02] dB
+    b = g["b"]
+    xb = np.tile(np.array(b["block"], dtype=np.complex64), 7).reshape(1, -1)
+    G, P = oracle.whitening_gain(xb, b["M"], 0.0)
+    assert np.allclose(P, b["P"], atol=1e-12) and np.allclose(G, b["G"], atol=1e-12)
+    assert np.allclose(10 * np.log10(G), b["dB"], atol=1e-4)
+    # (c) gamma = 1
+    G, _ = oracle.whitening_gain(xb, b["M"], g["c"]["gamma"])
+    assert np.allclose(G, g["c"]["G"], atol=1e-7)
+    # (d) gamma -> infinity: no shaping
+    G, _ = oracle.whitening_gain(xb, b["M"], 1e12)
+    assert np.max(np.abs(G - 1.0)) <= 1e-11
+
+
+def test_whitening_gain_partial_block_and_zero_batch():
+    """Ns < M: one zero-padded block; an all-zero batch has no spectrum (error)."""
+    x = np.zeros((2, 5), dtype=np.complex64)
+    x[:, 0] = 1.0
+    G, P = oracle.whitening_gain(x, 8, 0.0)
+    assert np.allclose(P, 1.0) and np.allclose(G, 1.0)
+    with pytest.raises(ValueError):
+        oracle.whitening_gain(np.zeros((2, 64), dtype=np.complex64), 8, 0.0)
+
+
+def test_whitened_compression_with_unit_gain_is_plain_compression():
+    """G = 1: w = delta[i], the cascade is exactly the matched filter of R14."""
+    rng = np.random.default_rng(21)
+    x = ((rng.normal(size=(2, 300)) + 1j * rng.normal(size=(2, 300))) / np.sqrt(2)).astype(np.complex64)
+    r = ((rng.normal(size=17) + 1j * rng.normal(size=17))).astype(np.complex64)
+    for M in (1, 2, 16):
+        y = oracle.rangecompress_whitened(x, r, np.ones(M))
+        assert np.max(np.abs(y - oracle.rangecompress(x, r))) <= 1e-12 * np.max(np.abs(y))
+
+
+def test_whitening_flattens_coloured_noise():
+    """Coloured noise (white noise through a 2-tap low-pass, spectrum 4 cos^2(pi f)): after the
+    whitening FIR with the estimated gain (gamma = 0) the batch periodogram's max/min ratio falls
+    by more than 10x (Eq. 9's purpose: 'flatten the spectrum'); the impulse replica r = [1] makes
+    the compression the identity."""
+    rng = np.random.default_rng(5)
+    n = (rng.normal(size=(8, 4097)) + 1j * rng.normal(size=(8, 4097))) / np.sqrt(2)
+    x = (n[:, 1:] + 0.8 * n[:, :-1]).astype(np.complex64)
+    M = 32
+    G, P = oracle.whitening_gain(x, M, 0.0)
+    assert P.max() / P.min() > 30
+    xw = oracle.rangecompress_whitened(x, np.array([1.0], dtype=np.complex64), G).astype(np.complex64)
+    _, Pw = oracle.whitening_gain(xw, M, 0.0)
+    assert (Pw.max() / Pw.min()) * 10 < P.max() / P.min()
+    assert Pw.max() / Pw.min() < 3.0
