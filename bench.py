@@ -407,6 +407,16 @@ def run_sasbp(args):
         bb_ms = _time(lambda: pkg.baseband_device(pb, 4 * s.fs, s.fc, s.t0, hbb, 4, bb_out, stream=stream), 5)
         bb_bytes = 4 * nch * nin + 8 * nch * Ns
         del pb, bb_out
+        # whitening (R21): gain estimate (M = 64 periodogram over the whole batch) and the
+        # whitened compression (one K1 pass with the composed Nr + 63-tap filter)
+        Mw = 64
+        Gw = torch.empty(Mw, dtype=torch.float32, device=dev)
+        wg_ms = _time(lambda: pkg.whitening_gain_device(echoes_d, Mw, 0.0, Gw, stream=stream), 3)
+        tt = np.arange(600) / s.fs - 2.5e-3
+        rep_w = torch.from_numpy((np.exp(1j * np.pi * (s.bandwidth / 5e-3) * tt ** 2) / np.sqrt(600)).astype(np.complex64)).to(dev)
+        wout = torch.empty_like(echoes_d)
+        wc_ms = _time(lambda: pkg.rangecompress_whitened_device(echoes_d, rep_w, Gw, wout, stream=stream), 5)
+        del wout
         next4 = {
             "weighted_k2": {"what": "TDBP with the spreading weight R_tx R_rx (R18), same workload",
                             "ms_per_step": w_ms, "Gterm_per_s": dense / (w_ms * 1e-3) / 1e9,
@@ -418,6 +428,12 @@ def run_sasbp(args):
                              "unit": "GB/s", "bound": "hbm", "peak": hbm[0], "peak_source": hbm[1],
                              "frac": up_bytes / (up_ms * 1e-3) / 1e9 / hbm[0],
                              "note": "8 B read + 32 B written per input sample"},
+            "whitening": {"gain_kernel": "wh_periodogram_kernel (M = 64 direct DFT per block) + wh_gain_kernel",
+                          "gain_ms": wg_ms, "gain_GB_per_s": 8 * nch * Ns / (wg_ms * 1e-3) / 1e9,
+                          "gain_frac_hbm": 8 * nch * Ns / (wg_ms * 1e-3) / 1e9 / hbm[0],
+                          "whitened_k1_ms": wc_ms,
+                          "whitened_k1_GB_per_s": 16 * nch * Ns / (wc_ms * 1e-3) / 1e9,
+                          "note": "gain: 8 B read per sample; whitened K1: 16 B per sample, Nr + M - 1 = 663 taps"},
             "k0_baseband": {"kernel": "baseband_kernel (polyphase, fp64 phase reduction)",
                             "shape": f"{nch} channels x {nin} real @ {4 * s.fs / 1e3:.0f} kHz -> {Ns} complex, D=4, "
                                      f"Nh={hbb.size}", "ms": bb_ms, "algorithmic_bytes": bb_bytes,

@@ -216,6 +216,38 @@ SASBP_API sas_status sas_rangecompress_device(const void* raw_dev, int32_t P, in
                                     const void* replica_dev, int32_t Nr, void* out_dev,
                                     void* cuda_stream);
 
+/* Spectral whitening gain (Eq. (eqn:whitening); reading R21):
+ *   P[k] = batch-mean M-point periodogram of raw (B = max(1, floor(Ns/M)) non-overlapping
+ *          blocks per channel, zero past Ns, averaged over all nch channels and blocks)
+ *   G[k] = h(1 / (gamma mean_k P + P[k])),  h = division by max_k (minimum attenuation 0 dB)
+ * G is a power gain (gamma = 0 makes G P constant).  raw: complex64 [nch][Ns]; G: float [M] out,
+ * HOST.  M must be 1 or even and <= 256; gamma >= 0 finite.
+ * Errors: SAS_E_INVALID for bad sizes / gamma / NULL pointers or an all-zero batch (no spectrum);
+ * SAS_E_NOMEM; SAS_E_CUDA. */
+SASBP_API sas_status sas_whitening_gain(const float* raw, int32_t nch, int32_t Ns, int32_t M, double gamma, float* G);
+
+/* Device variant: raw_dev and G_dev (float [M]) on the device, asynchronous on cuda_stream; an
+ * all-zero batch writes NaN to every G_dev[k] instead of failing. */
+SASBP_API sas_status sas_whitening_gain_device(const void* raw_dev, int32_t nch, int32_t Ns, int32_t M, double gamma,
+                                               float* G_dev, void* cuda_stream);
+
+/* Whitened range compression (R21 + R14): the data are filtered with the amplitude response
+ * sqrt(G[k]) at f = k fs / M (the M-tap frequency-sampling FIR over one centred period,
+ * w[i] = (1/M) sum_k sqrt(G[k]) exp(+j 2 pi k i / M), i = -M/2 .. M/2-1), then matched filtered:
+ *   out[ch][n] = sum_m (w * raw_ch)[n + m] conj(replica[m]),  n = 0..Ns-1, raw zero outside 0..Ns-1.
+ * Computed as ONE K1 pass with the composed filter conj(w) (x) replica (Nr + M - 1 taps, start lag
+ * 1 - M/2).  G: float [M], HOST for this call (device for the _device variant), finite, >= 0.
+ * Errors: SAS_E_INVALID (sizes, M not 1 or even <= 256, negative / non-finite G, NULL);
+ * SAS_E_UNSUPPORTED if Nr + M - 1 > 8192; SAS_E_NOMEM; SAS_E_CUDA. */
+SASBP_API sas_status sas_rangecompress_whitened(const float* raw, int32_t P, int32_t E, int32_t Ns,
+                                                const float* replica, int32_t Nr, const float* G, int32_t M,
+                                                float* out);
+
+/* Device variant (raw_dev, replica_dev, G_dev, out_dev on the device; asynchronous). */
+SASBP_API sas_status sas_rangecompress_whitened_device(const void* raw_dev, int32_t P, int32_t E, int32_t Ns,
+                                                       const void* replica_dev, int32_t Nr, const float* G_dev,
+                                                       int32_t M, void* out_dev, void* cuda_stream);
+
 /* Band-limited xU upsampling by the 8-tap windowed sinc (SPEC S:396
  * "8-tap windowed-sinc on the upsampled (x4) compressed series"; reading R19):
  *   out[ch][U n + r] = sum_{m=-3}^{4} in[ch][n + m] L(r/U - m),  L(s) = sinc(s) sinc(s/4), |s| < 4,

@@ -5,8 +5,10 @@ The product is libsasbp.so (C ABI, include/sasbp.h; hand-written sm_100a CUDA ke
 This package adds the ctypes binding (sasbp.py) and the multi-GPU driver (distributed.py).
 """
 from .sasbp import (Backprojector, SasError, load_library, make_grid, rangecompress,  # noqa: F401
-                    rangecompress_device, upsample, upsample_device, baseband, baseband_device, version,
+                    rangecompress_device, upsample, upsample_device, baseband, baseband_device, whitening_gain,
+                    whitening_gain_device, rangecompress_whitened, rangecompress_whitened_device, version,
                     EXPORTS, LIB_PATH)
 
 __all__ = ["Backprojector", "SasError", "load_library", "make_grid", "rangecompress", "rangecompress_device",
-           "upsample", "upsample_device", "baseband", "baseband_device", "version", "EXPORTS", "LIB_PATH"]
+           "upsample", "upsample_device", "baseband", "baseband_device", "whitening_gain", "whitening_gain_device",
+           "rangecompress_whitened", "rangecompress_whitened_device", "version", "EXPORTS", "LIB_PATH"]

@@ -17,6 +17,8 @@
 
 #include <cstdarg>
 #include <cstdio>
+#include <cmath>
+#include <cstdlib>
 #include <mutex>
 #include <cuda_runtime.h>
 
@@ -32,7 +34,7 @@ constexpr int kRcTile = kRcThreads * kRcOut;      // outputs per CTA
 constexpr int kRcMaxNr = 8192;
 
 __global__ void __launch_bounds__(kRcThreads) rc_direct_kernel(const float2* __restrict__ raw, int Ns,
-                                                               const float2* __restrict__ rep, int Nr,
+                                                               const float2* __restrict__ rep, int Nr, int lag0,
                                                                float2* __restrict__ out) {
   extern __shared__ float2 sm[];
   float2* sr = sm;            // replica [Nr], conjugated
@@ -46,8 +48,8 @@ __global__ void __launch_bounds__(kRcThreads) rc_direct_kernel(const float2* __r
   }
   const int span = kRcTile + Nr - 1;
   for (int i = threadIdx.x; i < span; i += kRcThreads) {
-    int n = n0 + i;
-    sx[i] = (n < Ns) ? x[n] : make_float2(0.f, 0.f);
+    const int n = n0 + lag0 + i;          // lag0 <= 0: the filter starts before lag 0 (whitening)
+    sx[i] = (n >= 0 && n < Ns) ? x[n] : make_float2(0.f, 0.f);
   }
   __syncthreads();
   float ar[kRcOut], ai[kRcOut];
@@ -193,7 +195,7 @@ __device__ __forceinline__ void fft_forward(float2 v[16], const float2* __restri
 #pragma unroll
   for (int r = 0; r < 16; ++r) {
     const int n = n0 + j + r * kFT;
-    v[r] = (n < Ns) ? __ldg(x + n) : make_float2(0.f, 0.f);
+    v[r] = ((unsigned)n < (unsigned)Ns) ? __ldg(x + n) : make_float2(0.f, 0.f);   // zero outside 0..Ns-1
   }
   pass_store<false, 1>(v, sm, tw, j);
   __syncthreads();
@@ -226,7 +228,7 @@ __global__ void __launch_bounds__(kFT) rc_prep_kernel(const float2* __restrict__
   for (int r = 0; r < 16; ++r) H[j + r * kFT] = make_float2(v[sig(r)].x * sc, -v[sig(r)].y * sc);
 }
 
-__global__ void __launch_bounds__(kFT, RC_MINB) rc_fft_kernel(const float2* __restrict__ raw, int Ns, int V,
+__global__ void __launch_bounds__(kFT, RC_MINB) rc_fft_kernel(const float2* __restrict__ raw, int Ns, int V, int lag0,
                                                         const float2* __restrict__ H, const float2* __restrict__ tw_g,
                                                         float2* __restrict__ out) {
   __shared__ float2 sm[kPad];
@@ -236,7 +238,7 @@ __global__ void __launch_bounds__(kFT, RC_MINB) rc_fft_kernel(const float2* __re
   const float2* x = raw + ch * Ns;
   const float2* tw = tw_g;
   float2 v[16];
-  fft_forward(v, x, n0, Ns, sm, tw, j);
+  fft_forward(v, x, n0 + lag0, Ns, sm, tw, j);
   // spectrum product in registers (slot sig(r) holds bin j + 256 r)
 #pragma unroll
   for (int r = 0; r < 16; ++r) v[sig(r)] = cmul(v[sig(r)], __ldg(H + j + r * kFT));
@@ -295,14 +297,14 @@ sas_status twiddles(float2** out, cudaStream_t st) {
 }  // namespace
 
 static sas_status rc_launch_direct(const float2* raw, long nch, int32_t Ns, const float2* rep, int32_t Nr, float2* out,
-                                   cudaStream_t st) {
+                                   cudaStream_t st, int lag0 = 0) {
   const size_t smem = sizeof(float2) * ((size_t)Nr + kRcTile + Nr - 1);
   cudaError_t e = cudaFuncSetAttribute(rc_direct_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return rc_cuda_fail("cudaFuncSetAttribute(rc_direct_kernel)", e);
   for (long c0 = 0; c0 < nch; c0 += 65535) {
     const unsigned n = (unsigned)((nch - c0) < 65535 ? (nch - c0) : 65535);
     dim3 grid((Ns + kRcTile - 1) / kRcTile, n);
-    rc_direct_kernel<<<grid, kRcThreads, smem, st>>>(raw + c0 * Ns, Ns, rep, Nr, out + c0 * Ns);
+    rc_direct_kernel<<<grid, kRcThreads, smem, st>>>(raw + c0 * Ns, Ns, rep, Nr, lag0, out + c0 * Ns);
     e = cudaGetLastError();
     if (e != cudaSuccess) return rc_cuda_fail("rc_direct_kernel launch", e);
   }
@@ -310,7 +312,7 @@ static sas_status rc_launch_direct(const float2* raw, long nch, int32_t Ns, cons
 }
 
 static sas_status rc_launch_fft(const float2* raw, long nch, int32_t Ns, const float2* rep, int32_t Nr, float2* out,
-                                cudaStream_t st) {
+                                cudaStream_t st, int lag0 = 0) {
   float2* tw = nullptr;
   sas_status s = twiddles(&tw, st);
   if (s != SAS_OK) return s;
@@ -323,7 +325,7 @@ static sas_status rc_launch_fft(const float2* raw, long nch, int32_t Ns, const f
   const unsigned blocks = (unsigned)((Ns + V - 1) / V);
   for (long c0 = 0; c0 < nch && e == cudaSuccess; c0 += 65535) {
     const unsigned n = (unsigned)((nch - c0) < 65535 ? (nch - c0) : 65535);
-    rc_fft_kernel<<<dim3(blocks, n), kFT, 0, st>>>(raw + c0 * Ns, Ns, V, H, tw, out + c0 * Ns);
+    rc_fft_kernel<<<dim3(blocks, n), kFT, 0, st>>>(raw + c0 * Ns, Ns, V, lag0, H, tw, out + c0 * Ns);
     e = cudaGetLastError();
   }
   cudaFreeAsync(H, st);
@@ -389,6 +391,278 @@ extern "C" sas_status sas_rangecompress(const float* raw, int32_t P, int32_t E, 
   }
   cudaStreamSynchronize(st);
   cudaFree(draw); cudaFree(dout); cudaFree(drep);
+  cudaStreamDestroy(st);
+  return rs;
+}
+
+// ---------------------------------------------------------------- spectral whitening (NEXT-4, R21)
+//
+// Eq. 9: G = h(1/(gamma mean P + P)) from the batch-mean M-point periodogram P (power
+// gain, max G = 1); applied as the M-tap frequency-sampling FIR of amplitude sqrt(G) composed with
+// the replica, q = conj(w) (x) r (Nr + M - 1 taps starting at lag 1 - M/2), so the whitened
+// compression is ONE K1 pass with a longer filter and a negative start lag (exactly the cascade
+// w * x then the matched filter: y[n] = sum_l x[n + l] conj(q[l])).
+//
+// Periodogram kernel: threads = (block slot, bin); each thread accumulates |X_b[k]|^2 over the
+// blocks its slot visits (direct M-point DFT from a shared twiddle table, M^2 complex MACs per
+// block); per-CTA partial sums go to a double accumulator with one atomic per bin.
+
+namespace {
+
+constexpr int kWhThreads = 256;
+constexpr int kWhMaxM = 256;
+
+__global__ void __launch_bounds__(kWhThreads) wh_periodogram_kernel(const float2* __restrict__ raw, int Ns, int M, int B,
+                                                                    long long items, double* __restrict__ Pacc) {
+  __shared__ float2 tw[kWhMaxM];
+  __shared__ float2 xs[kWhThreads];
+  __shared__ float red[kWhThreads];
+  const int slots = kWhThreads / M;          // blocks processed together (M <= 256)
+  const int s = threadIdx.x / M, k = threadIdx.x - (threadIdx.x / M) * M;
+  for (int i = threadIdx.x; i < M; i += kWhThreads) {
+    double sn, cs;
+    sincospi(-2.0 * i / M, &sn, &cs);
+    tw[i] = make_float2((float)cs, (float)sn);
+  }
+  float acc = 0.f;
+  for (long long it0 = (long long)blockIdx.x * slots; it0 < items; it0 += (long long)gridDim.x * slots) {
+    __syncthreads();
+    if (s < slots) {   // stage slot s's block: sample n = k of item it0 + s
+      const long long it = it0 + s;
+      float2 v = make_float2(0.f, 0.f);
+      if (it < items) {
+        const long long ch = it / B;
+        const int b = (int)(it - ch * B);
+        const int n = b * M + k;
+        if (n < Ns) v = __ldcs(raw + ch * (long long)Ns + n);
+      }
+      xs[s * M + k] = v;
+    }
+    __syncthreads();
+    if (s < slots && it0 + s < items) {
+      float re = 0.f, im = 0.f;
+      int idx = 0;
+      const float2* xb = xs + s * M;
+      for (int n = 0; n < M; ++n) {
+        const float2 w = tw[idx];
+        const float2 x = xb[n];
+        re = fmaf(x.x, w.x, fmaf(-x.y, w.y, re));
+        im = fmaf(x.x, w.y, fmaf(x.y, w.x, im));
+        idx += k;
+        if (idx >= M) idx -= M;
+      }
+      acc = fmaf(re, re, fmaf(im, im, acc));
+    }
+  }
+  red[threadIdx.x] = (s < slots) ? acc : 0.f;
+  __syncthreads();
+  if (threadIdx.x < M) {
+    double t = 0.0;
+    for (int q = 0; q < slots; ++q) t += (double)red[q * M + threadIdx.x];
+    atomicAdd(Pacc + threadIdx.x, t);
+  }
+}
+
+__global__ void __launch_bounds__(kWhThreads) wh_gain_kernel(const double* __restrict__ Pacc, int M, double items,
+                                                             double gamma, float* __restrict__ G) {
+  __shared__ double g[kWhMaxM];
+  __shared__ double mean_s, gmax_s;
+  __shared__ int bad;
+  if (threadIdx.x == 0) {
+    double m = 0.0;
+    for (int k = 0; k < M; ++k) m += Pacc[k] / items;
+    mean_s = m / M;
+    bad = 0;
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < M; k += kWhThreads) {
+    const double den = gamma * mean_s + Pacc[k] / items;
+    if (!(den > 0)) bad = 1;
+    g[k] = 1.0 / den;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double mx = 0.0;
+    for (int k = 0; k < M; ++k) mx = fmax(mx, g[k]);
+    gmax_s = mx;
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < M; k += kWhThreads) G[k] = bad ? __int_as_float(0x7fc00000) : (float)(g[k] / gmax_s);
+}
+
+// q[l'] = sum_i conj(w[i]) r[l' + l0 + i], l' = 0 .. Nr + M - 2, l0 = 1 - M + M/2;
+// w[i] = (1/M) sum_k sqrt(G[k]) exp(+j 2 pi k i / M), i = -M/2 .. M/2 - 1 (fp64)
+__global__ void __launch_bounds__(kWhThreads) wh_compose_kernel(const float2* __restrict__ rep, int Nr,
+                                                                const float* __restrict__ G, int M,
+                                                                float2* __restrict__ q) {
+  __shared__ double2 w[kWhMaxM];
+  const int i0 = -(M / 2);
+  for (int t = threadIdx.x; t < M; t += kWhThreads) {
+    const int i = i0 + t;
+    double re = 0.0, im = 0.0;
+    for (int k = 0; k < M; ++k) {
+      const int km = (int)((((long long)k * i) % M + M) % M);
+      double sn, cs;
+      sincospi(2.0 * km / M, &sn, &cs);
+      const double a = sqrt((double)G[k]);
+      re += a * cs;
+      im += a * sn;
+    }
+    w[t] = make_double2(re / M, im / M);
+  }
+  __syncthreads();
+  const int l0 = 1 - M + M / 2;
+  const int Nq = Nr + M - 1;
+  for (int lp = threadIdx.x; lp < Nq; lp += kWhThreads) {
+    const int l = lp + l0;
+    double re = 0.0, im = 0.0;
+    for (int t = 0; t < M; ++t) {
+      const int m = l + i0 + t;
+      if (m < 0 || m >= Nr) continue;
+      const float2 r = rep[m];
+      const double2 c = w[t];                     // conj(w) * r
+      re += c.x * r.x + c.y * r.y;
+      im += c.x * r.y - c.y * r.x;
+    }
+    q[lp] = make_float2((float)re, (float)im);
+  }
+}
+
+sas_status wh_check(long nch, int32_t Ns, int32_t M, double gamma) {
+  if (nch < 1 || Ns < 1) { sasbp_set_error("nch and Ns must be >= 1"); return SAS_E_INVALID; }
+  if (M < 1 || M > kWhMaxM || (M > 1 && (M & 1))) { sasbp_set_error("M must be 1 or even, <= 256"); return SAS_E_INVALID; }
+  if (!(gamma >= 0) || !std::isfinite(gamma)) { sasbp_set_error("gamma must be finite and >= 0"); return SAS_E_INVALID; }
+  return SAS_OK;
+}
+
+}  // namespace
+
+extern "C" sas_status sas_whitening_gain_device(const void* raw_dev, int32_t nch, int32_t Ns, int32_t M, double gamma,
+                                                float* G_dev, void* cuda_stream) {
+  sasbp_set_error("");
+  sas_status s = wh_check(nch, Ns, M, gamma);
+  if (s != SAS_OK) return s;
+  if (!raw_dev || !G_dev) { sasbp_set_error("NULL pointer"); return SAS_E_INVALID; }
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  const int B = Ns / M > 0 ? Ns / M : 1;
+  const long long items = (long long)nch * B;
+  double* Pacc = nullptr;
+  cudaError_t e = cudaMallocAsync(&Pacc, M * sizeof(double), st);
+  if (e != cudaSuccess) return rc_cuda_fail("cudaMallocAsync(P)", e);
+  e = cudaMemsetAsync(Pacc, 0, M * sizeof(double), st);
+  const int slots = kWhThreads / M;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  long long grid = (items + slots - 1) / slots;
+  grid = grid < (long long)sms * 8 ? grid : (long long)sms * 8;
+  if (e == cudaSuccess) {
+    wh_periodogram_kernel<<<(unsigned)grid, kWhThreads, 0, st>>>((const float2*)raw_dev, Ns, M, B, items, Pacc);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) {
+    wh_gain_kernel<<<1, kWhThreads, 0, st>>>(Pacc, M, (double)items, gamma, G_dev);
+    e = cudaGetLastError();
+  }
+  cudaFreeAsync(Pacc, st);
+  if (e != cudaSuccess) return rc_cuda_fail("whitening gain kernels", e);
+  return SAS_OK;
+}
+
+extern "C" sas_status sas_whitening_gain(const float* raw, int32_t nch, int32_t Ns, int32_t M, double gamma, float* G) {
+  sasbp_set_error("");
+  sas_status s = wh_check(nch, Ns, M, gamma);
+  if (s != SAS_OK) return s;
+  if (!raw || !G) { sasbp_set_error("NULL pointer"); return SAS_E_INVALID; }
+  const size_t n = (size_t)nch * Ns;
+  cudaStream_t st = nullptr;
+  cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  if (e != cudaSuccess) return rc_cuda_fail("cudaStreamCreate", e);
+  float2* draw = nullptr;
+  float* dG = nullptr;
+  sas_status rs = SAS_OK;
+  if (cudaMalloc(&draw, n * sizeof(float2)) != cudaSuccess || cudaMalloc(&dG, M * sizeof(float)) != cudaSuccess) {
+    sasbp_set_error("cudaMalloc failed in sas_whitening_gain");
+    rs = SAS_E_NOMEM;
+  }
+  if (rs == SAS_OK && (e = cudaMemcpyAsync(draw, raw, n * sizeof(float2), cudaMemcpyHostToDevice, st)) != cudaSuccess)
+    rs = rc_cuda_fail("H2D copy", e);
+  if (rs == SAS_OK) rs = sas_whitening_gain_device(draw, nch, Ns, M, gamma, dG, st);
+  if (rs == SAS_OK) {
+    e = cudaMemcpyAsync(G, dG, M * sizeof(float), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) rs = rc_cuda_fail("D2H copy", e);
+  }
+  if (rs == SAS_OK && !(G[0] == G[0])) { sasbp_set_error("all-zero batch: no spectrum to whiten"); rs = SAS_E_INVALID; }
+  cudaStreamSynchronize(st);
+  cudaFree(draw);
+  cudaFree(dG);
+  cudaStreamDestroy(st);
+  return rs;
+}
+
+extern "C" sas_status sas_rangecompress_whitened_device(const void* raw_dev, int32_t P, int32_t E, int32_t Ns,
+                                                        const void* replica_dev, int32_t Nr, const float* G_dev, int32_t M,
+                                                        void* out_dev, void* cuda_stream) {
+  sasbp_set_error("");
+  if (M < 1 || M > kWhMaxM || (M > 1 && (M & 1))) { sasbp_set_error("M must be 1 or even, <= 256"); return SAS_E_INVALID; }
+  const int Nq = Nr + M - 1;
+  sas_status s = rc_check(P, E, Ns, Nq);
+  if (s != SAS_OK) return s;
+  if (!raw_dev || !replica_dev || !G_dev || !out_dev) { sasbp_set_error("NULL pointer"); return SAS_E_INVALID; }
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  float2* q = nullptr;
+  cudaError_t e = cudaMallocAsync(&q, Nq * sizeof(float2), st);
+  if (e != cudaSuccess) return rc_cuda_fail("cudaMallocAsync(q)", e);
+  wh_compose_kernel<<<1, kWhThreads, 0, st>>>((const float2*)replica_dev, Nr, G_dev, M, q);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) { cudaFreeAsync(q, st); return rc_cuda_fail("wh_compose_kernel", e); }
+  const long nch = (long)P * E;
+  const int lag0 = 1 - M + M / 2;
+  const char* force = getenv("SASBP_RC_DIRECT");
+  if (Nq <= kL / 2 && !(force && force[0] == '1'))
+    s = rc_launch_fft((const float2*)raw_dev, nch, Ns, q, Nq, (float2*)out_dev, st, lag0);
+  else
+    s = rc_launch_direct((const float2*)raw_dev, nch, Ns, q, Nq, (float2*)out_dev, st, lag0);
+  cudaFreeAsync(q, st);
+  return s;
+}
+
+extern "C" sas_status sas_rangecompress_whitened(const float* raw, int32_t P, int32_t E, int32_t Ns, const float* replica,
+                                                 int32_t Nr, const float* G, int32_t M, float* out) {
+  sasbp_set_error("");
+  if (!raw || !replica || !G || !out) { sasbp_set_error("NULL pointer"); return SAS_E_INVALID; }
+  if (M < 1 || M > kWhMaxM || (M > 1 && (M & 1))) { sasbp_set_error("M must be 1 or even, <= 256"); return SAS_E_INVALID; }
+  sas_status s = rc_check(P, E, Ns, Nr + M - 1);
+  if (s != SAS_OK) return s;
+  for (int k = 0; k < M; ++k)
+    if (!(G[k] >= 0) || !std::isfinite(G[k])) { sasbp_set_error("G must be finite and >= 0"); return SAS_E_INVALID; }
+  const size_t n = (size_t)P * E * Ns;
+  float2 *draw = nullptr, *dout = nullptr, *drep = nullptr;
+  float* dG = nullptr;
+  cudaStream_t st = nullptr;
+  cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  if (e != cudaSuccess) return rc_cuda_fail("cudaStreamCreate", e);
+  sas_status rs = SAS_OK;
+  if (cudaMalloc(&draw, n * sizeof(float2)) != cudaSuccess || cudaMalloc(&dout, n * sizeof(float2)) != cudaSuccess ||
+      cudaMalloc(&drep, (size_t)Nr * sizeof(float2)) != cudaSuccess || cudaMalloc(&dG, (size_t)M * sizeof(float)) != cudaSuccess) {
+    sasbp_set_error("cudaMalloc failed in sas_rangecompress_whitened");
+    rs = SAS_E_NOMEM;
+  }
+  if (rs == SAS_OK) {
+    e = cudaMemcpyAsync(draw, raw, n * sizeof(float2), cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(drep, replica, (size_t)Nr * sizeof(float2), cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dG, G, (size_t)M * sizeof(float), cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) rs = rc_cuda_fail("H2D copy", e);
+  }
+  if (rs == SAS_OK) rs = sas_rangecompress_whitened_device(draw, P, E, Ns, drep, Nr, dG, M, dout, st);
+  if (rs == SAS_OK) {
+    e = cudaMemcpyAsync(out, dout, n * sizeof(float2), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) rs = rc_cuda_fail("D2H copy", e);
+  }
+  cudaStreamSynchronize(st);
+  cudaFree(draw); cudaFree(dout); cudaFree(drep); cudaFree(dG);
   cudaStreamDestroy(st);
   return rs;
 }

@@ -23,7 +23,9 @@ _NAMES = {0: "SAS_OK", -1: "SAS_E_INVALID", -2: "SAS_E_STATE", -3: "SAS_E_NOMEM"
 EXPORTS = ("sas_bp_create", "sas_bp_destroy", "sas_bp_set_pings", "sas_bp_set_pings_device", "sas_bp_form",
            "sas_bp_form_device", "sas_bp_count_terms", "sas_bp_workspace_bytes", "sas_rangecompress",
            "sas_rangecompress_device", "sas_last_error", "sas_version", "sas_bp_get_plan", "sas_bp_form_streamed", "sas_bp_set_beam", "sas_bp_set_motion", "sas_bp_set_medium",
-           "sas_bp_set_weighting", "sas_upsample", "sas_upsample_device", "sas_baseband", "sas_baseband_device")
+           "sas_bp_set_weighting", "sas_upsample", "sas_upsample_device", "sas_baseband", "sas_baseband_device",
+           "sas_whitening_gain", "sas_whitening_gain_device", "sas_rangecompress_whitened",
+           "sas_rangecompress_whitened_device")
 
 
 class SasError(RuntimeError):
@@ -83,6 +85,10 @@ def load_library(path: Optional[str] = None):
         "sas_bp_set_medium": ([vp, ctypes.c_double, ctypes.c_double], ctypes.c_int),
         "sas_bp_set_weighting": ([vp, i32], ctypes.c_int),
         "sas_upsample": ([f32p, i32, i32, i32, f32p], ctypes.c_int),
+        "sas_whitening_gain": ([f32p, i32, i32, i32, ctypes.c_double, f32p], ctypes.c_int),
+        "sas_whitening_gain_device": ([vp, i32, i32, i32, ctypes.c_double, vp, vp], ctypes.c_int),
+        "sas_rangecompress_whitened": ([f32p, i32, i32, i32, f32p, i32, f32p, i32, f32p], ctypes.c_int),
+        "sas_rangecompress_whitened_device": ([vp, i32, i32, i32, vp, i32, vp, i32, vp, vp], ctypes.c_int),
         "sas_upsample_device": ([vp, i32, i32, i32, vp, vp], ctypes.c_int),
         "sas_baseband": ([f32p, i32, i32, i32, ctypes.c_double, ctypes.c_double, f64p, f32p, i32, i32, i32, f32p],
                          ctypes.c_int),
@@ -389,4 +395,51 @@ def baseband_device(x, fs_in: float, fc: float, t0, h, D: int, out, stream=None)
     _check(lib.sas_baseband_device(_dev_ptr(x, x.numel() * 4), P, E, Nin, float(fs_in), float(fc),
                                    _ptr(t, ctypes.c_double), _ptr(hh, ctypes.c_float), hh.size, int(D), int(Nout),
                                    _dev_ptr(out, P * E * Nout * 8), _stream_ptr(stream)))
+    return out
+
+
+def whitening_gain(raw, M: int, gamma: float) -> np.ndarray:
+    """Eq. 9 whitening power gain G [M] (float32) of complex64 [..., Ns] (R21; GPU periodogram)."""
+    lib = load_library()
+    raw = np.ascontiguousarray(raw, dtype=np.complex64)
+    Ns = raw.shape[-1]
+    nch = raw.size // Ns
+    G = np.empty(int(M), dtype=np.float32)
+    f = lambda a: a.view(np.float32).ctypes.data_as(ctypes.POINTER(ctypes.c_float))
+    _check(lib.sas_whitening_gain(f(raw), nch, Ns, int(M), float(gamma), f(G)))
+    return G
+
+
+def whitening_gain_device(raw, M: int, gamma: float, G, stream=None):
+    """CUDA-tensor variant: G float32 [M] on the device (NaN for an all-zero batch)."""
+    lib = load_library()
+    Ns = raw.shape[-1]
+    _check(lib.sas_whitening_gain_device(_dev_ptr(raw, raw.numel() * 8), raw.numel() // Ns, Ns, int(M), float(gamma),
+                                         _dev_ptr(G, int(M) * 4), _stream_ptr(stream)))
+    return G
+
+
+def rangecompress_whitened(raw, replica, G) -> np.ndarray:
+    """Host whitened matched filter (R21 + R14): sqrt(G) frequency-sampling FIR, then the replica."""
+    lib = load_library()
+    raw = np.ascontiguousarray(raw, dtype=np.complex64)
+    rep = np.ascontiguousarray(replica, dtype=np.complex64).ravel()
+    g = np.ascontiguousarray(G, dtype=np.float32).ravel()
+    Ns = raw.shape[-1]
+    nch = raw.size // Ns
+    out = np.empty_like(raw)
+    f = lambda a: a.view(np.float32).ctypes.data_as(ctypes.POINTER(ctypes.c_float))
+    _check(lib.sas_rangecompress_whitened(f(raw), nch, 1, Ns, f(rep), rep.size, f(g), g.size, f(out)))
+    return out
+
+
+def rangecompress_whitened_device(raw, replica, G, out, stream=None):
+    """CUDA-tensor whitened matched filter (G a float32 CUDA tensor [M])."""
+    lib = load_library()
+    Ns = raw.shape[-1]
+    nch = raw.numel() // Ns
+    _check(lib.sas_rangecompress_whitened_device(_dev_ptr(raw, raw.numel() * 8), nch, 1, Ns,
+                                                 _dev_ptr(replica, replica.numel() * 8), replica.numel(),
+                                                 _dev_ptr(G, G.numel() * 4), G.numel(),
+                                                 _dev_ptr(out, raw.numel() * 8), _stream_ptr(stream)))
     return out

@@ -257,3 +257,61 @@ def test_baseband_tone_then_backproject_shape(bpmod):
     tm = t0 + np.arange(Nin // D) * D / fs_in
     inner = slice(16, Nin // D - 16)
     assert np.max(np.abs(y - a * np.exp(1j * (2 * np.pi * d * tm + th)))[inner]) <= 1e-2 * a
+
+
+# ------------------------------------------------------------------ R21 spectral whitening
+
+def _coloured(seed, nch=6, Ns=5000):
+    rng = np.random.default_rng(seed)
+    n = (rng.normal(size=(nch, Ns + 1)) + 1j * rng.normal(size=(nch, Ns + 1))) / np.sqrt(2)
+    return (n[:, 1:] + 0.8 * n[:, :-1]).astype(np.complex64)
+
+
+@pytest.mark.parametrize("M,gamma,Ns", [(1, 0.0, 100), (2, 0.0, 999), (32, 0.0, 5000), (64, 0.1, 3000),
+                                        (256, 1.0, 4096), (64, 0.0, 40)])
+def test_whitening_gain_vs_oracle(bpmod, M, gamma, Ns):
+    x = _coloured(M + Ns, Ns=Ns)
+    got = bpmod.whitening_gain(x, M, gamma)
+    ref, _ = oracle.whitening_gain(x, M, gamma)
+    assert np.max(np.abs(got - ref)) <= 2e-5
+
+
+def test_whitening_gain_errors(bpmod):
+    with pytest.raises(bpmod.SasError):
+        bpmod.whitening_gain(np.zeros((2, 128), dtype=np.complex64), 16, 0.0)
+    for M in (0, 3, 258):
+        with pytest.raises(bpmod.SasError):
+            bpmod.whitening_gain(np.ones((2, 128), dtype=np.complex64), M, 0.0)
+
+
+@pytest.mark.parametrize("M,Ns,Nr,path", [(32, 3000, 600, "fft"), (64, 10240, 600, "fft"), (2, 777, 160, "fft"),
+                                          (1, 500, 40, "fft"), (256, 5000, 1793, "fft"), (64, 3000, 600, "direct")])
+def test_rangecompress_whitened_vs_oracle(bpmod, M, Ns, Nr, path, monkeypatch):
+    """The composed single-pass K1 (filter conj(w) (x) r, start lag 1 - M/2) equals the oracle's
+    cascade (whitening FIR, then the matched filter)."""
+    if path == "direct":
+        monkeypatch.setenv("SASBP_RC_DIRECT", "1")
+    x = _coloured(Ns + M, nch=4, Ns=Ns)
+    rng = np.random.default_rng(Nr)
+    rep = ((rng.normal(size=Nr) + 1j * rng.normal(size=Nr)) / np.sqrt(2 * Nr)).astype(np.complex64)
+    G, _ = oracle.whitening_gain(x, M, 0.05)
+    got = bpmod.rangecompress_whitened(x, rep, G.astype(np.float32))
+    ref = oracle.rangecompress_whitened(x, rep, G.astype(np.float32).astype(np.float64))
+    assert np.max(np.abs(got - ref)) <= 2e-5 * np.max(np.abs(ref))
+
+
+def test_whitening_device_chain(bpmod):
+    """Device pipeline: gain estimated on the GPU feeds the whitened compression on the GPU."""
+    import torch
+    x = _coloured(9, nch=8, Ns=4096)
+    rep = np.exp(1j * np.linspace(0, 20, 100) ** 2 / 20).astype(np.complex64) / np.float32(10)
+    xd = torch.from_numpy(x).cuda()
+    G = torch.empty(64, dtype=torch.float32, device="cuda")
+    bpmod.whitening_gain_device(xd, 64, 0.0, G)
+    out = torch.empty_like(xd)
+    bpmod.rangecompress_whitened_device(xd, torch.from_numpy(rep).cuda(), G, out)
+    torch.cuda.synchronize()
+    Gh = G.cpu().numpy()
+    ref = oracle.rangecompress_whitened(x, rep, Gh.astype(np.float64))
+    got = out.cpu().numpy()
+    assert np.max(np.abs(got - ref)) <= 2e-5 * np.max(np.abs(ref))
