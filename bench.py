@@ -352,11 +352,11 @@ def run_sasbp(args):
         rep = np.exp(1j * np.pi * (Br / Tp) * tt ** 2).astype(np.complex64)
         rep_d = torch.from_numpy(rep / np.float32(np.sqrt(nr))).to(dev)
         out_d = torch.empty_like(echoes_d)
-        for _ in range(2):
+        for _ in range(10):
             pkg.rangecompress_device(echoes_d, rep_d, out_d, stream=stream)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        nrep = 5
+        nrep = 20
         e0.record(stream)
         for _ in range(nrep):
             pkg.rangecompress_device(echoes_d, rep_d, out_d, stream=stream)
@@ -377,7 +377,7 @@ def run_sasbp(args):
     next4 = None
     if not args.no_next4 and rank == 0 and world == 1:
         def _time(fn, nrep):
-            for _ in range(2):
+            for _ in range(3):
                 fn()
             torch.cuda.synchronize()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

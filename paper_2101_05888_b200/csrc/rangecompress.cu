@@ -463,6 +463,172 @@ __global__ void __launch_bounds__(kWhThreads) wh_periodogram_kernel(const float2
   }
 }
 
+// Power-of-two M: radix-2 FFT per block in shared memory instead of the direct DFT.  A CTA takes
+// 512 / M blocks per iteration; inputs land bit-reversed, log2 M in-place butterfly stages follow
+// (thread = (block, butterfly t)), and thread (block, t) then holds bins t and t + M/2 of its
+// block -- the same two bins every iteration, accumulated in registers.
+__global__ void __launch_bounds__(kWhThreads) wh_periodogram_fft_kernel(const float2* __restrict__ raw, int Ns, int M,
+                                                                        int logM, int B, long long items,
+                                                                        double* __restrict__ Pacc) {
+  __shared__ float2 tw[kWhMaxM / 2];
+  __shared__ float2 xs[2 * kWhThreads];
+  __shared__ float red[2 * kWhThreads];
+  const int H = M >> 1;                       // butterflies per block
+  const int nb = (2 * kWhThreads) / M;        // blocks per iteration
+  const int blk = threadIdx.x / H, t = threadIdx.x - (threadIdx.x / H) * H;
+  for (int i = threadIdx.x; i < H; i += kWhThreads) {
+    double sn, cs;
+    sincospi(-2.0 * i / M, &sn, &cs);
+    tw[i] = make_float2((float)cs, (float)sn);
+  }
+  float a0 = 0.f, a1 = 0.f;
+  for (long long it0 = (long long)blockIdx.x * nb; it0 < items; it0 += (long long)gridDim.x * nb) {
+    __syncthreads();
+    // load: element n of block slot s goes to position bitrev(n)
+    for (int i = threadIdx.x; i < 2 * kWhThreads; i += kWhThreads) {
+      const int s = i / M, n = i - (i / M) * M;
+      const long long it = it0 + s;
+      float2 v = make_float2(0.f, 0.f);
+      if (it < items) {
+        const long long ch = it / B;
+        const int b = (int)(it - ch * B);
+        const int idx = b * M + n;
+        if (idx < Ns) v = __ldcs(raw + ch * (long long)Ns + idx);
+      }
+      xs[s * M + (int)(__brev((unsigned)n) >> (32 - logM))] = v;
+    }
+    __syncthreads();
+    float2* xb = xs + blk * M;
+    for (int half = 1, st = H; half < M; half <<= 1, st >>= 1) {   // twiddle stride st = M / (2 half)
+      const int pos = t & (half - 1);
+      const int i = ((t - pos) << 1) + pos, j = i + half;
+      const float2 w = tw[pos * st];
+      const float2 b = xb[j];
+      const float2 bw = make_float2(fmaf(b.x, w.x, -b.y * w.y), fmaf(b.x, w.y, b.y * w.x));
+      const float2 a = xb[i];
+      xb[i] = make_float2(a.x + bw.x, a.y + bw.y);
+      xb[j] = make_float2(a.x - bw.x, a.y - bw.y);
+      __syncthreads();
+    }
+    if (it0 + blk < items) {
+      const float2 u = xb[t], v = xb[t + H];
+      a0 = fmaf(u.x, u.x, fmaf(u.y, u.y, a0));
+      a1 = fmaf(v.x, v.x, fmaf(v.y, v.y, a1));
+    }
+  }
+  red[2 * threadIdx.x] = a0;       // bin t
+  red[2 * threadIdx.x + 1] = a1;   // bin t + H
+  __syncthreads();
+  if (threadIdx.x < M) {
+    const int k = threadIdx.x, tt = k < H ? k : k - H, which = k < H ? 0 : 1;
+    double s = 0.0;
+    for (int q = 0; q < nb; ++q) s += (double)red[2 * (q * H + tt) + which];
+    atomicAdd(Pacc + k, s);
+  }
+}
+
+// M = 16 R (R = 1, 2, 4, 8, 16): register-resident FFT, R lanes per block.  Lane r of a group loads
+// x[R i + r], i = 0..15 (the group reads 16 R contiguous samples per load step), does the 16-point
+// DFT in registers (dft16), multiplies by W_M^{r k1}, and the groups transpose through shared
+// memory so lane r finishes the S = 16/R length-R DFTs over r for k1 = r S .. r S + S - 1:
+// X[k1 + 16 k2] = sum_r W_R^{r k2} W_M^{r k1} Y_r[k1].  Each lane then always holds the same 16
+// bins, accumulated in registers across blocks; no barriers inside the loop.
+template <int R>
+__device__ __forceinline__ void dftR(float2 (&z)[R]) {
+  if constexpr (R == 2) {
+    const float2 a = z[0], b = z[1];
+    z[0] = make_float2(a.x + b.x, a.y + b.y);
+    z[1] = make_float2(a.x - b.x, a.y - b.y);
+  } else if constexpr (R == 4) {
+    dft4<false>(z[0], z[1], z[2], z[3]);
+  } else if constexpr (R == 8) {
+    // radix-2 x radix-4: n = 2 a + b; X[k] with k = c + 4 d
+    float2 e[4] = {z[0], z[2], z[4], z[6]}, o[4] = {z[1], z[3], z[5], z[7]};
+    dft4<false>(e[0], e[1], e[2], e[3]);
+    dft4<false>(o[0], o[1], o[2], o[3]);
+    const float r2 = 0.70710678118654752f;
+    const float2 w[4] = {make_float2(1.f, 0.f), make_float2(r2, -r2), make_float2(0.f, -1.f), make_float2(-r2, -r2)};
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const float2 t = cmul(o[c], w[c]);
+      z[c] = make_float2(e[c].x + t.x, e[c].y + t.y);
+      z[c + 4] = make_float2(e[c].x - t.x, e[c].y - t.y);
+    }
+  } else if constexpr (R == 16) {
+    float2 v[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = z[i];
+    dft16<false, false>(v);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) z[k] = v[sig(k)];
+  }
+}
+
+template <int R>
+__global__ void __launch_bounds__(kWhThreads) wh_periodogram_reg_kernel(const float2* __restrict__ raw, int Ns, int B,
+                                                                        long long items, double* __restrict__ Pacc) {
+  constexpr int M = 16 * R, S = 16 / R, G = kWhThreads / R;   // G blocks per CTA iteration
+  constexpr int GS = 17 * R;                                     // padded complex per group
+  __shared__ float2 T[G * GS];
+  __shared__ float red[M];
+  const int r = threadIdx.x % R, g = threadIdx.x / R;
+  for (int k = threadIdx.x; k < M; k += kWhThreads) red[k] = 0.f;
+  float2 w[16];   // W_M^{r k1}
+#pragma unroll
+  for (int k1 = 0; k1 < 16; ++k1) {
+    float sn, cs;
+    sincospif(-2.0f * (float)(r * k1) / (float)M, &sn, &cs);
+    w[k1] = make_float2(cs, sn);
+  }
+  float acc[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) acc[i] = 0.f;
+  for (long long it = (long long)blockIdx.x * G + g; it - g < items; it += (long long)gridDim.x * G) {
+    float2 v[16];
+    const bool live = it < items;
+    long long ch = 0;
+    int b = 0;
+    if (live) { ch = it / B; b = (int)(it - ch * B); }
+    const float2* xb = raw + ch * (long long)Ns + (long long)b * M;
+    const int nmax = live ? Ns - b * M : 0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int n = R * i + r;
+      v[i] = n < nmax ? __ldcs(xb + n) : make_float2(0.f, 0.f);
+    }
+    if constexpr (R == 1) {
+      dft16<false, false>(v);
+#pragma unroll
+      for (int k = 0; k < 16; ++k) acc[k] = fmaf(v[sig(k)].x, v[sig(k)].x, fmaf(v[sig(k)].y, v[sig(k)].y, acc[k]));
+    } else {
+      dft16<false, false>(v);
+      __syncwarp();
+      float2* Tg = T + g * GS;
+#pragma unroll
+      for (int k1 = 0; k1 < 16; ++k1) Tg[k1 * R + r] = cmul(v[sig(k1)], w[k1]);   // Z_r[k1]
+      __syncwarp();
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        float2 z[R];
+#pragma unroll
+        for (int q = 0; q < R; ++q) z[q] = Tg[(r * S + s) * R + q];
+        dftR<R>(z);
+#pragma unroll
+        for (int k2 = 0; k2 < R; ++k2) acc[s * R + k2] = fmaf(z[k2].x, z[k2].x, fmaf(z[k2].y, z[k2].y, acc[s * R + k2]));
+      }
+    }
+  }
+  // lane r holds bins k = k1 + 16 k2 with k1 = r S + s (slot s R + k2); R = 1: bin k in slot k
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int k = (R == 1) ? i : (r * S + i / R) + 16 * (i % R);
+    atomicAdd(red + k, acc[i]);
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < M; k += kWhThreads) atomicAdd(Pacc + k, (double)red[k]);
+}
+
 __global__ void __launch_bounds__(kWhThreads) wh_gain_kernel(const double* __restrict__ Pacc, int M, double items,
                                                              double gamma, float* __restrict__ G) {
   __shared__ double g[kWhMaxM];
@@ -556,7 +722,31 @@ extern "C" sas_status sas_whitening_gain_device(const void* raw_dev, int32_t nch
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   long long grid = (items + slots - 1) / slots;
   grid = grid < (long long)sms * 8 ? grid : (long long)sms * 8;
-  if (e == cudaSuccess) {
+  const bool pow2 = M >= 2 && (M & (M - 1)) == 0;
+  const char* force = getenv("SASBP_WH_DFT");
+  const char* force_rad2 = getenv("SASBP_WH_RADIX2");
+  if (e == cudaSuccess && pow2 && M >= 16 && !(force && force[0] == '1') && !(force_rad2 && force_rad2[0] == '1')) {
+    const int R = M / 16, Gb = kWhThreads / R;
+    long long g3 = (items + Gb - 1) / Gb;
+    g3 = g3 < (long long)sms * 8 ? g3 : (long long)sms * 8;
+    const float2* rp = (const float2*)raw_dev;
+    switch (R) {
+      case 1: wh_periodogram_reg_kernel<1><<<(unsigned)g3, kWhThreads, 0, st>>>(rp, Ns, B, items, Pacc); break;
+      case 2: wh_periodogram_reg_kernel<2><<<(unsigned)g3, kWhThreads, 0, st>>>(rp, Ns, B, items, Pacc); break;
+      case 4: wh_periodogram_reg_kernel<4><<<(unsigned)g3, kWhThreads, 0, st>>>(rp, Ns, B, items, Pacc); break;
+      case 8: wh_periodogram_reg_kernel<8><<<(unsigned)g3, kWhThreads, 0, st>>>(rp, Ns, B, items, Pacc); break;
+      default: wh_periodogram_reg_kernel<16><<<(unsigned)g3, kWhThreads, 0, st>>>(rp, Ns, B, items, Pacc); break;
+    }
+    e = cudaGetLastError();
+  } else if (e == cudaSuccess && pow2 && !(force && force[0] == '1')) {
+    const int nb = 2 * kWhThreads / M;
+    long long g2 = (items + nb - 1) / nb;
+    g2 = g2 < (long long)sms * 8 ? g2 : (long long)sms * 8;
+    int logM = 0;
+    while ((1 << logM) < M) ++logM;
+    wh_periodogram_fft_kernel<<<(unsigned)g2, kWhThreads, 0, st>>>((const float2*)raw_dev, Ns, M, logM, B, items, Pacc);
+    e = cudaGetLastError();
+  } else if (e == cudaSuccess) {
     wh_periodogram_kernel<<<(unsigned)grid, kWhThreads, 0, st>>>((const float2*)raw_dev, Ns, M, B, items, Pacc);
     e = cudaGetLastError();
   }

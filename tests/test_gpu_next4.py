@@ -268,8 +268,16 @@ def _coloured(seed, nch=6, Ns=5000):
 
 
 @pytest.mark.parametrize("M,gamma,Ns", [(1, 0.0, 100), (2, 0.0, 999), (32, 0.0, 5000), (64, 0.1, 3000),
-                                        (256, 1.0, 4096), (64, 0.0, 40)])
-def test_whitening_gain_vs_oracle(bpmod, M, gamma, Ns):
+                                        (256, 1.0, 4096), (64, 0.0, 40), (48, 0.2, 2000), (4, 0.0, 4099), (16, 0.0, 3001),
+                                        (128, 0.0, 1000)])
+@pytest.mark.parametrize("path", ["reg", "radix2", "dft"])
+def test_whitening_gain_vs_oracle(bpmod, M, gamma, Ns, path, monkeypatch):
+    """The three periodogram kernels: register FFT (M = 16 R), shared-memory radix-2 (power-of-two
+    M) and the direct DFT (any even M)."""
+    if path == "dft":
+        monkeypatch.setenv("SASBP_WH_DFT", "1")
+    if path == "radix2":
+        monkeypatch.setenv("SASBP_WH_RADIX2", "1")
     x = _coloured(M + Ns, Ns=Ns)
     got = bpmod.whitening_gain(x, M, gamma)
     ref, _ = oracle.whitening_gain(x, M, gamma)
