@@ -84,21 +84,46 @@ constexpr int kPad = kL + kL / 16;
 
 __device__ __forceinline__ int pad(int i) { return i + (i >> 4); }
 
+#ifndef RC_PAIRED
+#define RC_PAIRED 1   // complex arithmetic on the sm_100 paired FP32 path (FADD2 / FMUL2 / FFMA2)
+#endif
+
+// complex product; paired: a.x (b.x, b.y) + a.y (-b.y, b.x) -- FMUL2 + FFMA2 (+ one sign flip
+// unless b is a constant)
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+#if RC_PAIRED
+  return __ffma2_rn(make_float2(a.y, a.y), make_float2(-b.y, b.x), __fmul2_rn(make_float2(a.x, a.x), b));
+#else
   return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+#endif
+}
+
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) {
+#if RC_PAIRED
+  return __fadd2_rn(a, b);
+#else
+  return make_float2(a.x + b.x, a.y + b.y);
+#endif
+}
+__device__ __forceinline__ float2 csub(float2 a, float2 b) {
+#if RC_PAIRED
+  return __fadd2_rn(a, make_float2(-b.x, -b.y));
+#else
+  return make_float2(a.x - b.x, a.y - b.y);
+#endif
 }
 
 // radix-4 DFT in place; INV selects exp(+i) kernels
 template <bool INV>
 __device__ __forceinline__ void dft4(float2& x0, float2& x1, float2& x2, float2& x3) {
-  const float2 t0 = make_float2(x0.x + x2.x, x0.y + x2.y), t1 = make_float2(x0.x - x2.x, x0.y - x2.y);
-  const float2 t2 = make_float2(x1.x + x3.x, x1.y + x3.y);
-  const float2 d = make_float2(x1.x - x3.x, x1.y - x3.y);
+  const float2 t0 = cadd(x0, x2), t1 = csub(x0, x2);
+  const float2 t2 = cadd(x1, x3);
+  const float2 d = csub(x1, x3);
   const float2 t3 = INV ? make_float2(-d.y, d.x) : make_float2(d.y, -d.x);   // (+/- i) * d
-  x0 = make_float2(t0.x + t2.x, t0.y + t2.y);
-  x2 = make_float2(t0.x - t2.x, t0.y - t2.y);
-  x1 = make_float2(t1.x + t3.x, t1.y + t3.y);
-  x3 = make_float2(t1.x - t3.x, t1.y - t3.y);
+  x0 = cadd(t0, t2);
+  x2 = csub(t0, t2);
+  x1 = cadd(t1, t3);
+  x3 = csub(t1, t3);
 }
 
 // base-4 digit reversal of a 16-point index: sigma(4a + b) = 4b + a (an involution)
