@@ -167,6 +167,13 @@ def host_cpu_model():
 
 # ------------------------------------------------------------------ arms
 
+def workload_name(cid, s):
+    g = s.grid
+    kind = "3D volumetric" if g["nz"] > 1 else "2D stripmap"
+    return (f"BASELINE config {cid}: {s.name} {kind} {g['nx']}x{g['ny']}x{g['nz']} pixels, "
+            f"P={s.P} pings x E={s.E} elements x Ns={s.Ns} samples")
+
+
 def run_reference(args):
     """Reference arm: the fp64 CPU oracle (this tier has no reference implementation)."""
     rank = int(os.environ.get("RANK", "0"))
@@ -184,11 +191,11 @@ def run_reference(args):
             rates.append(last["value"])
     v = float(np.mean(rates))
     terms_per_step = s.dense_terms
-    out = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": 0, "steps": args.steps,
+    out = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": terms_per_step / (v * 1e9) * 1e3, "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": f"BASELINE config {args.config}: {s.name} {s.grid['nx']}x{s.grid['ny']}x{s.grid['nz']} "
-                                  f"P={s.P} E={s.E} Ns={s.Ns}", "sampled": True},
+           "config": {"workload": workload_name(args.config, s), "terms_per_step": terms_per_step,
+                      "parallelism": "host cores (oracle)", "sampled": True},
            "cpu_baseline": {"value": v, "unit": UNIT, "cores": last["cores"], "kind": "oracle",
                             "sample": "per step: " + last["sample"], "cpu_model": host_cpu_model()},
            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -454,8 +461,7 @@ def run_sasbp(args):
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded synth/ forward model)",
-            "config": {"workload": f"BASELINE config {args.config}: {s.name} 2D stripmap {g['nx']}x{g['ny']}x{g['nz']} "
-                                   f"pixels, P={P} pings x E={E} elements x Ns={Ns} samples",
+            "config": {"workload": workload_name(args.config, s),
                        "terms_per_step": dense, "parallelism": f"image-shard x{world}" if world > 1 else "single GPU",
                        "l2": f"inputs larger than L2 ({P * E * Ns * 8 / 1e9:.2f} GB echoes)"},
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": UNIT, "frac": achieved / peak,
