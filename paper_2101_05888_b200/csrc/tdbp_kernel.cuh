@@ -45,6 +45,14 @@ namespace sasbp {
 #ifndef SASBP_CUNROLL2
 #define SASBP_CUNROLL2 0
 #endif
+#ifndef SASBP_BININDEX
+// 1: the window cell index comes from the exponent-aligned window coordinate V = u - k_lo + 2^kb
+//    by integer ops (SHF + LOP3 + IADD3 on the ALU pipe); the phase and the lerp use the small
+//    tile-relative delay U' directly.  0: the original magic-number rounding (FADD2 + IMAD on the
+//    FMA pipe).  Both compute the same sum; A/B on config 2: 1271 (1) vs 1328 (0) Gterm/s, so 0 is
+//    the default (moving the index off the FMA pipe does not help: MUFU / latency bound).
+#define SASBP_BININDEX 0
+#endif
 #ifndef SASBP_TILE_GROUP
 #define SASBP_TILE_GROUP 8   // tiles per side of the square groups the launch order walks
 #endif
@@ -316,7 +324,11 @@ __device__ __forceinline__ ChanConst chan_prologue(const TdbpParams& prm, int ch
   const int Wh = prm.W >> 1;
   // window coordinate U = u - k_lo - 0.5 - Wh, so cell j = rn(U) + Wh
   const double urr = Uref - (double)(klo + Wh) - 0.5;
+#if SASBP_BININDEX
+  double ph = S * prm.k_c;                                    // reference phase (cycles) at U' = 0 (tau = tau_ref)
+#else
   double ph = fma(-urr, prm.k_r, S * prm.k_c);                // reference phase (cycles) at U = 0
+#endif
   ph -= floor(ph);
   ChanConst k;
   k.ux2 = (float)(2.0 * urx_m); k.uy2 = (float)(2.0 * ury_m); k.uz2 = (float)(2.0 * urz_m);
@@ -339,7 +351,11 @@ __device__ __forceinline__ ChanConst chan_prologue(const TdbpParams& prm, int ch
     k.a1 = (float)Ar; k.r_t = (float)At;
   }
   k.ping = p;
+#if SASBP_BININDEX
+  k.woff = (int)(win_base + (uint32_t)(slot * prm.W) * 16u);   // cell 0 of this channel's window
+#else
   k.woff = (int)(win_base + (uint32_t)(slot * prm.W + Wh) * 16u - (uint32_t)kMagicBits * 16u);
+#endif
   k.klo = klo;
   k.gate = gate_bits;
   return k;
@@ -482,6 +498,14 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
   const float kfs = (float)prm.k_s;
   // spreading weight (R18): w = R_tx R_rx = (r_t k_s + dU_tx)(r_r k_s + dU_rx) / k_s^2, in samples
   const float inv_ks2 = (float)(1.0 / (prm.k_s * prm.k_s));
+#if SASBP_BININDEX
+  // V = U' + urr + Wh + 0.5 + 2^kb = u - k_lo + 2^kb lies in the binade [2^kb, 2^(kb+1)) for every
+  // window coordinate u - k_lo in [0, W) (W <= 2^kb): the cell index floor(u - k_lo) is the top kb
+  // mantissa bits, and (bits >> (19 - kb)) & ((2^kb - 1) << 4) is already its byte offset (16 B cells)
+  const int vkb = 32 - __clz(max(prm.W - 1, 1));
+  const float voff = (float)(prm.W >> 1) + 0.5f + (float)(1 << vkb);
+  const uint32_t vsh = (uint32_t)(19 - vkb), vmask = ((1u << vkb) - 1u) << 4;
+#endif
   // refraction: interface height relative to the tile centre, slownesses in samples per metre
   const float zbr = MODE == kRefract ? (float)(prm.zb - ct[2]) : 0.f;
   const float k1r = (float)(prm.fs / prm.c), k2r = MODE == kRefract ? (float)(prm.fs / prm.c2) : 0.f;
@@ -599,7 +623,11 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
         const float2* rw = reinterpret_cast<const float2*>(rawp + c * rsb);
         const float2 d0 = rw[j], d1 = rw[j + 1];
         const float2 sl = __fadd2_rn(d1, make_float2(-d0.x, -d0.y));
+#if SASBP_BININDEX
+        const float2 ic = __ffma2_rn(sl, f2(0.5f - (float)(j - Wh) + cc[(b % kRing) * kNB + c].urr), d0);
+#else
         const float2 ic = __ffma2_rn(sl, f2(0.5f - (float)(j - Wh)), d0);
+#endif
         win[c * W + j] = make_float4(ic.x, ic.y, sl.x, sl.y);
       }
     }
@@ -619,7 +647,12 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
         const float2 d0 = make_float2(d01.x, d01.y), d1 = make_float2(d01.z, d01.w);
         const float2 s0 = __fadd2_rn(d1, make_float2(-d0.x, -d0.y));
         const float2 s1 = __fadd2_rn(d2, make_float2(-d1.x, -d1.y));
+#if SASBP_BININDEX
+        // the cells take the channel's fractional window offset: ehat = ic' + U' slope
+        const float j0 = (float)(Wh - 2 * t) + 0.5f + cc[(b % kRing) * kNB + c].urr;
+#else
         const float j0 = (float)(Wh - 2 * t) + 0.5f;
+#endif
         const float2 i0 = __ffma2_rn(s0, f2(j0), d0);
         const float2 i1 = __ffma2_rn(s1, f2(j0 - 1.0f), d1);
         float4* wc = win + c * W + 2 * t;
@@ -694,6 +727,9 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
         }
         masked = (kc.gate & 3) == kGEdge || ((kc.gate >> 2) & 3) == kGEdge;   // warp-uniform
       }
+#if SASBP_BININDEX
+      const float urrv = kc.urr + voff;                            // V = U' + urrv
+#endif
       const float rtk = WEIGHT ? kc.r_t * kfs : 0.f;               // r_t, r_r in samples
       const float rrk = WEIGHT ? kc.r_r * kfs * inv_ks2 : 0.f;
 #pragma unroll
@@ -737,6 +773,15 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
             U = __ffma2_rn(q, h, BT[p]);
           }
         }
+#if SASBP_BININDEX
+        if (MOTION) {   // moving receiver: U' = dU / (1 + w.v/c) ~ dU (kap0 + kg.d)
+          float2 kap = __ffma2_rn(f2(kc.kgy), DY[p], f2(kc.kap0));
+          kap = __ffma2_rn(f2(kc.kgx), DX[p], kap);
+          if (HAS_DZ) kap = __ffma2_rn(f2(kc.kgz), DZ[p], kap);
+          U = __fmul2_rn(U, kap);
+        }
+        const float2 T = __fadd2_rn(U, f2(urrv));            // exponent-aligned window coordinate V
+#else
         if (MOTION) {   // moving receiver: U = dU / (1 + w.v/c) ~ dU (kap0 + kg.d) + urr
           float2 kap = __ffma2_rn(f2(kc.kgy), DY[p], f2(kc.kap0));
           kap = __ffma2_rn(f2(kc.kgx), DX[p], kap);
@@ -746,13 +791,18 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
           U = __fadd2_rn(U, f2(kc.urr));                     // centred window coordinate
         }
         const float2 T = __fadd2_rn(U, f2(kMagic));          // rn(U) in the mantissa
+#endif
         const float2 ph = __ffma2_rn(U, f2(kph), f2(kc.phi0));
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
           const float Us = s ? U.y : U.x;
           const float Ts = s ? T.y : T.x;
           const float phs = s ? ph.y : ph.x;
+#if SASBP_BININDEX
+          uint32_t addr = ((uint32_t)__float_as_int(Ts) >> vsh & vmask) + (uint32_t)kc.woff;
+#else
           uint32_t addr = (uint32_t)__float_as_int(Ts) * 16u + (uint32_t)kc.woff;
+#endif
           if (GATE && masked) {   // gated-out pixel: read the zero cell
             const uint32_t mk = 0u - ((msk >> (2 * p + s)) & 1u);
             addr = (addr & mk) | (zcell & ~mk);
