@@ -190,11 +190,13 @@ __device__ __forceinline__ void bb_block(float2 (&acc)[kBbR], const float2 (&wa)
   }
 }
 
+template <int DT>   // DT = decimation at compile time (2, 4, 8: loops unrolled, all loads in flight), 0 = runtime
 __global__ void __launch_bounds__(256) baseband_blocked_kernel(const float* __restrict__ x, int E, int Nin, double kr,
                                                                const double* __restrict__ base,
-                                                               const float2* __restrict__ hq_g, int Nh, int D, int Apad,
+                                                               const float2* __restrict__ hq_g, int Nh, int D_rt, int Apad,
                                                                int Nout, int MO, long long runs, float2 rot1,
                                                                float2* __restrict__ out) {
+  const int D = DT ? DT : D_rt;
   extern __shared__ __align__(16) unsigned char bb_smem[];
   float2* hs = reinterpret_cast<float2*>(bb_smem);            // [D][Apad] (h, h)
   float2* sz = hs + (size_t)D * Apad;                          // [D][LqP] padded polyphase input
@@ -214,54 +216,84 @@ __global__ void __launch_bounds__(256) baseband_blocked_kernel(const float* __re
   // every 8 phases, so the error stays ~8 fp32 ulps.  No integer division anywhere.
   constexpr int kU = 8;
   const float2 rot = rot1;
-  for (int k0 = threadIdx.x; k0 < Lq; k0 += kU * blockDim.x) {
+  // full groups of kU slots per thread (unrolled, 8 loads in flight), then the Apad-slot tail.
+  // Slot k0 + u B (B = blockDim) of phase q is sample nlo + (k0 + u B) D + q; its padded shared
+  // position is bb_pad(k0) + u (B + B/8) (B is a multiple of 8).  Paired FP32 for the phasor
+  // rotation (w <- w rot) and the mix (v w).
+  const int Lfull = (Lq / (kU * (int)blockDim.x)) * (kU * (int)blockDim.x);
+  const int Bd = blockDim.x;
+  const float2 rotp = make_float2(-rot.y, rot.x);
+  const bool interior = nlo >= 0 && nlo + Lq * D <= Nin;   // no bounds checks needed (CTA-uniform)
+  for (int k0 = threadIdx.x; k0 < Lfull; k0 += kU * Bd) {
     float2 w[kU];
-    for (int q = 0; q < D; ++q) {
-      float v[kU];
+    const float* xk = xc + nlo + k0 * D;
+    float2* sk = sz + bb_pad(k0);
 #pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        const int k = k0 + u * blockDim.x;
-        const int n = nlo + k * D + q;
-        v[u] = (k < Lq && n >= 0 && n < Nin) ? __ldcs(xc + n) : 0.f;
+    for (int q = 0; q < (DT ? DT : D); ++q) {
+      float v[kU];
+      if (interior) {
+#pragma unroll
+        for (int u = 0; u < kU; ++u) v[u] = __ldcs(xk + u * Bd * D + q);
+      } else {
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const int n = nlo + (k0 + u * Bd) * D + q;
+          v[u] = (n >= 0 && n < Nin) ? __ldcs(xc + n) : 0.f;
+        }
       }
       if ((q & 7) == 0) {
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
-          double ph = fma((double)(nlo + (k0 + u * (int)blockDim.x) * D + q), kr, bp);   // cycles, fp64
+          double ph = fma((double)(nlo + (k0 + u * Bd) * D + q), kr, bp);   // cycles, fp64
           ph -= rint(ph);
           __sincosf(-6.283185307179586f * (float)ph, &w[u].y, &w[u].x);
         }
       } else {
 #pragma unroll
-        for (int u = 0; u < kU; ++u)
-          w[u] = make_float2(fmaf(w[u].x, rot.x, -w[u].y * rot.y), fmaf(w[u].x, rot.y, w[u].y * rot.x));
+        for (int u = 0; u < kU; ++u) w[u] = __ffma2_rn(make_float2(w[u].y, w[u].y), rotp, __fmul2_rn(make_float2(w[u].x, w[u].x), rot));
       }
+      float2* sq = sk + q * LqP;
 #pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        const int k = k0 + u * blockDim.x;
-        if (k < Lq) sz[q * LqP + bb_pad(k)] = make_float2(v[u] * w[u].x, v[u] * w[u].y);
+      for (int u = 0; u < kU; ++u) sq[u * (Bd + (Bd >> 3))] = __fmul2_rn(make_float2(v[u], v[u]), w[u]);
+    }
+  }
+  for (int k = Lfull + threadIdx.x; k < Lq; k += blockDim.x) {
+    for (int q = 0; q < D; ++q) {
+      const int n = nlo + k * D + q;
+      float2 z = make_float2(0.f, 0.f);
+      if (n >= 0 && n < Nin) {
+        double ph = fma((double)n, kr, bp);
+        ph -= rint(ph);
+        float sn, cs;
+        __sincosf(-6.283185307179586f * (float)ph, &sn, &cs);
+        const float v = __ldcs(xc + n);
+        z = make_float2(v * cs, v * sn);
       }
+      sz[q * LqP + bb_pad(k)] = z;
     }
   }
   __syncthreads();
   const int t0 = threadIdx.x * kBbR;
-  if (m0 + t0 >= Nout) return;
+  if (t0 >= MO || m0 + t0 >= Nout) return;
   float2 acc[kBbR];
 #pragma unroll
   for (int r = 0; r < kBbR; ++r) acc[r] = make_float2(0.f, 0.f);
-  for (int q = 0; q < D; ++q) {
+#pragma unroll
+  for (int q = 0; q < (DT ? DT : D); ++q) {
     const float2* zq = sz + q * LqP;
     const float2* hq = hs + q * Apad;
     float2 wa[kBbR], wb[kBbR];
+    // t0 and ab are multiples of 8, so bb_pad(t0 + ab + r) = bb_pad(t0 + ab) + r for r < 8
+    const float2* z0 = zq + bb_pad(t0);
 #pragma unroll
-    for (int r = 0; r < kBbR; ++r) wa[r] = zq[bb_pad(t0 + r)];
-    for (int ab = 0; ab < Apad; ab += 16) {
+    for (int r = 0; r < kBbR; ++r) wa[r] = z0[r];
+    for (int ab = 0; ab < Apad; ab += 16, z0 += 18) {
 #pragma unroll
-      for (int r = 0; r < kBbR; ++r) wb[r] = zq[bb_pad(t0 + ab + 8 + r)];
+      for (int r = 0; r < kBbR; ++r) wb[r] = z0[9 + r];
       bb_block(acc, wa, wb, hq + ab);
       if (ab + 8 >= Apad) break;
 #pragma unroll
-      for (int r = 0; r < kBbR; ++r) wa[r] = zq[bb_pad(t0 + ab + 16 + r)];
+      for (int r = 0; r < kBbR; ++r) wa[r] = z0[18 + r];
       bb_block(acc, wb, wa, hq + ab + 8);
     }
   }
@@ -274,6 +306,12 @@ __global__ void __launch_bounds__(256) baseband_blocked_kernel(const float* __re
     for (int r = 0; r < kBbR; ++r)
       if (m0 + t0 + r < Nout) __stcs(yo + r, acc[r]);
   }
+}
+
+cudaError_t set_bb_smem(int D, size_t smem) {
+  auto kern = D == 2 ? baseband_blocked_kernel<2> : D == 4 ? baseband_blocked_kernel<4>
+            : D == 8 ? baseband_blocked_kernel<8> : baseband_blocked_kernel<0>;
+  return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
 
 }  // namespace
@@ -396,9 +434,11 @@ extern "C" sas_status sas_baseband_device(const void* x_dev, int32_t P, int32_t 
       e = cudaMemcpyAsync(dbase, base.data(), P * sizeof(double), cudaMemcpyHostToDevice, st);
       if (e == cudaSuccess) e = cudaMemcpyAsync(dhq, hq.data(), hq.size() * sizeof(float2), cudaMemcpyHostToDevice, st);
       if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(baseband_blocked_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        e = set_bb_smem(D, smem);
       if (e == cudaSuccess) {
-        baseband_blocked_kernel<<<(unsigned)blocks, threads, smem, st>>>(
+        auto kern = D == 2 ? baseband_blocked_kernel<2> : D == 4 ? baseband_blocked_kernel<4>
+                  : D == 8 ? baseband_blocked_kernel<8> : baseband_blocked_kernel<0>;
+        kern<<<(unsigned)blocks, threads, smem, st>>>(
             (const float*)x_dev, E, Nin, kr, dbase, dhq, Nh, D, Apad, Nout, MOb, runs,
             make_float2((float)std::cos(2.0 * 3.141592653589793 * kr), (float)-std::sin(2.0 * 3.141592653589793 * kr)),
             (float2*)out_dev);
