@@ -411,7 +411,9 @@ def run_sasbp(args):
         kk = np.arange(-31, 32)
         hbb = (2 * 0.1 * np.sinc(2 * 0.1 * kk) * (0.5 + 0.5 * np.cos(np.pi * kk / 32))).astype(np.float32)
         hbb *= np.float32(2.0 / hbb.sum())
-        bb_ms = _time(lambda: pkg.baseband_device(pb, 4 * s.fs, s.fc, s.t0, hbb, 4, bb_out, stream=stream), 5)
+        t0_d = torch.from_numpy(np.ascontiguousarray(s.t0, dtype=np.float64)).to(dev)
+        hbb_d = torch.from_numpy(hbb).to(dev)
+        bb_ms = _time(lambda: pkg.baseband_device(pb, 4 * s.fs, s.fc, t0_d, hbb_d, 4, bb_out, stream=stream), 5)
         bb_bytes = 4 * nch * nin + 8 * nch * Ns
         del pb, bb_out
         # whitening (R21): gain estimate (M = 64 periodogram over the whole batch) and the

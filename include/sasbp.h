@@ -280,10 +280,11 @@ SASBP_API sas_status sas_baseband(const float* x, int32_t P, int32_t E, int32_t 
                                   const double* t0, const float* h, int32_t Nh, int32_t D, int32_t Nout,
                                   float* out);
 
-/* Device-pointer variant of sas_baseband (x_dev, out_dev on the device; t0 and h stay HOST
- * arrays, copied), asynchronous on cuda_stream. */
+/* Device variant of sas_baseband: x_dev, t0_dev (fp64 [P] or NULL), h_dev (float [Nh]) and out_dev
+ * all on the device; fully asynchronous on cuda_stream (no host staging or allocation).  t0_dev and
+ * h_dev values are not validated (non-finite values propagate to the output). */
 SASBP_API sas_status sas_baseband_device(const void* x_dev, int32_t P, int32_t E, int32_t Nin, double fs_in,
-                                         double fc, const double* t0, const float* h, int32_t Nh, int32_t D,
+                                         double fc, const double* t0_dev, const float* h_dev, int32_t Nh, int32_t D,
                                          int32_t Nout, void* out_dev, void* cuda_stream);
 
 /* Thread-local message describing the last failure on this thread ("" if none). */

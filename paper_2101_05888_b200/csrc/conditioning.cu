@@ -113,8 +113,15 @@ constexpr int kBbThreads = 256;
 constexpr int kBbSmem = 48 * 1024;    // bytes of mixed input per CTA
 constexpr int kBbMaxNh = 1023;
 
+// carrier cycles at sample 0 of ping p, fc t0_p mod 1 (fp64; t0 == NULL -> 0)
+__device__ __forceinline__ double bb_base(const double* __restrict__ t0, long long p, double fc) {
+  if (!t0) return 0.0;
+  const double v = fc * t0[p];
+  return v - floor(v);
+}
+
 __global__ void __launch_bounds__(kBbThreads) baseband_kernel(const float* __restrict__ x, int E, int Nin, double kr,
-                                                              const double* __restrict__ base, const float* __restrict__ h,
+                                                              double fc, const double* __restrict__ t0, const float* __restrict__ h,
                                                               int Nh, int D, int Nout, int MO, long long runs,
                                                               float2* __restrict__ out) {
   extern __shared__ __align__(16) unsigned char bb_smem[];
@@ -129,7 +136,7 @@ __global__ void __launch_bounds__(kBbThreads) baseband_kernel(const float* __res
   const int span = (MO - 1) * D + Nh;
   const int Lq = (span + D - 1) / D;          // samples per phase
   const float* xc = x + ch * (long long)Nin;
-  const double bp = base[ch / E];             // fc t0_p mod 1 (cycles)
+  const double bp = bb_base(t0, ch / E, fc);  // fc t0_p mod 1 (cycles)
   for (int k = threadIdx.x; k < Nh; k += kBbThreads) sh[k] = h[k];
   for (int i = threadIdx.x; i < span; i += kBbThreads) {
     const int n = nlo + i;
@@ -192,8 +199,8 @@ __device__ __forceinline__ void bb_block(float2 (&acc)[kBbR], const float2 (&wa)
 
 template <int DT>   // DT = decimation at compile time (2, 4, 8: loops unrolled, all loads in flight), 0 = runtime
 __global__ void __launch_bounds__(256) baseband_blocked_kernel(const float* __restrict__ x, int E, int Nin, double kr,
-                                                               const double* __restrict__ base,
-                                                               const float2* __restrict__ hq_g, int Nh, int D_rt, int Apad,
+                                                               double fc, const double* __restrict__ t0p,
+                                                               const float* __restrict__ h, int Nh, int D_rt, int Apad,
                                                                int Nout, int MO, long long runs, float2 rot1,
                                                                float2* __restrict__ out) {
   const int D = DT ? DT : D_rt;
@@ -208,8 +215,12 @@ __global__ void __launch_bounds__(256) baseband_blocked_kernel(const float* __re
   const int Lq = MO + Apad;                     // samples per phase (+ slack for the last block)
   const int LqP = bb_pad(Lq) + 1;
   const float* xc = x + ch * (long long)Nin;
-  const double bp = base[ch / E];
-  for (int k = threadIdx.x; k < D * Apad; k += blockDim.x) hs[k] = hq_g[k];
+  const double bp = bb_base(t0p, ch / E, fc);
+  for (int k = threadIdx.x; k < D * Apad; k += blockDim.x) {   // hq[q][a] = h[Nh - 1 - (a D + q)], zero padded
+    const int q = k / Apad, a = k - q * Apad, j = a * D + q;
+    const float hv = j < Nh ? h[Nh - 1 - j] : 0.f;
+    hs[k] = make_float2(hv, hv);
+  }
   // Staging, phase-inner: thread k-slots k = k0 + u blockDim (8 in flight), samples n = nlo + k D + q.
   // The carrier phasor exp(-j 2 pi fc t_n) is evaluated exactly (fp64 reduction + sincos) at
   // q = 0 and advanced by the fp32 rotation exp(-j 2 pi fc / fs_in) for q = 1..D-1, re-anchored
@@ -374,81 +385,43 @@ extern "C" sas_status sas_upsample(const float* in, int32_t nch, int32_t Ns, int
   return rs;
 }
 
-extern "C" sas_status sas_baseband_device(const void* x_dev, int32_t P, int32_t E, int32_t Nin, double fs_in,
-                                          double fc, const double* t0, const float* h, int32_t Nh, int32_t D,
-                                          int32_t Nout, void* out_dev, void* cuda_stream) {
-  sasbp_set_error("");
-  if (P < 1 || E < 1 || Nin < 1 || Nout < 1 || D < 1) return cond_fail(SAS_E_INVALID, "P, E, Nin, Nout, D must be >= 1");
-  if (Nh < 1 || Nh > kBbMaxNh || (Nh % 2) == 0) return cond_fail(SAS_E_INVALID, "Nh must be odd and in 1..1023");
-  if (!(std::isfinite(fs_in) && fs_in > 0) || !(std::isfinite(fc) && fc > 0))
-    return cond_fail(SAS_E_INVALID, "fs_in and fc must be finite and > 0");
-  if (!x_dev || !h || !out_dev) return cond_fail(SAS_E_INVALID, "NULL pointer");
-  if ((((uintptr_t)x_dev) & 3) || (((uintptr_t)out_dev) & 7)) return cond_fail(SAS_E_INVALID, "misaligned pointer");
-  if ((long double)P * E * ((long double)Nin + Nout) > 4.0e15L) return cond_fail(SAS_E_INVALID, "sizes too large");
-  std::vector<double> base(P);
-  for (int32_t p = 0; p < P; ++p) {
-    const double tp = t0 ? t0[p] : 0.0;
-    if (!std::isfinite(tp)) return cond_fail(SAS_E_INVALID, "non-finite t0");
-    const double v = fc * tp;                 // carrier cycles at sample 0, reduced mod 1 in fp64
-    base[p] = v - std::floor(v);
-  }
-  for (int32_t k = 0; k < Nh; ++k)
-    if (!std::isfinite(h[k])) return cond_fail(SAS_E_INVALID, "non-finite FIR tap");
+// Fully asynchronous launch (all operands on the device): no host staging, no allocation.
+static sas_status bb_launch(const float* x, int32_t P, int32_t E, int32_t Nin, double fs_in, double fc, const double* t0,
+                            const float* h, int32_t Nh, int32_t D, int32_t Nout, float2* out, cudaStream_t st) {
   double kr = fc / fs_in;                     // cycles per input sample, mod 1
   kr -= std::floor(kr);
-  cudaStream_t st = (cudaStream_t)cuda_stream;
   // blocked polyphase kernel: 8 outputs per thread, threads = 256 / 128 / 64 / 32 so that the
   // padded polyphase arrays fit shared memory
-  {
-    const int A = (Nh + D - 1) / D;                  // taps per phase
-    const int Apad = (A + 7) & ~7;
-    int threads = 256;
-    size_t smem = 0;
-    for (; threads >= 32; threads >>= 1) {
-      const long long MOb = (long long)threads * kBbR;
-      const long long Lq = MOb + Apad;
-      const long long LqP = Lq + (Lq >> 3) + 1;
-      smem = ((size_t)D * Apad + (size_t)D * LqP) * sizeof(float2);
-      if (smem <= 200 * 1024) break;
+  const int A = (Nh + D - 1) / D;             // taps per phase
+  const int Apad = (A + 7) & ~7;
+  int threads = 256;
+  size_t smem = 0;
+  for (; threads >= 32; threads >>= 1) {
+    const long long MOb = (long long)threads * kBbR;
+    const long long Lq = MOb + Apad;
+    const long long LqP = Lq + (Lq >> 3) + 1;
+    smem = ((size_t)D * Apad + (size_t)D * LqP) * sizeof(float2);
+    if (smem <= 200 * 1024) break;
+  }
+  const char* force = getenv("SASBP_BB_SIMPLE");
+  cudaError_t e = cudaSuccess;
+  if (threads >= 32 && !(force && force[0] == '1')) {
+    const int MOb = threads * kBbR;
+    const long long runs = (Nout + MOb - 1) / MOb;
+    const long long blocks = runs * (long long)P * E;
+    if (blocks > 2147483647LL) return cond_fail(SAS_E_INVALID, "too many channels for one launch");
+    e = set_bb_smem(D, smem);
+    if (e == cudaSuccess) {
+      auto kern = D == 2 ? baseband_blocked_kernel<2> : D == 4 ? baseband_blocked_kernel<4>
+                : D == 8 ? baseband_blocked_kernel<8> : baseband_blocked_kernel<0>;
+      kern<<<(unsigned)blocks, threads, smem, st>>>(
+          x, E, Nin, kr, fc, t0, h, Nh, D, Apad, Nout, MOb, runs,
+          make_float2((float)std::cos(2.0 * 3.141592653589793 * kr), (float)-std::sin(2.0 * 3.141592653589793 * kr)),
+          out);
+      e = cudaGetLastError();
     }
-    const char* force = getenv("SASBP_BB_SIMPLE");
-    if (threads >= 32 && !(force && force[0] == '1')) {
-      const int MOb = threads * kBbR;
-      const long long runs = (Nout + MOb - 1) / MOb;
-      const long long blocks = runs * (long long)P * E;
-      if (blocks > 2147483647LL) return cond_fail(SAS_E_INVALID, "too many channels for one launch");
-      std::vector<float2> hq((size_t)D * Apad, make_float2(0.f, 0.f));
-      for (int q = 0; q < D; ++q)
-        for (int a = 0; a < Apad; ++a) {
-          const int j = a * D + q;
-          if (j < Nh) hq[(size_t)q * Apad + a] = make_float2(h[Nh - 1 - j], h[Nh - 1 - j]);
-        }
-      double* dbase = nullptr;
-      float2* dhq = nullptr;
-      cudaError_t e = cudaMallocAsync(&dbase, P * sizeof(double), st);
-      if (e == cudaSuccess) e = cudaMallocAsync(&dhq, hq.size() * sizeof(float2), st);
-      if (e != cudaSuccess) {
-        if (dbase) cudaFreeAsync(dbase, st);
-        return cond_fail(SAS_E_NOMEM, "cudaMallocAsync(baseband tables)", e);
-      }
-      e = cudaMemcpyAsync(dbase, base.data(), P * sizeof(double), cudaMemcpyHostToDevice, st);
-      if (e == cudaSuccess) e = cudaMemcpyAsync(dhq, hq.data(), hq.size() * sizeof(float2), cudaMemcpyHostToDevice, st);
-      if (e == cudaSuccess)
-        e = set_bb_smem(D, smem);
-      if (e == cudaSuccess) {
-        auto kern = D == 2 ? baseband_blocked_kernel<2> : D == 4 ? baseband_blocked_kernel<4>
-                  : D == 8 ? baseband_blocked_kernel<8> : baseband_blocked_kernel<0>;
-        kern<<<(unsigned)blocks, threads, smem, st>>>(
-            (const float*)x_dev, E, Nin, kr, dbase, dhq, Nh, D, Apad, Nout, MOb, runs,
-            make_float2((float)std::cos(2.0 * 3.141592653589793 * kr), (float)-std::sin(2.0 * 3.141592653589793 * kr)),
-            (float2*)out_dev);
-        e = cudaGetLastError();
-      }
-      cudaFreeAsync(dbase, st);
-      cudaFreeAsync(dhq, st);
-      if (e != cudaSuccess) return cond_fail(SAS_E_CUDA, "baseband_blocked_kernel", e);
-      return SAS_OK;
-    }
+    if (e != cudaSuccess) return cond_fail(SAS_E_CUDA, "baseband_blocked_kernel", e);
+    return SAS_OK;
   }
   // simple kernel (very large decimation): the mixed span (MO - 1) D + Nh fits kBbSmem bytes
   const int tap_bytes = ((Nh + 3) & ~3) * 4;
@@ -459,51 +432,71 @@ extern "C" sas_status sas_baseband_device(const void* x_dev, int32_t P, int32_t 
   MO = std::min<long long>(MO, Nout);
   const long long span = (MO - 1) * D + Nh;
   const long long Lq = (span + D - 1) / D;
-  const size_t smem = (size_t)tap_bytes + (size_t)D * Lq * 8;
+  const size_t smem2 = (size_t)tap_bytes + (size_t)D * Lq * 8;
   const long long runs = (Nout + MO - 1) / MO;
   const long long blocks = runs * (long long)P * E;
   if (blocks > 2147483647LL) return cond_fail(SAS_E_INVALID, "too many channels for one launch");
-  double* dbase = nullptr;
-  float* dh = nullptr;
-  cudaError_t e = cudaMallocAsync(&dbase, P * sizeof(double), st);
-  if (e == cudaSuccess) e = cudaMallocAsync(&dh, Nh * sizeof(float), st);
-  if (e != cudaSuccess) {
-    if (dbase) cudaFreeAsync(dbase, st);
-    return cond_fail(SAS_E_NOMEM, "cudaMallocAsync(baseband tables)", e);
-  }
-  e = cudaMemcpyAsync(dbase, base.data(), P * sizeof(double), cudaMemcpyHostToDevice, st);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(dh, h, Nh * sizeof(float), cudaMemcpyHostToDevice, st);
-  if (e == cudaSuccess && smem > 48 * 1024)
-    e = cudaFuncSetAttribute(baseband_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (smem2 > 48 * 1024) e = cudaFuncSetAttribute(baseband_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
   if (e == cudaSuccess) {
-    baseband_kernel<<<(unsigned)blocks, kBbThreads, smem, st>>>((const float*)x_dev, E, Nin, kr, dbase, dh, Nh, D, Nout,
-                                                                (int)MO, runs, (float2*)out_dev);
+    baseband_kernel<<<(unsigned)blocks, kBbThreads, smem2, st>>>(x, E, Nin, kr, fc, t0, h, Nh, D, Nout, (int)MO, runs, out);
     e = cudaGetLastError();
   }
-  // (pageable-source cudaMemcpyAsync has consumed the host vectors when it returns)
-  cudaFreeAsync(dbase, st);
-  cudaFreeAsync(dh, st);
   if (e != cudaSuccess) return cond_fail(SAS_E_CUDA, "baseband_kernel", e);
   return SAS_OK;
+}
+
+static sas_status bb_check(int32_t P, int32_t E, int32_t Nin, double fs_in, double fc, int32_t Nh, int32_t D,
+                           int32_t Nout) {
+  if (P < 1 || E < 1 || Nin < 1 || Nout < 1 || D < 1) return cond_fail(SAS_E_INVALID, "P, E, Nin, Nout, D must be >= 1");
+  if (Nh < 1 || Nh > kBbMaxNh || (Nh % 2) == 0) return cond_fail(SAS_E_INVALID, "Nh must be odd and in 1..1023");
+  if (!(std::isfinite(fs_in) && fs_in > 0) || !(std::isfinite(fc) && fc > 0))
+    return cond_fail(SAS_E_INVALID, "fs_in and fc must be finite and > 0");
+  if ((long double)P * E * ((long double)Nin + Nout) > 4.0e15L) return cond_fail(SAS_E_INVALID, "sizes too large");
+  return SAS_OK;
+}
+
+extern "C" sas_status sas_baseband_device(const void* x_dev, int32_t P, int32_t E, int32_t Nin, double fs_in,
+                                          double fc, const double* t0_dev, const float* h_dev, int32_t Nh, int32_t D,
+                                          int32_t Nout, void* out_dev, void* cuda_stream) {
+  sasbp_set_error("");
+  sas_status st = bb_check(P, E, Nin, fs_in, fc, Nh, D, Nout);
+  if (st != SAS_OK) return st;
+  if (!x_dev || !h_dev || !out_dev) return cond_fail(SAS_E_INVALID, "NULL pointer");
+  if ((((uintptr_t)x_dev) & 3) || (((uintptr_t)out_dev) & 7) || (((uintptr_t)t0_dev) & 7) || (((uintptr_t)h_dev) & 3))
+    return cond_fail(SAS_E_INVALID, "misaligned pointer");
+  return bb_launch((const float*)x_dev, P, E, Nin, fs_in, fc, t0_dev, h_dev, Nh, D, Nout, (float2*)out_dev,
+                   (cudaStream_t)cuda_stream);
 }
 
 extern "C" sas_status sas_baseband(const float* x, int32_t P, int32_t E, int32_t Nin, double fs_in, double fc,
                                    const double* t0, const float* h, int32_t Nh, int32_t D, int32_t Nout, float* out) {
   sasbp_set_error("");
   if (!x || !h || !out) return cond_fail(SAS_E_INVALID, "NULL pointer");
-  if (P < 1 || E < 1 || Nin < 1 || Nout < 1) return cond_fail(SAS_E_INVALID, "P, E, Nin, Nout must be >= 1");
+  sas_status rs = bb_check(P, E, Nin, fs_in, fc, Nh, D, Nout);
+  if (rs != SAS_OK) return rs;
+  for (int32_t k = 0; k < Nh; ++k)
+    if (!std::isfinite(h[k])) return cond_fail(SAS_E_INVALID, "non-finite FIR tap");
+  if (t0)
+    for (int32_t p = 0; p < P; ++p)
+      if (!std::isfinite(t0[p])) return cond_fail(SAS_E_INVALID, "non-finite t0");
   const size_t nin = (size_t)P * E * Nin, nout = (size_t)P * E * Nout;
   cudaStream_t st = nullptr;
   cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
   if (e != cudaSuccess) return cond_fail(SAS_E_CUDA, "cudaStreamCreate", e);
-  float* dx = nullptr;
+  float *dx = nullptr, *dh = nullptr;
+  double* dt0 = nullptr;
   float2* dout = nullptr;
-  sas_status rs = SAS_OK;
-  if (cudaMalloc(&dx, nin * sizeof(float)) != cudaSuccess || cudaMalloc(&dout, nout * sizeof(float2)) != cudaSuccess)
+  if (cudaMalloc(&dx, nin * sizeof(float)) != cudaSuccess || cudaMalloc(&dout, nout * sizeof(float2)) != cudaSuccess ||
+      cudaMalloc(&dh, (size_t)Nh * sizeof(float)) != cudaSuccess ||
+      (t0 && cudaMalloc(&dt0, (size_t)P * sizeof(double)) != cudaSuccess))
     rs = cond_fail(SAS_E_NOMEM, "cudaMalloc failed in sas_baseband");
-  if (rs == SAS_OK && (e = cudaMemcpyAsync(dx, x, nin * sizeof(float), cudaMemcpyHostToDevice, st)) != cudaSuccess)
-    rs = cond_fail(SAS_E_CUDA, "H2D copy", e);
-  if (rs == SAS_OK) rs = sas_baseband_device(dx, P, E, Nin, fs_in, fc, t0, h, Nh, D, Nout, dout, st);
+  if (rs == SAS_OK) {
+    e = cudaMemcpyAsync(dx, x, nin * sizeof(float), cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dh, h, (size_t)Nh * sizeof(float), cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess && t0) e = cudaMemcpyAsync(dt0, t0, (size_t)P * sizeof(double), cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) rs = cond_fail(SAS_E_CUDA, "H2D copy", e);
+  }
+  if (rs == SAS_OK) rs = bb_launch(dx, P, E, Nin, fs_in, fc, dt0, dh, Nh, D, Nout, dout, st);
   if (rs == SAS_OK) {
     e = cudaMemcpyAsync(out, dout, nout * sizeof(float2), cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
@@ -511,6 +504,8 @@ extern "C" sas_status sas_baseband(const float* x, int32_t P, int32_t E, int32_t
   }
   cudaStreamSynchronize(st);
   cudaFree(dx);
+  cudaFree(dh);
+  cudaFree(dt0);
   cudaFree(dout);
   cudaStreamDestroy(st);
   return rs;

@@ -92,7 +92,7 @@ def load_library(path: Optional[str] = None):
         "sas_upsample_device": ([vp, i32, i32, i32, vp, vp], ctypes.c_int),
         "sas_baseband": ([f32p, i32, i32, i32, ctypes.c_double, ctypes.c_double, f64p, f32p, i32, i32, i32, f32p],
                          ctypes.c_int),
-        "sas_baseband_device": ([vp, i32, i32, i32, ctypes.c_double, ctypes.c_double, f64p, f32p, i32, i32, i32, vp,
+        "sas_baseband_device": ([vp, i32, i32, i32, ctypes.c_double, ctypes.c_double, vp, vp, i32, i32, i32, vp,
                                  vp], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
@@ -387,13 +387,14 @@ def baseband(x, fs_in: float, fc: float, t0, h, D: int, Nout: int) -> np.ndarray
 
 
 def baseband_device(x, fs_in: float, fc: float, t0, h, D: int, out, stream=None):
-    """CUDA-tensor basebanding: float32 [P][E][Nin] -> out complex64 [P][E][Nout] (t0, h host)."""
+    """CUDA-tensor basebanding: float32 [P][E][Nin] -> out complex64 [P][E][Nout]; t0 (float64
+    [P] CUDA tensor or None) and h (float32 [Nh] CUDA tensor) on the device; asynchronous."""
     lib = load_library()
     P, E, Nin = x.shape
     Nout = out.shape[-1]
-    t, hh = _bb_args(t0, h, P)
-    _check(lib.sas_baseband_device(_dev_ptr(x, x.numel() * 4), P, E, Nin, float(fs_in), float(fc),
-                                   _ptr(t, ctypes.c_double), _ptr(hh, ctypes.c_float), hh.size, int(D), int(Nout),
+    t0p = None if t0 is None else _dev_ptr(t0, P * 8)
+    _check(lib.sas_baseband_device(_dev_ptr(x, x.numel() * 4), P, E, Nin, float(fs_in), float(fc), t0p,
+                                   _dev_ptr(h, h.numel() * 4), h.numel(), int(D), int(Nout),
                                    _dev_ptr(out, P * E * Nout * 8), _stream_ptr(stream)))
     return out
 

@@ -224,13 +224,28 @@ def test_baseband_vs_oracle(bpmod, P, E, Nin, D, Nh, Nout, path, monkeypatch):
     assert np.max(np.abs(got - ref)) <= TOL_FILT * max(np.max(np.abs(ref)), 1e-30) or np.max(np.abs(ref)) == 0
 
 
+def test_baseband_device_t0(bpmod):
+    """Device variant with a device t0 array (per-ping carrier phase computed on the GPU)."""
+    import torch
+    rng = np.random.default_rng(4)
+    x = rng.normal(size=(3, 2, 2048)).astype(np.float32)
+    h = 2.0 * _lowpass(16, 0.1)
+    t0 = np.array([0.0123, 0.0456, 0.0789])
+    out = torch.empty((3, 2, 512), dtype=torch.complex64, device="cuda")
+    bpmod.baseband_device(torch.from_numpy(x).cuda(), 480e3, 120e3 + 3.0, torch.from_numpy(t0).cuda(),
+                          torch.from_numpy(h).cuda(), 4, out)
+    torch.cuda.synchronize()
+    ref = oracle.baseband(x, 480e3, 120e3 + 3.0, t0, h, 4, 512)
+    assert np.max(np.abs(out.cpu().numpy() - ref)) <= TOL_FILT * np.max(np.abs(ref))
+
+
 def test_baseband_device_and_t0_none(bpmod):
     import torch
     rng = np.random.default_rng(3)
     x = rng.normal(size=(2, 3, 4096)).astype(np.float32)
     h = 2.0 * _lowpass(24, 0.1)
     out = torch.empty((2, 3, 1024), dtype=torch.complex64, device="cuda")
-    bpmod.baseband_device(torch.from_numpy(x).cuda(), 480e3, 120e3, None, h, 4, out)
+    bpmod.baseband_device(torch.from_numpy(x).cuda(), 480e3, 120e3, None, torch.from_numpy(h).cuda(), 4, out)
     torch.cuda.synchronize()
     ref = oracle.baseband(x, 480e3, 120e3, None, h, 4, 1024)
     assert np.max(np.abs(out.cpu().numpy() - ref)) <= TOL_FILT * np.max(np.abs(ref))
