@@ -216,12 +216,20 @@ def run_sasbp(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test plumbing only (never used for a reported number): run the multi-rank path with every
+    # rank on cuda:0 and gloo collectives, to exercise N > 1 on a one-GPU box
+    if os.environ.get("SASBP_SAME_DEVICE") == "1":
+        local = 0
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("SASBP_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     pkg.load_library()
 
     s = synth.scenario(args.config)
@@ -465,7 +473,9 @@ def run_sasbp(args):
             "data": "synthetic (seeded synth/ forward model)",
             "config": {"workload": workload_name(args.config, s),
                        "terms_per_step": dense, "parallelism": f"image-shard x{world}" if world > 1 else "single GPU",
-                       "l2": f"inputs larger than L2 ({P * E * Ns * 8 / 1e9:.2f} GB echoes)"},
+                       "l2": (f"inputs larger than L2 ({P * E * Ns * 8 / 1e9:.2f} GB echoes, 126 MB L2), no flush"
+                              if P * E * Ns * 8 > 126e6 else
+                              f"inputs SMALLER than L2 ({P * E * Ns * 8 / 1e6:.1f} MB): not a timing config")},
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": UNIT, "frac": achieved / peak,
                          "traffic": traffic,
                          "algorithmic_bytes": P * E * Ns * 8 + g["nx"] * g["ny"] * g["nz"] * 8,
