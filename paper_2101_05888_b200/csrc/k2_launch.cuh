@@ -110,9 +110,15 @@ cudaError_t k2_launch_3d_w(const TdbpParams& prm, const TmaDesc& tmap, const K2L
 #ifndef SASBP_WY2D
 #define SASBP_WY2D 4
 #endif
+#ifndef SASBP_KX2D
+#define SASBP_KX2D 4   // pixels per thread along x (even: x-adjacent pairs)
+#endif
+#ifndef SASBP_KY2D
+#define SASBP_KY2D 2   // pixels per thread along y
+#endif
 #if SASBP_K4
 #define SASBP_T2D 4, 1, 1, 8, 1
 #else
-#define SASBP_T2D 4, 2, 1, SASBP_WY2D, 1
+#define SASBP_T2D SASBP_KX2D, SASBP_KY2D, 1, SASBP_WY2D, 1
 #endif
 #define SASBP_T3D 2, 2, 2, 1, 4

@@ -317,7 +317,7 @@ sas_status sas_bp_create(double fc, double bandwidth, double fs, double c, const
   h->fc = fc; h->bandwidth = bandwidth; h->fs = fs; h->c = c;
   h->grid = g;
   const bool flat_z = (g.nz == 1) && g.step_x[2] == 0.0 && g.step_y[2] == 0.0;
-  if (g.nz == 1) { h->variant = flat_z ? V2D : V2D_DZ; h->TX = 32; h->TY = 8 * SASBP_WY2D; h->TZ = 1; }
+  if (g.nz == 1) { h->variant = flat_z ? V2D : V2D_DZ; h->TX = 8 * SASBP_KX2D; h->TY = 4 * SASBP_KY2D * SASBP_WY2D; h->TZ = 1; }
   else { h->variant = V3D; h->TX = 16; h->TY = 8; h->TZ = 8; }
   h->tiles_x = (g.nx + h->TX - 1) / h->TX;
   h->tiles_y = (g.ny + h->TY - 1) / h->TY;
