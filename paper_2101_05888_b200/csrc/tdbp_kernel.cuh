@@ -45,6 +45,9 @@ namespace sasbp {
 #ifndef SASBP_CUNROLL2
 #define SASBP_CUNROLL2 0
 #endif
+#ifndef SASBP_CC_LDS
+#define SASBP_CC_LDS 0   // A/B knob: channel constants via explicit ld.shared (see lds_struct)
+#endif
 #ifndef SASBP_BININDEX
 // 1: the window cell index comes from the exponent-aligned window coordinate V = u - k_lo + 2^kb
 //    by integer ops (SHF + LOP3 + IADD3 on the ALU pipe); the phase and the lerp use the small
@@ -119,6 +122,18 @@ constexpr int kMagicBits = 0x4B400000;
 __device__ __forceinline__ float4 lds128(uint32_t addr) {
   float4 v;
   asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
+}
+// ChanConst read through a 32-bit shared-window address (ld.shared): a generic pointer into dynamic
+// shared memory makes ptxas rematerialise its base with S2R SR_CgaCtaId inside the channel loop
+// under register pressure
+template <typename T>
+__device__ __forceinline__ T lds_struct(uint32_t addr) {
+  static_assert(sizeof(T) % 16 == 0, "16-byte multiple");
+  T v;
+  float4* p = reinterpret_cast<float4*>(&v);
+#pragma unroll
+  for (int i = 0; i < (int)(sizeof(T) / 16); ++i) p[i] = lds128(addr + 16u * i);
   return v;
 }
 __device__ __forceinline__ float rcp_approx(float x) {
@@ -667,6 +682,9 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
     if ((b + 2) % kGroup == 0) prologue_group(b + 2);   // batches b+2 .. b+1+kGroup (ring slots not in use)
     if (!live) continue;
     const ChanConst* cb = cc + (b % kRing) * kNB;
+#if SASBP_CC_LDS
+    const uint32_t cb_s = (uint32_t)__cvta_generic_to_shared(cc) + (uint32_t)((b % kRing) * kNB) * (uint32_t)sizeof(ChanConst);
+#endif
 
 #if SASBP_CUNROLL2
 #pragma unroll 2
@@ -674,7 +692,11 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
 #pragma unroll 1
 #endif
     for (int c = 0; c < nb; ++c) {
+#if SASBP_CC_LDS
+      const ChanConst kc = lds_struct<ChanConst>(cb_s + (uint32_t)c * (uint32_t)sizeof(ChanConst));
+#else
       const ChanConst kc = cb[c];
+#endif
       if (GATE && (kc.gate & 16)) continue;                 // culled: tile outside a cone
       if (kc.ping != cur_ping) {
         cur_ping = kc.ping;
