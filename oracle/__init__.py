@@ -99,6 +99,11 @@ def _load():
         lib.oracle_rangecompress_whitened.argtypes = [f32p, ctypes.c_int64, ctypes.c_int32, f32p, ctypes.c_int32,
                                                       f64p, ctypes.c_int32, f64p]
         lib.oracle_rangecompress_whitened.restype = ctypes.c_int
+        lib.oracle_tdbp_points_gated_weighted.argtypes = [f32p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                                          f64p, f64p, f64p, ctypes.c_double, ctypes.c_double,
+                                                          ctypes.c_double, f64p, ctypes.c_double, ctypes.c_double,
+                                                          ctypes.c_int32, f64p, ctypes.c_int64, f64p]
+        lib.oracle_tdbp_points_gated_weighted.restype = ctypes.c_int
         lib.oracle_num_threads.restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -289,6 +294,24 @@ def tdbp_points_weighted(echoes, tx, rx, t0, fc, fs, c, pts, with_count=False):
         raise ValueError("oracle_tdbp_points_weighted: invalid arguments")
     res = out[:, 0] + 1j * out[:, 1]
     return (res, cnt) if with_count else res
+
+
+def tdbp_points_gated_weighted(echoes, tx, rx, t0, fc, fs, c, pts, az, el=0.0, bistatic=False, axes=None):
+    """Gated (R15) and spreading-weighted (R18) TDBP at explicit points."""
+    lib = _load()
+    echoes, P, E, Ns, tx, rx, t0 = _echo_arrays(echoes, tx, rx, t0)
+    pts = np.ascontiguousarray(pts, dtype=np.float64).reshape(-1, 3)
+    ax = None if axes is None else np.ascontiguousarray(axes, dtype=np.float64).reshape(P, 2, 3)
+    N = pts.shape[0]
+    out = np.zeros((N, 2), dtype=np.float64)
+    rc = lib.oracle_tdbp_points_gated_weighted(_p(echoes, ctypes.c_float), P, E, Ns, _p(tx, ctypes.c_double),
+                                               _p(rx, ctypes.c_double), _p(t0, ctypes.c_double), float(fc), float(fs),
+                                               float(c), _p(ax, ctypes.c_double), float(az), float(el),
+                                               1 if bistatic else 0, _p(pts, ctypes.c_double), N,
+                                               _p(out, ctypes.c_double))
+    if rc != 0:
+        raise ValueError("oracle_tdbp_points_gated_weighted: invalid arguments")
+    return out[:, 0] + 1j * out[:, 1]
 
 
 def lanczos4(s) -> float:

@@ -587,6 +587,43 @@ int oracle_rangecompress_whitened(const float* raw, int64_t nch, int32_t Ns, con
   return 0;
 }
 
+/*
+ * Gated AND spreading-weighted TDBP (NEXT-1 gate R15 combined with the NEXT-4 weight R18): the
+ * gated sum of oracle_tdbp_points_gated with every admitted term multiplied by R_tx R_rx.
+ */
+int oracle_tdbp_points_gated_weighted(const float* echoes, int32_t P, int32_t E, int32_t Ns, const double* tx,
+                                      const double* rx, const double* t0, double fc, double fs, double c,
+                                      const double* axes, double az, double el, int32_t bistatic,
+                                      const double* pts, int64_t N, double* out) {
+  if (P < 1 || E < 1 || Ns < 1 || N < 0 || !(c > 0) || !(fs > 0)) return -1;
+  static const double def_a[3] = {1.0, 0.0, 0.0}, def_b[3] = {0.0, 1.0, 0.0};
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int64_t i = 0; i < N; ++i) {
+    const double* x = pts + 3 * i;
+    double ar = 0.0, ai = 0.0;
+    for (int32_t p = 0; p < P; ++p) {
+      const double* a = axes ? axes + 6 * p : def_a;
+      const double* b = axes ? axes + 6 * p + 3 : def_b;
+      if (!in_fov(x, tx + 3 * p, a, b, az, el)) continue;
+      const double t0p = t0 ? t0[p] : 0.0;
+      const double rt = dist3(x, tx + 3 * p);
+      for (int32_t e = 0; e < E; ++e) {
+        const double* r = rx + 3 * ((int64_t)p * E + e);
+        if (bistatic && !in_fov(x, r, a, b, az, el)) continue;
+        const float* ch = echoes + 2 * ((int64_t)p * E + e) * (int64_t)Ns;
+        const double rr = dist3(x, r);
+        double tr = 0.0, ti = 0.0;
+        one_term_tau(x, ch, Ns, (rt + rr) / c, t0p, fc, fs, &tr, &ti);
+        ar += rt * rr * tr;
+        ai += rt * rr * ti;
+      }
+    }
+    out[2 * i] = ar;
+    out[2 * i + 1] = ai;
+  }
+  return 0;
+}
+
 /* Number of OpenMP threads the oracle will use (for the cpu_baseline "cores"). */
 int oracle_num_threads(void) {
 #ifdef _OPENMP

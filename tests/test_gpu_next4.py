@@ -338,3 +338,20 @@ def test_whitening_device_chain(bpmod):
     ref = oracle.rangecompress_whitened(x, rep, Gh.astype(np.float64))
     got = out.cpu().numpy()
     assert np.max(np.abs(got - ref)) <= 2e-5 * np.max(np.abs(ref))
+
+
+@pytest.mark.parametrize("cid,bistatic", [(2, False), (3, True)])
+def test_weighted_gated_vs_oracle(bpmod, cid, bistatic):
+    """Gate (R15) and weight (R18) together: reduced configs with the generator's beam."""
+    s = synth.scenario(cid, reduced=True)
+    e = s.echoes()
+    az = 2 * float(np.arcsin(s.sin_half_beam))
+    with bpmod.Backprojector(s.fc, s.bandwidth, s.fs, s.c, s.grid) as bp:
+        bp.set_pings(e, s.tx, s.rx, s.t0)
+        bp.set_weighting(True)
+        bp.set_beam(az, 0.0, bistatic, True)
+        got = bp.form()
+    idx = _grid_idx(s.grid)
+    pts = oracle.grid_points(s.grid, idx)
+    ref = oracle.tdbp_points_gated_weighted(e, s.tx, s.rx, s.t0, s.fc, s.fs, s.c, pts, az=az, bistatic=bistatic)
+    _check(_at(got, idx), ref, label=f"weighted+gated {s.name}")

@@ -280,3 +280,22 @@ def test_whitening_flattens_coloured_noise():
     _, Pw = oracle.whitening_gain(xw, M, 0.0)
     assert (Pw.max() / Pw.min()) * 10 < P.max() / P.min()
     assert Pw.max() / Pw.min() < 3.0
+
+
+def test_gated_weighted_reduces_to_its_parts():
+    """The combined gate + weight: a wide-open beam equals the weighted sum; with weights the
+    gated sum of the config-1 target equals the in-beam count (as the weighted dense one, since the
+    generator's echoes carry only in-beam scatterer terms)."""
+    r = synth.random_case(9)
+    e = r["echoes"]
+    pts = oracle.grid_points(r["grid"])
+    a = oracle.tdbp_points_gated_weighted(e, r["tx"], r["rx"], r["t0"], r["fc"], r["fs"], r["c"], pts, az=4.0)
+    b = oracle.tdbp_points_weighted(e, r["tx"], r["rx"], r["t0"], r["fc"], r["fs"], r["c"], pts)
+    assert np.max(np.abs(a - b)) <= 1e-12 * np.max(np.abs(b))
+    s = synth.scenario(1)
+    e1 = s.echoes()
+    x = s.targets[0][None]
+    az = 2 * np.arcsin(s.sin_half_beam)
+    g = oracle.tdbp_points_gated_weighted(e1, s.tx, s.rx, s.t0, s.fc, s.fs, s.c, x, az=az)[0]
+    w = oracle.tdbp_points_weighted(e1, s.tx, s.rx, s.t0, s.fc, s.fs, s.c, x)[0]
+    assert abs(g - w) <= 1e-3 * abs(w)
