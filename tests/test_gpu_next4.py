@@ -355,3 +355,35 @@ def test_weighted_gated_vs_oracle(bpmod, cid, bistatic):
     pts = oracle.grid_points(s.grid, idx)
     ref = oracle.tdbp_points_gated_weighted(e, s.tx, s.rx, s.t0, s.fc, s.fs, s.c, pts, az=az, bistatic=bistatic)
     _check(_at(got, idx), ref, label=f"weighted+gated {s.name}")
+
+
+@pytest.mark.parametrize("how", ["odd_ns", "env"])
+def test_weighted_cp_async_path(bpmod, how, monkeypatch):
+    """The WEIGHT instantiation on the cp.async staging path (odd Ns, or SASBP_NO_TMA=1)."""
+    s = synth.scenario(2, reduced=True)
+    e = s.echoes()
+    if how == "odd_ns":
+        e = np.ascontiguousarray(e[:, :, :-1])
+    else:
+        monkeypatch.setenv("SASBP_NO_TMA", "1")
+    with bpmod.Backprojector(s.fc, s.bandwidth, s.fs, s.c, s.grid) as bp:
+        bp.set_pings(e, s.tx, s.rx, s.t0)
+        bp.set_weighting(True)
+        assert bp.plan()["tma"] is False
+        got = bp.form()
+    idx = _grid_idx(s.grid)
+    pts = oracle.grid_points(s.grid, idx)
+    ref = oracle.tdbp_points_weighted(e, s.tx, s.rx, s.t0, s.fc, s.fs, s.c, pts)
+    _check(_at(got, idx), ref, label=f"weighted cp.async {how}")
+
+
+def test_weighted_streamed_matches_form(bpmod):
+    """sas_bp_form_streamed (chunked H2D + accumulating launches) honours the weight."""
+    s = synth.scenario(2, reduced=True)
+    e = s.echoes()
+    with bpmod.Backprojector(s.fc, s.bandwidth, s.fs, s.c, s.grid) as bp:
+        bp.set_weighting(True)
+        a = bp.form_streamed(e, s.tx, s.rx, s.t0, chunks=3)
+        bp.set_pings(e, s.tx, s.rx, s.t0)
+        b = bp.form()
+    assert np.max(np.abs(a - b)) <= 1e-5 * np.max(np.abs(b))
