@@ -156,7 +156,7 @@ __device__ __forceinline__ void dft16(float2 v[16]) {
 #define RC_TW_RECUR 1
 #endif
 #ifndef RC_MINB
-#define RC_MINB 2
+#define RC_MINB 3   // 3 CTAs per SM: 80 registers (paired complex arithmetic), measured best of 2-4
 #endif
 // twiddle W_4096^m (forward sign) from the global table (L1 resident)
 __device__ __forceinline__ float2 twid(const float2* __restrict__ tw, int m) { return __ldg(tw + m); }
