@@ -589,22 +589,26 @@ __device__ __forceinline__ void dftR(float2 (&z)[R]) {
   }
 }
 
+#ifndef WH_MINB
+#define WH_MINB 3   // 3 CTAs per SM (72 registers, twiddles in shared memory): A/B best of 2-4 without spills
+#endif
 template <int R>
-__global__ void __launch_bounds__(kWhThreads) wh_periodogram_reg_kernel(const float2* __restrict__ raw, int Ns, int B,
+__global__ void __launch_bounds__(kWhThreads, WH_MINB) wh_periodogram_reg_kernel(const float2* __restrict__ raw, int Ns, int B,
                                                                         long long items, double* __restrict__ Pacc) {
   constexpr int M = 16 * R, S = 16 / R, G = kWhThreads / R;   // G blocks per CTA iteration
   constexpr int GS = 17 * R;                                     // padded complex per group
   __shared__ float2 T[G * GS];
   __shared__ float red[M];
+  __shared__ float2 wtab[R * 16];   // W_M^{r k1}, shared (frees 32 registers per thread)
   const int r = threadIdx.x % R, g = threadIdx.x / R;
   for (int k = threadIdx.x; k < M; k += kWhThreads) red[k] = 0.f;
-  float2 w[16];   // W_M^{r k1}
-#pragma unroll
-  for (int k1 = 0; k1 < 16; ++k1) {
+  for (int i = threadIdx.x; i < R * 16; i += kWhThreads) {
     float sn, cs;
-    sincospif(-2.0f * (float)(r * k1) / (float)M, &sn, &cs);
-    w[k1] = make_float2(cs, sn);
+    sincospif(-2.0f * (float)((i >> 4) * (i & 15)) / (float)M, &sn, &cs);
+    wtab[i] = make_float2(cs, sn);
   }
+  __syncthreads();
+  const float2* w = wtab + r * 16;
   float acc[16];
 #pragma unroll
   for (int i = 0; i < 16; ++i) acc[i] = 0.f;
