@@ -394,7 +394,13 @@ static sas_status bb_launch(const float* x, int32_t P, int32_t E, int32_t Nin, d
   // padded polyphase arrays fit shared memory
   const int A = (Nh + D - 1) / D;             // taps per phase
   const int Apad = (A + 7) & ~7;
-  int threads = 256;
+  // 128 threads (1024 outputs, ~37 KB of polyphase staging) per CTA: 6 CTAs/SM interleave their
+  // stage and FIR phases better than 3 of 256 (A/B on config 2: 3.17 vs 3.65 ms)
+  int threads = 128;
+  if (const char* tv = getenv("SASBP_BB_THREADS")) {   // A/B knob: CTA size of the blocked kernel
+    const int t = atoi(tv);
+    if (t == 32 || t == 64 || t == 128 || t == 256) threads = t;
+  }
   size_t smem = 0;
   for (; threads >= 32; threads >>= 1) {
     const long long MOb = (long long)threads * kBbR;
