@@ -3,7 +3,7 @@
  * synthetic aperture sonar, the data-parallel hot path of Gerg et al., "GPU Acceleration
  * for Synthetic Aperture Sonar Image Reconstruction" (arXiv 2101.05888).
  *
- * Citation key: P:n = PAPER.md line n; S:n = SPEC.md line n; R1..R14 = readings in DESIGN.md.
+ * Citation key: P:n = PAPER.md line n; S:n = SPEC.md line n; R1..R21 = readings in DESIGN.md.
  *
  * The operation (DESIGN.md §1 "Definition"): for every pixel / voxel centre
  *   x = origin + ix*step_x + iy*step_y + iz*step_z                                   (R8)

@@ -119,3 +119,16 @@ def test_product_has_no_oracle_dependency():
                 with open(os.path.join(dirpath, fn)) as f:
                     txt = f.read()
                 assert "import oracle" not in txt and "oracle/" not in txt and "liboracle" not in txt, fn
+
+
+def test_c_example_compiles_and_links_against_the_header():
+    """include/sasbp.h is plain C11 and libsasbp.so resolves every symbol a C program uses
+    (examples/c_smoke.c; it is run on the GPU by tests/test_c_example.py)."""
+    import subprocess
+    import tempfile
+    out = os.path.join(tempfile.mkdtemp(), "c_smoke")
+    r = subprocess.run(["gcc", "-std=c11", "-O2", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
+                        os.path.join(ROOT, "examples", "c_smoke.c"), "-L", os.path.join(ROOT, "paper_2101_05888_b200"),
+                        "-lsasbp", "-lm", "-Wl,-rpath," + os.path.join(ROOT, "paper_2101_05888_b200"), "-o", out],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
