@@ -146,6 +146,14 @@ __device__ __forceinline__ float rsqrt_approx(float x) {
   asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// Denominator sqrt(r^2 + q) + r of dR = q / (sqrt(r^2 + q) + r), safe when the pixel coincides
+// with the sensor: r^2 + q (which can round to 0 or slightly below there) is floored at 1e-30, so
+// sqrt = x rsqrt(x) >= 1e-15 > 0 and no 0 * inf or negative root arises (dR stays bounded by the
+// window; q / den -> 0 when the tile centre is on the sensor as well)
+__device__ __forceinline__ float leg_den(float r2, float r) {
+  const float r2c = fmaxf(r2, 1e-30f);
+  return fmaf(r2c, rsqrt_approx(r2c), r);
+}
 __device__ __forceinline__ void cp_async8(uint32_t dst, const void* src, bool valid) {
   // 8-byte global -> shared copy; src-size 0 writes zeros (zero extension, reading R2)
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst), "l"(src), "r"(valid ? 8 : 0));
@@ -728,8 +736,8 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
           q = __ffma2_rn(f2(kc.tx2x), DX[p], q);
           if (HAS_DZ) q = __ffma2_rn(f2(kc.tx2z), DZ[p], q);
           const float2 r2 = __fadd2_rn(q, f2(kc.r2_t));
-          const float den0 = fmaf(r2.x, rsqrt_approx(r2.x), kc.r_t);
-          const float den1 = fmaf(r2.y, rsqrt_approx(r2.y), kc.r_t);
+          const float den0 = leg_den(r2.x, kc.r_t);
+          const float den1 = leg_den(r2.y, kc.r_t);
           BT[p] = __fmul2_rn(__fmul2_rn(q, make_float2(rcp_approx(den0), rcp_approx(den1))), f2(kfs));
         }
       }
@@ -769,8 +777,8 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
           U = __fadd2_rn(make_float2(r0 - kc.a1, r1 - kc.a1), BT[p]);
         } else if (MODE == kExact) {
           const float2 r2 = __fadd2_rn(q, f2(kc.r2_r));
-          const float den0 = fmaf(r2.x, rsqrt_approx(r2.x), kc.r_r);
-          const float den1 = fmaf(r2.y, rsqrt_approx(r2.y), kc.r_r);
+          const float den0 = leg_den(r2.x, kc.r_r);
+          const float den1 = leg_den(r2.y, kc.r_r);
           if (WEIGHT) {
             const float2 dU = __fmul2_rn(__fmul2_rn(q, make_float2(rcp_approx(den0), rcp_approx(den1))), f2(kfs));
             U = __fadd2_rn(dU, BT[p]);
@@ -894,9 +902,9 @@ __global__ void __launch_bounds__(32 * WY * WZ) count_kernel(const TdbpParams pr
         }
         const float qt = fmaf(kc.tx2x, dx[k], fmaf(kc.tx2y, dy[k], fmaf(kc.tx2z, dz[k], dd[k])));
         const float qr = fmaf(kc.ux2, dx[k], fmaf(kc.uy2, dy[k], fmaf(kc.uz2, dz[k], dd[k])));
-        const float rt = sqrtf(kc.r2_t + qt), rr = sqrtf(kc.r2_r + qr);
+        const float rt = sqrtf(fmaxf(kc.r2_t + qt, 0.f)), rr = sqrtf(fmaxf(kc.r2_r + qr, 0.f));
         const float kap = kc.kap0 + kc.kgx * dx[k] + kc.kgy * dy[k] + kc.kgz * dz[k];
-        const float du = (qt / (rt + kc.r_t) + qr / (rr + kc.r_r)) * (float)prm.k_s * kap;
+        const float du = (qt / fmaxf(rt + kc.r_t, 1e-30f) + qr / fmaxf(rr + kc.r_r, 1e-30f)) * (float)prm.k_s * kap;
         // absolute u = k_lo + 0.5 + Wh + (du + urr)
         const float ua = (float)kc.klo + 0.5f + (float)(prm.W >> 1) + (du + kc.urr);
         bool admit = ok[k] && ua > -1.f && ua < Nsf;

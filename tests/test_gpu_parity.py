@@ -630,3 +630,38 @@ def test_set_medium_errors(bpmod):
         assert ei.value.status == -5
         bp.set_motion(None)
         bp.form()
+
+
+def test_sensor_at_a_pixel_centre(bpmod):
+    """Degenerate geometry: the transmitter and one receiver sit exactly on pixel centres inside
+    the grid (R = 0 legs; the near-field exact mode); the image stays finite and matches the
+    oracle."""
+    s, e = _tiny(P=2, E=2, Ns=512, n=(9, 9, 3), seed=21)
+    g = s.grid
+    c0 = oracle.grid_points(g, np.array([[4, 4, 1]]))[0]
+    c1 = oracle.grid_points(g, np.array([[2, 6, 1]]))[0]
+    tx = s.tx.copy()
+    rx = s.rx.copy()
+    tx[0] = c0
+    rx[1, 0] = c1
+    t0 = np.zeros(s.P)
+    got = _form(bpmod, s, e, tx=tx, rx=rx, t0=t0)
+    assert np.all(np.isfinite(got))
+    ref = oracle.tdbp_grid(e, tx, rx, t0, s.fc, s.fs, s.c, g)
+    _check(got, ref, label="sensor on a pixel")
+
+
+def test_sensor_at_a_pixel_centre_counts(bpmod):
+    """K3 on the same degenerate geometry: the in-window count equals the oracle's."""
+    s, e = _tiny(P=2, E=2, Ns=512, n=(9, 9, 3), seed=21)
+    g = s.grid
+    tx = s.tx.copy()
+    rx = s.rx.copy()
+    tx[0] = oracle.grid_points(g, np.array([[4, 4, 1]]))[0]
+    rx[1, 0] = oracle.grid_points(g, np.array([[2, 6, 1]]))[0]
+    t0 = np.zeros(s.P)
+    with bpmod.Backprojector(s.fc, s.bandwidth, s.fs, s.c, g) as bp:
+        bp.set_pings(e, tx, rx, t0)
+        dense, inwin = bp.count_terms()
+    _, cnt = oracle.tdbp_grid(e, tx, rx, t0, s.fc, s.fs, s.c, g, with_count=True)
+    assert inwin == int(cnt.sum()) and dense == g["nx"] * g["ny"] * g["nz"] * s.P * s.E
