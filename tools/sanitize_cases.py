@@ -1,0 +1,75 @@
+"""Small representative launches of every kernel and mode, for compute-sanitizer:
+    compute-sanitizer --tool memcheck --error-exitcode 9 python tools/sanitize_cases.py
+(racecheck / initcheck likewise).  Prints one line per case; no parity checks (the tests do that)."""
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import synth  # noqa: E402
+import paper_2101_05888_b200 as pkg  # noqa: E402
+
+
+def run(name, fn):
+    fn()
+    torch.cuda.synchronize()
+    print("ok", name, flush=True)
+
+
+def tdbp(s, e, **opt):
+    with pkg.Backprojector(s.fc, s.bandwidth, s.fs, s.c, s.grid) as bp:
+        if opt.get("weight"):
+            bp.set_weighting(True)
+        if "beam" in opt:
+            bp.set_beam(*opt["beam"])
+        if "vel" in opt:
+            bp.set_motion(opt["vel"])
+        if "medium" in opt:
+            bp.set_medium(*opt["medium"])
+        bp.set_pings(e, s.tx, s.rx, s.t0)
+        bp.form()
+        bp.count_terms()
+
+
+for cid in (1, 2, 3, 4):
+    s = synth.scenario(cid, reduced=(cid != 1))
+    s = s.subset_pings(np.arange(min(s.P, 12)))
+    e = s.echoes()
+    run(f"dense cfg{cid}", lambda: tdbp(s, e))
+    run(f"weighted cfg{cid}", lambda: tdbp(s, e, weight=True))
+    if s.sin_half_beam > 0:
+        az = 2 * float(np.arcsin(s.sin_half_beam))
+        run(f"gated cfg{cid}", lambda: tdbp(s, e, beam=(az, 0.0, True, True)))
+    run(f"motion cfg{cid}", lambda: tdbp(s, e, vel=np.tile([1.5, 0.2, 0.05], (s.P, 1))))
+s4 = synth.scenario(4, reduced=True).subset_pings(np.arange(6))
+e4 = s4.echoes()
+run("refracted cfg4", lambda: tdbp(s4, e4, medium=(float(s4.grid["origin"][2]) + 0.2, 1700.0)))
+os.environ["SASBP_NO_TMA"] = "1"
+s2 = synth.scenario(2, reduced=True).subset_pings(np.arange(8))
+e2 = s2.echoes()
+run("cp.async dense cfg2", lambda: tdbp(s2, e2))
+del os.environ["SASBP_NO_TMA"]
+rng = np.random.default_rng(1)
+x = (rng.normal(size=(3, 2, 3001)) + 1j * rng.normal(size=(3, 2, 3001))).astype(np.complex64)
+rep = (rng.normal(size=600) + 1j * rng.normal(size=600)).astype(np.complex64)
+run("rangecompress fft", lambda: pkg.rangecompress(x, rep))
+os.environ["SASBP_RC_DIRECT"] = "1"
+run("rangecompress direct", lambda: pkg.rangecompress(x, rep))
+del os.environ["SASBP_RC_DIRECT"]
+for U in (1, 3, 4, 8):
+    run(f"upsample U={U}", lambda: pkg.upsample(x, U))
+xr = rng.normal(size=(2, 3, 5000)).astype(np.float32)
+h = np.hanning(65).astype(np.float32)
+for D in (1, 4, 37):
+    run(f"baseband D={D}", lambda: pkg.baseband(xr, 480e3, 120e3, np.array([0.01, 0.02]), h, D, 5000 // D))
+os.environ["SASBP_BB_SIMPLE"] = "1"
+run("baseband simple", lambda: pkg.baseband(xr, 480e3, 120e3, None, h, 4, 1250))
+del os.environ["SASBP_BB_SIMPLE"]
+for M in (2, 48, 64, 256):
+    run(f"whitening gain M={M}", lambda: pkg.whitening_gain(x, M, 0.1))
+G = pkg.whitening_gain(x, 64, 0.1)
+run("whitened compression", lambda: pkg.rangecompress_whitened(x, rep, G))
+print("all cases ran")
