@@ -324,11 +324,13 @@ __device__ __forceinline__ ChanConst chan_prologue(const TdbpParams& prm, int ch
       r_r = sqrt(urx_m * urx_m + ury_m * ury_m + urz_m * urz_m);
       tau = (r_t + r_r) / prm.c;
     }
-    const double ux = urx_m / r_r, uy = ury_m / r_r, uz = urz_m / r_r;
-    const double uv = ux * V[0] + uy * V[1] + uz * V[2];
-    kap0 = 1.0 / (1.0 + uv / prm.c);
-    const double s1 = -kap0 * kap0 / (prm.c * r_r);   // d kappa = -kap0^2 g1.d, g1 = (v - (u.v) u) / (c r)
-    kg[0] = s1 * (V[0] - uv * ux); kg[1] = s1 * (V[1] - uv * uy); kg[2] = s1 * (V[2] - uv * uz);
+    if (r_r > 1e-9) {   // (a receiver exactly at the tile centre keeps kappa = 1: no direction defined)
+      const double ux = urx_m / r_r, uy = ury_m / r_r, uz = urz_m / r_r;
+      const double uv = ux * V[0] + uy * V[1] + uz * V[2];
+      kap0 = 1.0 / (1.0 + uv / prm.c);
+      const double s1 = -kap0 * kap0 / (prm.c * r_r);   // d kappa = -kap0^2 g1.d, g1 = (v - (u.v) u) / (c r)
+      kg[0] = s1 * (V[0] - uv * ux); kg[1] = s1 * (V[1] - uv * uy); kg[2] = s1 * (V[2] - uv * uz);
+    }
   }
   double S = r_t + r_r;
   double At = 0.0, Ar = 0.0;   // refraction: reference one-way times in samples

@@ -73,3 +73,18 @@ for M in (2, 48, 64, 256):
 G = pkg.whitening_gain(x, 64, 0.1)
 run("whitened compression", lambda: pkg.rangecompress_whitened(x, rep, G))
 print("all cases ran")
+# degenerate geometry: sensors on a pixel centre and on a tile centre (with receiver motion)
+import oracle  # noqa: E402  (positions only: grid_points)
+r = synth.random_case(21, P=2, E=2, Ns=512, n=(17, 9, 9))
+g = r["grid"]
+tx, rx = r["tx"].copy(), r["rx"].copy()
+tx[0] = oracle.grid_points(g, np.array([[4, 4, 1]]))[0]
+rx[1, 0] = oracle.grid_points(g, np.array([[2, 6, 1]]))[0]
+ctr = np.asarray(g["origin"]) + 7.5 * np.asarray(g["step_x"]) + 3.5 * np.asarray(g["step_y"]) + 3.5 * np.asarray(g["step_z"])
+rx[0, 1] = ctr
+sd = synth.Scenario(name="degenerate", fc=r["fc"], bandwidth=r["fs"] / 4, fs=r["fs"], c=r["c"], tx=tx, rx=rx,
+                    t0=np.zeros(2), Ns=512, grid=g, targets=np.zeros((0, 3)), target_pixels=np.zeros((0, 3), dtype=np.int64),
+                    scat=np.zeros((0, 3)), sigma=np.zeros(0, dtype=np.complex128), sin_half_beam=0.0)
+run("degenerate dense", lambda: tdbp(sd, r["echoes"]))
+run("degenerate motion", lambda: tdbp(sd, r["echoes"], vel=np.tile([2.0, 0.5, 0.1], (2, 1))))
+print("degenerate cases ran")
