@@ -84,8 +84,9 @@ SASBP_API void sas_bp_destroy(sas_bp_t h);
  *   tx      fp64 [P][3]     transmitter position per ping (stationary during transmit)
  *   rx      fp64 [P][E][3]  receiver phase centre per ping and element (stop-and-hop, R5)
  *   t0      fp64 [P] time of sample 0 after transmit, or NULL for all zero (R4)
- * Errors: SAS_E_INVALID for P|E|Ns < 1, NULL echoes/tx/rx, non-finite tx/rx/t0, or
- * P*E*Ns overflow; SAS_E_NOMEM; SAS_E_CUDA. Synchronous w.r.t. the host buffers. */
+ * Errors: SAS_E_INVALID for P|E|Ns < 1, NULL echoes/tx/rx, non-finite tx/rx/t0, P*E*Ns
+ * overflow, or delays beyond 1e9 samples (sensor-to-grid distances and |t0| at fs; e.g. t0 in
+ * the wrong unit); SAS_E_NOMEM; SAS_E_CUDA. Synchronous w.r.t. the host buffers. */
 SASBP_API sas_status sas_bp_set_pings(sas_bp_t h, const float* echoes, int32_t P, int32_t E, int32_t Ns,
                             const double* tx, const double* rx, const double* t0);
 

@@ -254,6 +254,23 @@ sas_status upload_geo(sas_bp_t h, int32_t P, int32_t E, int32_t Ns, const double
   h->max_sensor_z = -INFINITY;
   for (int32_t p = 0; p < P; ++p) h->max_sensor_z = std::fmax(h->max_sensor_z, tx[3 * (size_t)p + 2]);
   for (size_t i = 0; i < (size_t)P * E; ++i) h->max_sensor_z = std::fmax(h->max_sensor_z, rx[3 * i + 2]);
+  // sample indices must stay far inside int32 (window starts, TMA coordinates): reject geometries
+  // whose delays exceed 1e9 samples (e.g. t0 in the wrong unit)
+  {
+    double bc[3], hd2 = 0, far_t = 0, far_r = 0, t0max = 0;
+    for (int a = 0; a < 3; ++a) { bc[a] = 0.5 * (lo[a] + hi[a]); hd2 += 0.25 * (hi[a] - lo[a]) * (hi[a] - lo[a]); }
+    const double hd = std::sqrt(hd2);
+    auto dist = [&](const double* q) {
+      return std::sqrt((q[0] - bc[0]) * (q[0] - bc[0]) + (q[1] - bc[1]) * (q[1] - bc[1]) + (q[2] - bc[2]) * (q[2] - bc[2]));
+    };
+    for (int32_t p = 0; p < P; ++p) {
+      far_t = std::fmax(far_t, dist(tx + 3 * (size_t)p) + hd);
+      if (t0) t0max = std::fmax(t0max, std::fabs(t0[p]));
+    }
+    for (size_t i = 0; i < (size_t)P * E; ++i) far_r = std::fmax(far_r, dist(rx + 3 * i) + hd);
+    if ((far_t + far_r) * h->fs / h->c + t0max * h->fs > 1e9)
+      return fail(SAS_E_INVALID, "delays beyond 1e9 samples (check t0 units and sensor positions)");
+  }
   h->mode = choose_mode(h->d_max, rmin, h->c / h->fc);
   h->P = P; h->E = E; h->Ns = Ns;
   return SAS_OK;

@@ -665,3 +665,14 @@ def test_sensor_at_a_pixel_centre_counts(bpmod):
         dense, inwin = bp.count_terms()
     _, cnt = oracle.tdbp_grid(e, tx, rx, t0, s.fc, s.fs, s.c, g, with_count=True)
     assert inwin == int(cnt.sum()) and dense == g["nx"] * g["ny"] * g["nz"] * s.P * s.E
+
+
+def test_rejects_delays_beyond_int32_windows(bpmod):
+    """t0 in the wrong unit (e.g. 3e4 s): delays of ~1e9 samples are rejected, not launched."""
+    s, e = _tiny(P=2, E=2, Ns=256, seed=5)
+    with bpmod.Backprojector(s.fc, s.bandwidth, s.fs, s.c, s.grid) as bp:
+        with pytest.raises(bpmod.SasError) as ei:
+            bp.set_pings(e, s.tx, s.rx, np.full(s.P, 3.0e4))
+        assert ei.value.status == bpmod.sasbp.SAS_E_INVALID
+        bp.set_pings(e, s.tx, s.rx, s.t0)   # the handle stays usable
+        assert np.all(np.isfinite(bp.form()))
