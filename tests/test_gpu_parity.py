@@ -676,3 +676,21 @@ def test_rejects_delays_beyond_int32_windows(bpmod):
         assert ei.value.status == bpmod.sasbp.SAS_E_INVALID
         bp.set_pings(e, s.tx, s.rx, s.t0)   # the handle stays usable
         assert np.all(np.isfinite(bp.form()))
+
+
+def test_coarse_pixels_large_window_cp_async(bpmod):
+    """Coarse 5 cm pixels at fs = 4B: the tile window exceeds a TMA box (256 samples), so the
+    plan falls back to cp.async staging with ~150 KB of shared memory per CTA; parity holds."""
+    s = synth.scenario(2, reduced=True)
+    g = dict(s.grid)
+    g["step_x"] = np.array([0.05, 0.0, 0.0])
+    g["step_y"] = np.array([0.0, 0.05, 0.0])
+    g["nx"], g["ny"] = 40, 37
+    e = s.echoes()
+    with bpmod.Backprojector(s.fc, s.bandwidth, s.fs, s.c, g) as bp:
+        bp.set_pings(e, s.tx, s.rx, s.t0)
+        plan = bp.plan()
+        got = bp.form()
+    assert plan["window"] > 256 and plan["tma"] is False
+    ref = oracle.tdbp_grid(e, s.tx, s.rx, s.t0, s.fc, s.fs, s.c, g)
+    _check(got, ref, label="coarse pixels")
