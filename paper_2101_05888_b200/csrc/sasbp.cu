@@ -188,6 +188,7 @@ cudaError_t launch_tdbp(sas_bp_t h, float2* image, unsigned long long* counter, 
   prm.d_max = h->d_max;
   prm.vel = h->vel;
   prm.refract = h->refract; prm.zb = h->zb; prm.c2 = h->c2;
+  prm.mode = h->refract ? sasbp::kRefract : h->mode;
   if (h->refract) {   // the window must cover the slowest medium: |grad tau| <= 2 / min(c, c2)
     prm.hw = 2.0 * h->d_max * h->fs / std::min(h->c, h->c2);
     prm.W = (int)std::ceil(2.0 * prm.hw + 4.0) + 3;

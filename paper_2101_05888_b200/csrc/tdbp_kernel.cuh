@@ -103,6 +103,7 @@ struct TdbpParams {
   // sediment-water interface (NEXT-3, reading R17): z = zb, sediment speed c2 (refract != 0)
   int refract;
   double zb, c2;
+  int mode;               // receive-leg mode of the plan (kSeries3 / kSeries4 / kExact / kRefract)
 };
 
 // per-channel constants in shared memory (fp64 prologue output)
@@ -324,7 +325,12 @@ __device__ __forceinline__ ChanConst chan_prologue(const TdbpParams& prm, int ch
       r_r = sqrt(urx_m * urx_m + ury_m * ury_m + urz_m * urz_m);
       tau = (r_t + r_r) / prm.c;
     }
-    if (r_r > 1e-9) {   // (a receiver exactly at the tile centre keeps kappa = 1: no direction defined)
+    if (prm.mode == kExact) {
+      // near-field plans: the kernel evaluates kappa = |x - rx'| / (|x - rx'| + (u + d).v / c) exactly
+      // per pixel (the first-order expansion below is only accurate for |d| << R); pass (u.v)/c, v/c
+      kap0 = (urx_m * V[0] + ury_m * V[1] + urz_m * V[2]) / prm.c;
+      kg[0] = V[0] / prm.c; kg[1] = V[1] / prm.c; kg[2] = V[2] / prm.c;
+    } else if (r_r > 1e-9) {   // (a receiver exactly at the tile centre keeps kappa = 1: no direction defined)
       const double ux = urx_m / r_r, uy = ury_m / r_r, uz = urz_m / r_r;
       const double uv = ux * V[0] + uy * V[1] + uz * V[2];
       kap0 = 1.0 / (1.0 + uv / prm.c);
@@ -771,6 +777,7 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
         if (HAS_DZ) q = __ffma2_rn(f2(kc.uz2), DZ[p], q);
         float2 U;
         float2 wgt = f2(1.f);
+        float2 srr = f2(0.f);   // exact-mode moving receiver: |x - rx'| per pixel
         if (MODE == kRefract) {
           const float r0 = refr_time32(DX[p].x - kc.ux2, DY[p].x - kc.uy2, DZ[p].x - kc.uz2, zbr - kc.uz2,
                                        DZ[p].x - zbr, k1r, k2r);
@@ -781,6 +788,7 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
           const float2 r2 = __fadd2_rn(q, f2(kc.r2_r));
           const float den0 = leg_den(r2.x, kc.r_r);
           const float den1 = leg_den(r2.y, kc.r_r);
+          if (MOTION) srr = __fadd2_rn(make_float2(den0, den1), f2(-kc.r_r));   // |x - rx'|
           if (WEIGHT) {
             const float2 dU = __fmul2_rn(__fmul2_rn(q, make_float2(rcp_approx(den0), rcp_approx(den1))), f2(kfs));
             U = __fadd2_rn(dU, BT[p]);
@@ -818,6 +826,10 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
           float2 kap = __ffma2_rn(f2(kc.kgy), DY[p], f2(kc.kap0));
           kap = __ffma2_rn(f2(kc.kgx), DX[p], kap);
           if (HAS_DZ) kap = __ffma2_rn(f2(kc.kgz), DZ[p], kap);
+          if (MODE == kExact) {   // exact: kappa = |x - rx'| / (|x - rx'| + (u + d).v / c)
+            const float2 dn = __fadd2_rn(srr, kap);
+            kap = __fmul2_rn(srr, make_float2(rcp_approx(dn.x), rcp_approx(dn.y)));
+          }
           U = __ffma2_rn(U, kap, f2(kc.urr));
         } else {
           U = __fadd2_rn(U, f2(kc.urr));                     // centred window coordinate
@@ -905,7 +917,8 @@ __global__ void __launch_bounds__(32 * WY * WZ) count_kernel(const TdbpParams pr
         const float qt = fmaf(kc.tx2x, dx[k], fmaf(kc.tx2y, dy[k], fmaf(kc.tx2z, dz[k], dd[k])));
         const float qr = fmaf(kc.ux2, dx[k], fmaf(kc.uy2, dy[k], fmaf(kc.uz2, dz[k], dd[k])));
         const float rt = sqrtf(fmaxf(kc.r2_t + qt, 0.f)), rr = sqrtf(fmaxf(kc.r2_r + qr, 0.f));
-        const float kap = kc.kap0 + kc.kgx * dx[k] + kc.kgy * dy[k] + kc.kgz * dz[k];
+        const float tk = kc.kap0 + kc.kgx * dx[k] + kc.kgy * dy[k] + kc.kgz * dz[k];
+        const float kap = (prm.vel && prm.mode == kExact) ? rr / (rr + tk) : tk;
         const float du = (qt / fmaxf(rt + kc.r_t, 1e-30f) + qr / fmaxf(rr + kc.r_r, 1e-30f)) * (float)prm.k_s * kap;
         // absolute u = k_lo + 0.5 + Wh + (du + urr)
         const float ua = (float)kc.klo + 0.5f + (float)(prm.W >> 1) + (du + kc.urr);
