@@ -68,6 +68,7 @@ struct sas_bp_s {
   // TMA descriptor of the current echoes (row staging), rebuilt when the ping set changes
   sasbp::TmaDesc tmap{};
   bool use_tma = false;
+  int tma_W = -1;        // window the descriptor's box was encoded for (a launch with another W re-encodes)
   int ctas_per_sm = 0;   // measured occupancy of the last form
   // field-of-view gating (sas_bp_set_beam; NEXT-1)
   int gate = 0, cull = 0, az_on = 0, el_on = 0;
@@ -132,10 +133,10 @@ double dist_to_box(const double* p, const double lo[3], const double hi[3]) {
 // Encode the TMA descriptor for the echo array [P*E][Ns] of 8-byte samples, box = one window
 // row.  Returns false (cp.async fallback) when the layout does not meet TMA's rules: 16-B
 // aligned base and row pitch (Ns even), box <= 256 samples.
-bool encode_tma(sas_bp_t h) {
+bool encode_tma(sas_bp_t h, int W) {
   const char* no = getenv("SASBP_NO_TMA");
   if (no && no[0] == '1') return false;
-  const int box = sasbp::box_samples(h->W);
+  const int box = sasbp::box_samples(W);
   if ((h->Ns & 1) || box > 256 || (((uintptr_t)h->echoes) & 15)) return false;
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   if (!encode) {
@@ -150,10 +151,14 @@ bool encode_tma(sas_bp_t h) {
   cuuint64_t strides[1] = {(cuuint64_t)h->Ns * 8};
   cuuint32_t boxd[2] = {(cuuint32_t)box, 1};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = encode(reinterpret_cast<CUtensorMap*>(&h->tmap), CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, (void*)h->echoes,
+  sasbp::TmaDesc t{};
+  CUresult r = encode(reinterpret_cast<CUtensorMap*>(&t), CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, (void*)h->echoes,
                       dims, strides, boxd, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS;
+  if (r != CUDA_SUCCESS) return false;
+  h->tmap = t;
+  h->tma_W = W;
+  return true;
 }
 
 cudaError_t launch_tdbp(sas_bp_t h, float2* image, unsigned long long* counter, int accumulate,
@@ -193,7 +198,11 @@ cudaError_t launch_tdbp(sas_bp_t h, float2* image, unsigned long long* counter, 
     prm.hw = 2.0 * h->d_max * h->fs / std::min(h->c, h->c2);
     prm.W = (int)std::ceil(2.0 * prm.hw + 4.0) + 3;
   }
-  sasbp::K2Launch L{h->use_tma, h->mode, count, st, &g_last_occ};
+  // the TMA box must match the window this launch stages (the refracted plan widens it): a
+  // descriptor encoded for another W would never complete the batch's mbarrier transaction
+  bool tma = h->use_tma;
+  if (tma && h->tma_W != prm.W) tma = encode_tma(h, prm.W);
+  sasbp::K2Launch L{tma, h->mode, count, st, &g_last_occ};
   g_last_occ = 0;
   const bool g = prm.gate && !count;
   if (h->weight && !count) {
@@ -411,7 +420,7 @@ sas_status sas_bp_set_pings(sas_bp_t h, const float* echoes, int32_t P, int32_t 
   st = upload_geo(h, P, E, Ns, tx, rx, t0, h->stream);  // synchronises the stream
   if (st != SAS_OK) { h->has_pings = false; return st; }
   h->echoes = h->echoes_owned;
-  h->use_tma = encode_tma(h);
+  h->use_tma = encode_tma(h, h->W);
   h->has_pings = true;
   return SAS_OK;
 }
@@ -430,7 +439,7 @@ sas_status sas_bp_set_pings_device(sas_bp_t h, const void* echoes_dev, int32_t P
   st = upload_geo(h, P, E, Ns, tx, rx, t0, s);
   if (st != SAS_OK) { h->has_pings = false; return st; }
   h->echoes = (const float2*)echoes_dev;
-  h->use_tma = encode_tma(h);
+  h->use_tma = encode_tma(h, h->W);
   h->has_pings = true;
   return SAS_OK;
 }
@@ -498,7 +507,7 @@ sas_status sas_bp_form_streamed(sas_bp_t h, const float* echoes, int32_t P, int3
   st = upload_geo(h, P, E, Ns, tx, rx, t0, h->stream);  // small, synchronous
   if (st != SAS_OK) { h->has_pings = false; return st; }
   h->echoes = h->echoes_owned;
-  h->use_tma = encode_tma(h);
+  h->use_tma = encode_tma(h, h->W);
   h->has_pings = true;
   if (h->gate && h->axes && h->axes_P != h->P) return fail(SAS_E_STATE, "beam axes were given for %d pings, the ping set has %d", h->axes_P, h->P);
   if (h->vel && h->vel_P != h->P) return fail(SAS_E_STATE, "velocities were given for %d pings, the ping set has %d", h->vel_P, h->P);

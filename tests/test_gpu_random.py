@@ -97,3 +97,91 @@ def test_random_problem(pk, seed):
     else:
         ref = oracle.tdbp_points_motion(ech, tx, rx, t0, vel, fc, fs, c, pts)
     _cmp(got, ref, f"seed {seed} {mode} grid {grid['nx']}x{grid['ny']}x{grid['nz']} P{len(tx)}")
+
+
+def _axes(rng, P):
+    a = rng.normal(size=(P, 3))
+    a /= np.linalg.norm(a, axis=1, keepdims=True)
+    b = rng.normal(size=(P, 3))
+    b -= (b * a).sum(1, keepdims=True) * a
+    b /= np.linalg.norm(b, axis=1, keepdims=True)
+    return np.stack([a, b], axis=1)
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_random_gated(pk, seed):
+    """Random beams: azimuth 0.1-1.5 rad, optional elevation, bistatic or not, per-ping axes or the
+    default, culling on or off; the gate decisions are fp64 on both sides (R15)."""
+    grid, tx, rx, t0, ech, fc, fs, c, _ = _case(100 + seed)
+    rng = np.random.default_rng(7000 + seed)
+    P = len(tx)
+    az = float(rng.uniform(0.1, 1.5))
+    el = float(rng.uniform(0.2, 2.0)) if seed % 3 == 0 else 0.0
+    bistatic = bool(seed % 2)
+    axes = _axes(rng, P) if seed % 4 < 2 else None
+    cull = seed % 5 != 0
+    idx = _idx(grid)
+    pts = oracle.grid_points(grid, idx)
+    with pk.Backprojector(fc, fs / 4, fs, c, grid) as bp:
+        bp.set_pings(ech, tx, rx, t0)
+        bp.set_beam(az, el, bistatic, cull, axes)
+        got = bp.form()
+        _, inc = bp.count_terms()
+    ref, cnt = oracle.tdbp_points_gated(ech, tx, rx, t0, fc, fs, c, pts, az, el, bistatic, axes, with_count=True)
+    assert inc == int(cnt.sum()), (seed, inc, int(cnt.sum()))
+    _cmp(got, ref, f"gated seed {seed}")
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_refracted(pk, seed):
+    """Random flat interfaces through or below the volume, sediment faster or slower than water."""
+    grid, tx, rx, t0, ech, fc, fs, c, _ = _case(200 + 2 * seed + 1)   # odd -> 3D grids
+    rng = np.random.default_rng(8000 + seed)
+    zs = max(tx[:, 2].max(), rx[:, :, 2].max())
+    pts_all = oracle.grid_points(grid, _idx(grid))
+    zb = float(zs + rng.uniform(0.01, 1.0) * max(1e-3, pts_all[:, 2].max() - zs)) if pts_all[:, 2].max() > zs \
+        else float(zs + 0.05)
+    c2 = float(rng.choice([1450.0, 1600.0, 1750.0]))
+    with pk.Backprojector(fc, fs / 4, fs, c, grid) as bp:
+        bp.set_pings(ech, tx, rx, t0)
+        try:
+            bp.set_medium(zb, c2)
+        except pk.SasError:
+            pytest.skip("window for this sediment speed exceeds shared memory")
+        got = bp.form()
+    ref = oracle.tdbp_points_refracted(ech, tx, rx, t0, zb, c2, fc, fs, c, pts_all)
+    _cmp(got, ref, f"refracted seed {seed}")
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_conditioning(pk, seed):
+    """Random sizes for K1 (both paths), K1b, K0 and the whitening pair."""
+    rng = np.random.default_rng(9000 + seed)
+    nch, Ns = int(rng.integers(1, 7)), int(rng.integers(1, 5000))
+    x = ((rng.normal(size=(nch, Ns)) + 1j * rng.normal(size=(nch, Ns))) / np.sqrt(2)).astype(np.complex64)
+    Nr = int(rng.integers(1, 2100))
+    rep = ((rng.normal(size=Nr) + 1j * rng.normal(size=Nr)) / np.sqrt(2 * Nr)).astype(np.complex64)
+    r = oracle.rangecompress(x, rep)
+    assert np.max(np.abs(pk.rangecompress(x, rep) - r)) <= 2e-5 * max(np.max(np.abs(r)), 1e-30)
+    U = int(rng.integers(1, 17))
+    u = oracle.upsample(x, U)
+    assert np.max(np.abs(pk.upsample(x, U) - u)) <= 2e-5 * np.max(np.abs(u))
+    D = int(rng.integers(1, 40))
+    Nh = int(rng.integers(0, 200)) * 2 + 1
+    h = rng.normal(size=Nh).astype(np.float32)
+    xr = rng.normal(size=(1, nch, max(Ns, 1))).astype(np.float32)
+    Nout = int(rng.integers(1, max(2, Ns // D + 3)))
+    t0 = np.array([float(rng.uniform(0, 0.05))])
+    fcb = float(rng.uniform(1e3, 200e3))
+    b = oracle.baseband(xr, 480e3, fcb, t0, h, D, Nout)
+    bg = pk.baseband(xr, 480e3, fcb, t0, h, D, Nout)
+    assert np.max(np.abs(bg - b)) <= 2e-5 * max(np.max(np.abs(b)), 1e-30) or np.max(np.abs(b)) == 0
+    M = int(rng.choice([1, 2, 16, 32, 48, 64, 128, 256]))
+    if np.max(np.abs(x)) > 0:
+        G, _ = oracle.whitening_gain(x, M, 0.05)
+        Gg = pk.whitening_gain(x, M, 0.05)
+        assert np.max(np.abs(Gg - G)) <= 2e-5
+        if Nr + M - 1 <= 8192 and nch * Ns * Nr * M <= 3e8:   # the oracle cascade is O(Ns Nr M)
+            w = oracle.rangecompress_whitened(x, rep, G.astype(np.float32).astype(np.float64))
+            wg = pk.rangecompress_whitened(x, rep, G.astype(np.float32))
+            assert np.max(np.abs(wg - w)) <= 2e-5 * max(np.max(np.abs(w)), 1e-30)
