@@ -185,3 +185,63 @@ def test_random_conditioning(pk, seed):
             w = oracle.rangecompress_whitened(x, rep, G.astype(np.float32).astype(np.float64))
             wg = pk.rangecompress_whitened(x, rep, G.astype(np.float32))
             assert np.max(np.abs(wg - w)) <= 2e-5 * max(np.max(np.abs(w)), 1e-30)
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_random_partition_accumulate_streamed(pk, seed):
+    """Ping-partition additivity through SAS_FORM_ACCUMULATE on borrowed (device) echoes, an
+    8-byte-but-not-16-byte aligned device pointer (cp.async staging), and form_streamed with a
+    random chunk count -- all against the single dense form."""
+    import torch
+    grid, tx, rx, t0, ech, fc, fs, c, _ = _case(300 + seed)
+    P = len(tx)
+    rng = np.random.default_rng(9500 + seed)
+    with pk.Backprojector(fc, fs / 4, fs, c, grid) as bp:
+        bp.set_pings(ech, tx, rx, t0)
+        ref = bp.form()
+        # partition the pings, accumulate on the device
+        cut = int(rng.integers(0, P + 1))
+        img = torch.zeros(bp.shape, dtype=torch.complex64, device="cuda")
+        first = True
+        for sl in (slice(0, cut), slice(cut, P)):
+            if sl.stop - sl.start == 0:
+                continue
+            e_d = torch.from_numpy(np.ascontiguousarray(ech[sl])).cuda()
+            bp.set_pings_device(e_d, tx[sl], rx[sl], t0[sl])
+            bp.form_device(img, accumulate=not first)
+            first = False
+        torch.cuda.synchronize()
+        part = img.cpu().numpy()
+        # misaligned (8-byte) borrowed pointer -> cp.async staging
+        buf = torch.empty(ech.size + 1, dtype=torch.complex64, device="cuda")
+        view = buf[1:].view(ech.shape)
+        view.copy_(torch.from_numpy(ech))
+        bp.set_pings_device(view, tx, rx, t0)
+        mis = torch.empty(bp.shape, dtype=torch.complex64, device="cuda")
+        bp.form_device(mis)
+        torch.cuda.synchronize()
+        tma_mis = bp.plan()["tma"]
+        st = bp.form_streamed(ech, tx, rx, t0, chunks=int(rng.integers(0, 5)))
+    assert tma_mis is False
+    scale = np.max(np.abs(ref))
+    if scale == 0:
+        return
+    assert np.max(np.abs(part - ref)) <= 1e-5 * scale
+    assert np.max(np.abs(mis.cpu().numpy() - ref)) <= 1e-6 * scale
+    assert np.max(np.abs(st - ref)) <= 1e-5 * scale
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_random_gated_weighted(pk, seed):
+    grid, tx, rx, t0, ech, fc, fs, c, _ = _case(400 + seed)
+    rng = np.random.default_rng(9700 + seed)
+    az = float(rng.uniform(0.2, 1.5))
+    bistatic = bool(seed % 2)
+    pts = oracle.grid_points(grid, _idx(grid))
+    with pk.Backprojector(fc, fs / 4, fs, c, grid) as bp:
+        bp.set_pings(ech, tx, rx, t0)
+        bp.set_weighting(True)
+        bp.set_beam(az, 0.0, bistatic, True)
+        got = bp.form()
+    ref = oracle.tdbp_points_gated_weighted(ech, tx, rx, t0, fc, fs, c, pts, az=az, bistatic=bistatic)
+    _cmp(got, ref, f"gated weighted seed {seed}")
