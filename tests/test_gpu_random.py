@@ -245,3 +245,44 @@ def test_random_gated_weighted(pk, seed):
         got = bp.form()
     ref = oracle.tdbp_points_gated_weighted(ech, tx, rx, t0, fc, fs, c, pts, az=az, bistatic=bistatic)
     _cmp(got, ref, f"gated weighted seed {seed}")
+
+
+def _case_many(seed):
+    """Stripmap-like problems with many channels (multi-batch pipelines: prologue groups, the
+    constant ring, mbarrier phases, culled batches) on small grids."""
+    rng = np.random.default_rng(11000 + seed)
+    c, fs = 1500.0, float(rng.choice([40e3, 120e3]))
+    fc = fs * float(rng.uniform(0.5, 2.0))
+    P, E = int(rng.integers(20, 90)), int(rng.integers(1, 9))
+    nx, ny = int(rng.integers(8, 70)), int(rng.integers(8, 70))
+    step = float(rng.uniform(0.005, 0.02))
+    y0 = float(rng.uniform(5, 20))
+    grid = {"origin": np.array([0.0, y0, 0.0]), "step_x": np.array([step, 0, 0]), "step_y": np.array([0, step, 0]),
+            "step_z": np.array([0, 0, 1.0]), "nx": nx, "ny": ny, "nz": 1}
+    xs = np.linspace(-3, 3 + nx * step, P)
+    tx = np.stack([xs, np.zeros(P), np.full(P, -5.0)], axis=1) + rng.normal(size=(P, 3)) * 0.02
+    rx = tx[:, None, :] + np.stack([(np.arange(E) - (E - 1) / 2) * 0.03, np.zeros(E), np.zeros(E)], axis=1)[None]
+    ctr = np.array([nx * step / 2, y0 + ny * step / 2, 0.0])
+    d = np.linalg.norm(ctr[None] - tx, axis=1)
+    Ns = int(rng.integers(300, 1500))
+    t0 = 2 * d / c - 0.5 * Ns / fs + rng.uniform(-0.2, 0.2) * Ns / fs
+    ech = ((rng.normal(size=(P, E, Ns)) + 1j * rng.normal(size=(P, E, Ns))) / np.sqrt(2)).astype(np.complex64)
+    return grid, tx, rx, t0, ech, fc, fs, c
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_random_many_channels(pk, seed):
+    grid, tx, rx, t0, ech, fc, fs, c = _case_many(seed)
+    pts = oracle.grid_points(grid, _idx(grid))
+    gated = seed % 2 == 1
+    az = 0.3 + 0.05 * seed
+    with pk.Backprojector(fc, fs / 4, fs, c, grid) as bp:
+        bp.set_pings(ech, tx, rx, t0)
+        if gated:
+            bp.set_beam(az, 0.0, seed % 4 == 3, True)
+        got = bp.form()
+    if gated:
+        ref = oracle.tdbp_points_gated(ech, tx, rx, t0, fc, fs, c, pts, az, 0.0, seed % 4 == 3)
+    else:
+        ref = oracle.tdbp_points(ech, tx, rx, t0, fc, fs, c, pts)
+    _cmp(got, ref, f"many channels seed {seed} P{len(tx)} E{rx.shape[1]} gated={gated}")
