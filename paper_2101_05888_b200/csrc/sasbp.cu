@@ -261,6 +261,7 @@ sas_status upload_geo(sas_bp_t h, int32_t P, int32_t E, int32_t Ns, const double
   }
   double rmin = INFINITY;
   for (size_t i = 0; i < (size_t)P * E; ++i) rmin = std::fmin(rmin, dist_to_box(rx + 3 * i, lo, hi));
+  for (int32_t p = 0; p < P; ++p) rmin = std::fmin(rmin, dist_to_box(tx + 3 * (size_t)p, lo, hi));   // tx leg series too
   h->max_sensor_z = -INFINITY;
   for (int32_t p = 0; p < P; ++p) h->max_sensor_z = std::fmax(h->max_sensor_z, tx[3 * (size_t)p + 2]);
   for (size_t i = 0; i < (size_t)P * E; ++i) h->max_sensor_z = std::fmax(h->max_sensor_z, rx[3 * i + 2]);

@@ -48,6 +48,9 @@ namespace sasbp {
 #ifndef SASBP_CC_LDS
 #define SASBP_CC_LDS 0   // A/B knob: channel constants via explicit ld.shared (see lds_struct)
 #endif
+#ifndef SASBP_TX_SERIES
+#define SASBP_TX_SERIES 1   // series plans evaluate the transmit leg with the same series (no MUFU)
+#endif
 #ifndef SASBP_BININDEX
 // 1: the window cell index comes from the exponent-aligned window coordinate V = u - k_lo + 2^kb
 //    by integer ops (SHF + LOP3 + IADD3 on the ALU pipe); the phase and the lerp use the small
@@ -738,6 +741,15 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
           }
         }
         // transmit leg, exact range-relative form: dR = q / (sqrt(r^2 + q) + r), in samples
+#if SASBP_TX_SERIES
+        // series plans: dU_tx = q (a0 + a1 q + a2 q^2 [+ a3 q^3]), a_n = c_n (fs/c) / r_t^(2n+1)
+        // (the plan's truncation bound covers the transmitter too)
+        float ta0 = 0.f, ta1 = 0.f, ta2 = 0.f, ta3 = 0.f;
+        if (MODE == kSeries3 || MODE == kSeries4) {
+          const float ir = rcp_approx(kc.r_t), ir2 = ir * ir, g = kfs * ir;
+          ta0 = 0.5f * g; ta1 = -0.125f * g * ir2; ta2 = 0.0625f * g * ir2 * ir2; ta3 = -0.0390625f * g * ir2 * ir2 * ir2;
+        }
+#endif
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
           if (MODE == kRefract) {   // Fermat time through the interface minus the tile reference
@@ -751,6 +763,15 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
           float2 q = __ffma2_rn(f2(kc.tx2y), AXIS ? f2(DYS[p]) : DY[p], DD[p]);
           q = __ffma2_rn(f2(kc.tx2x), DX[p], q);
           if (HAS_DZ) q = __ffma2_rn(f2(kc.tx2z), DZ[p], q);
+#if SASBP_TX_SERIES
+          if (MODE == kSeries3 || MODE == kSeries4) {   // far field: the rx leg's series, no MUFU
+            float2 h = MODE == kSeries4 ? __ffma2_rn(f2(ta3), q, f2(ta2)) : f2(ta2);
+            h = __ffma2_rn(h, q, f2(ta1));
+            h = __ffma2_rn(h, q, f2(ta0));
+            BT[p] = __fmul2_rn(q, h);
+            continue;
+          }
+#endif
           const float2 r2 = __fadd2_rn(q, f2(kc.r2_t));
           const float den0 = leg_den(r2.x, kc.r_t);
           const float den1 = leg_den(r2.y, kc.r_t);
