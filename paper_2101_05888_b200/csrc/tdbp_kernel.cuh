@@ -477,9 +477,31 @@ __device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
 // Wait for a batch's TMA transaction.  A transaction that never completes (a byte count that does
 // not match what was issued) is a bug: trap -- the launch fails with an error -- instead of
 // spinning forever (each try_wait already suspends for a hardware time slice).
+#ifndef SASBP_MBAR_TRAP
+#define SASBP_MBAR_TRAP 0   // debug option: trap instead of spinning on a transaction that never completes (costs 3 % on 3D plans)
+#endif
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  for (uint32_t n = 0; !mbar_try(bar, parity); ++n)
-    if (n > (1u << 22)) __trap();
+#if SASBP_MBAR_TRAP
+  // the poll loop stays in PTX (a C++ loop around try_wait cost 3 % on the 3D plan); the counter
+  // only runs while the transaction is incomplete
+  asm volatile(
+      "{\n .reg .pred p, q;\n .reg .u32 n;\n"
+      " mov.u32 n, 0;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @p bra DONE_%=;\n"
+      " add.u32 n, n, 1;\n"
+      " setp.lt.u32 q, n, 4194304;\n"
+      " @q bra WAIT_%=;\n"
+      " trap;\n"
+      "DONE_%=:\n}\n" ::"r"(bar), "r"(parity) : "memory");
+#else
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(bar), "r"(parity) : "memory");
+#endif
 }
 __device__ __forceinline__ void tma_load_row(uint32_t dst, const void* tmap, int x, int y, uint32_t bar) {
   asm volatile(
