@@ -48,6 +48,9 @@ namespace sasbp {
 #ifndef SASBP_CC_LDS
 #define SASBP_CC_LDS 0   // A/B knob: channel constants via explicit ld.shared (see lds_struct)
 #endif
+#ifndef SASBP_DIV_MULHI
+#define SASBP_DIV_MULHI 1
+#endif
 #ifndef SASBP_TX_SERIES
 #define SASBP_TX_SERIES 1   // series plans evaluate the transmit leg with the same series (no MUFU)
 #endif
@@ -589,7 +592,10 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
   const float inv_w = 1.0f / (float)W;
 #endif
   const int P2 = (W + 1) >> 1;                // cell pairs per channel
-  const float inv_p2 = 1.0f / (float)P2;
+  [[maybe_unused]] const float inv_p2 = 1.0f / (float)P2;
+  // i / P2 as a multiply-high (exact for i < 2^32 / P2^2): keeps the transform's index math off
+  // the XU (the float trick below is an I2F + F2I pair per lane-step)
+  const uint32_t mp2 = 0xFFFFFFFFu / (uint32_t)P2 + 1u;
 
   if (tid == 0) {
     if (USE_TMA) {
@@ -701,7 +707,11 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
       const int nmine = (nb - warp + kWarps - 1) / kWarps;
       const int tot = nmine * P2;
       for (int i = lane; i < tot; i += 32) {
+#if SASBP_DIV_MULHI
+        const int q = (int)__umulhi((uint32_t)i, mp2);        // i / P2
+#else
         const int q = (int)(((float)i + 0.5f) * inv_p2);   // i / P2, exact for i < 2^20
+#endif
         const int t = i - q * P2;
         const int c = warp + q * kWarps;
         if (GATE && (cc[(b % kRing) * kNB + c].gate & 16)) continue;
