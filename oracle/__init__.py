@@ -104,6 +104,17 @@ def _load():
                                                           ctypes.c_double, f64p, ctypes.c_double, ctypes.c_double,
                                                           ctypes.c_int32, f64p, ctypes.c_int64, f64p]
         lib.oracle_tdbp_points_gated_weighted.restype = ctypes.c_int
+        lib.oracle_tdbp_points_gated_motion.argtypes = [f32p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                                        f64p, f64p, f64p, f64p, ctypes.c_double, ctypes.c_double,
+                                                        ctypes.c_double, f64p, ctypes.c_double, ctypes.c_double,
+                                                        ctypes.c_int32, f64p, ctypes.c_int64, f64p, i64p]
+        lib.oracle_tdbp_points_gated_motion.restype = ctypes.c_int
+        lib.oracle_tdbp_points_gated_refracted.argtypes = [f32p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                                           f64p, f64p, f64p, ctypes.c_double, ctypes.c_double,
+                                                           ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                                           f64p, ctypes.c_double, ctypes.c_double, ctypes.c_int32,
+                                                           f64p, ctypes.c_int64, f64p, i64p]
+        lib.oracle_tdbp_points_gated_refracted.restype = ctypes.c_int
         lib.oracle_num_threads.restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -312,6 +323,52 @@ def tdbp_points_gated_weighted(echoes, tx, rx, t0, fc, fs, c, pts, az, el=0.0, b
     if rc != 0:
         raise ValueError("oracle_tdbp_points_gated_weighted: invalid arguments")
     return out[:, 0] + 1j * out[:, 1]
+
+
+def tdbp_points_gated_motion(echoes, tx, rx, t0, vel, fc, fs, c, pts, az, el=0.0, bistatic=False, axes=None,
+                             with_count=False):
+    """Gated (R15) TDBP with the moving-receiver delay (R16); gate on transmit-time positions (R22)."""
+    lib = _load()
+    echoes, P, E, Ns, tx, rx, t0 = _echo_arrays(echoes, tx, rx, t0)
+    vel = np.ascontiguousarray(vel, dtype=np.float64).reshape(P, 3)
+    pts = np.ascontiguousarray(pts, dtype=np.float64).reshape(-1, 3)
+    ax = None if axes is None else np.ascontiguousarray(axes, dtype=np.float64).reshape(P, 2, 3)
+    N = pts.shape[0]
+    out = np.zeros((N, 2), dtype=np.float64)
+    cnt = np.zeros(N, dtype=np.int64) if with_count else None
+    rc = lib.oracle_tdbp_points_gated_motion(_p(echoes, ctypes.c_float), P, E, Ns, _p(tx, ctypes.c_double),
+                                             _p(rx, ctypes.c_double), _p(t0, ctypes.c_double),
+                                             _p(vel, ctypes.c_double), float(fc), float(fs), float(c),
+                                             _p(ax, ctypes.c_double), float(az), float(el), 1 if bistatic else 0,
+                                             _p(pts, ctypes.c_double), N, _p(out, ctypes.c_double),
+                                             _p(cnt, ctypes.c_int64))
+    if rc != 0:
+        raise ValueError("oracle_tdbp_points_gated_motion: invalid arguments")
+    res = out[:, 0] + 1j * out[:, 1]
+    return (res, cnt) if with_count else res
+
+
+def tdbp_points_gated_refracted(echoes, tx, rx, t0, zb, c2, fc, fs, c, pts, az, el=0.0, bistatic=False,
+                                axes=None, with_count=False):
+    """Gated (R15) TDBP with the Fermat delay through a flat interface (R17); straight line-of-sight
+    gate from the recorded sensor positions (R22)."""
+    lib = _load()
+    echoes, P, E, Ns, tx, rx, t0 = _echo_arrays(echoes, tx, rx, t0)
+    pts = np.ascontiguousarray(pts, dtype=np.float64).reshape(-1, 3)
+    ax = None if axes is None else np.ascontiguousarray(axes, dtype=np.float64).reshape(P, 2, 3)
+    N = pts.shape[0]
+    out = np.zeros((N, 2), dtype=np.float64)
+    cnt = np.zeros(N, dtype=np.int64) if with_count else None
+    rc = lib.oracle_tdbp_points_gated_refracted(_p(echoes, ctypes.c_float), P, E, Ns, _p(tx, ctypes.c_double),
+                                                _p(rx, ctypes.c_double), _p(t0, ctypes.c_double), float(zb),
+                                                float(c2), float(fc), float(fs), float(c), _p(ax, ctypes.c_double),
+                                                float(az), float(el), 1 if bistatic else 0,
+                                                _p(pts, ctypes.c_double), N, _p(out, ctypes.c_double),
+                                                _p(cnt, ctypes.c_int64))
+    if rc != 0:
+        raise ValueError("oracle_tdbp_points_gated_refracted: invalid arguments")
+    res = out[:, 0] + 1j * out[:, 1]
+    return (res, cnt) if with_count else res
 
 
 def lanczos4(s) -> float:

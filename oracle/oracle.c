@@ -624,6 +624,84 @@ int oracle_tdbp_points_gated_weighted(const float* echoes, int32_t P, int32_t E,
   return 0;
 }
 
+/*
+ * Gated TDBP with the receiver moving during reception (NEXT-1 gate R15 combined with the NEXT-2
+ * delay R16; reading R22 in DESIGN.md): the FOV decision is taken on the sensor positions at the
+ * transmit instant (tx_p, rx_{p,e} as recorded; the paper tests the sonar geometry per ping,
+ * P:160) along the straight line of sight, and every admitted term takes the moving-receiver
+ * delay of oracle_tdbp_points_motion:
+ *   I(x) = sum_{p,e} [x in FOV(tx_p)] [bistatic -> x in FOV(rx_{p,e})] term(x; tau = delay_moving)
+ */
+int oracle_tdbp_points_gated_motion(const float* echoes, int32_t P, int32_t E, int32_t Ns, const double* tx,
+                                    const double* rx, const double* t0, const double* vel, double fc, double fs,
+                                    double c, const double* axes, double az, double el, int32_t bistatic,
+                                    const double* pts, int64_t N, double* out, int64_t* n_in) {
+  if (P < 1 || E < 1 || Ns < 1 || N < 0 || !(c > 0) || !(fs > 0) || !vel) return -1;
+  static const double def_a[3] = {1.0, 0.0, 0.0}, def_b[3] = {0.0, 1.0, 0.0};
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int64_t i = 0; i < N; ++i) {
+    const double* x = pts + 3 * i;
+    double ar = 0.0, ai = 0.0;
+    int64_t cnt = 0;
+    for (int32_t p = 0; p < P; ++p) {
+      const double* a = axes ? axes + 6 * p : def_a;
+      const double* b = axes ? axes + 6 * p + 3 : def_b;
+      if (!in_fov(x, tx + 3 * p, a, b, az, el)) continue;
+      const double t0p = t0 ? t0[p] : 0.0;
+      for (int32_t e = 0; e < E; ++e) {
+        const double* r = rx + 3 * ((int64_t)p * E + e);
+        if (bistatic && !in_fov(x, r, a, b, az, el)) continue;
+        const float* ch = echoes + 2 * ((int64_t)p * E + e) * (int64_t)Ns;
+        const double tau = delay_moving(x, tx + 3 * p, r, vel + 3 * p, c);
+        cnt += one_term_tau(x, ch, Ns, tau, t0p, fc, fs, &ar, &ai);
+      }
+    }
+    out[2 * i] = ar;
+    out[2 * i + 1] = ai;
+    if (n_in) n_in[i] = cnt;
+  }
+  return 0;
+}
+
+/*
+ * Gated TDBP through a flat sediment-water interface (NEXT-1 gate R15 combined with the NEXT-3
+ * delay R17; reading R22; the paper's near-field craft uses bistatic culling and the refraction
+ * model together): the FOV decision is the straight line-of-sight cone test from the
+ * recorded sensor positions, every admitted term takes the Fermat delay of
+ * oracle_tdbp_points_refracted.
+ */
+int oracle_tdbp_points_gated_refracted(const float* echoes, int32_t P, int32_t E, int32_t Ns, const double* tx,
+                                       const double* rx, const double* t0, double zb, double c2, double fc,
+                                       double fs, double c, const double* axes, double az, double el,
+                                       int32_t bistatic, const double* pts, int64_t N, double* out, int64_t* n_in) {
+  if (P < 1 || E < 1 || Ns < 1 || N < 0 || !(c > 0) || !(fs > 0) || !(c2 > 0)) return -1;
+  static const double def_a[3] = {1.0, 0.0, 0.0}, def_b[3] = {0.0, 1.0, 0.0};
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int64_t i = 0; i < N; ++i) {
+    const double* x = pts + 3 * i;
+    double ar = 0.0, ai = 0.0;
+    int64_t cnt = 0;
+    for (int32_t p = 0; p < P; ++p) {
+      const double* a = axes ? axes + 6 * p : def_a;
+      const double* b = axes ? axes + 6 * p + 3 : def_b;
+      if (!in_fov(x, tx + 3 * p, a, b, az, el)) continue;
+      const double t0p = t0 ? t0[p] : 0.0;
+      const double tt = travel_refracted(x, tx + 3 * p, zb, c, c2);
+      for (int32_t e = 0; e < E; ++e) {
+        const double* r = rx + 3 * ((int64_t)p * E + e);
+        if (bistatic && !in_fov(x, r, a, b, az, el)) continue;
+        const float* ch = echoes + 2 * ((int64_t)p * E + e) * (int64_t)Ns;
+        const double tau = tt + travel_refracted(x, r, zb, c, c2);
+        cnt += one_term_tau(x, ch, Ns, tau, t0p, fc, fs, &ar, &ai);
+      }
+    }
+    out[2 * i] = ar;
+    out[2 * i + 1] = ai;
+    if (n_in) n_in[i] = cnt;
+  }
+  return 0;
+}
+
 /* Number of OpenMP threads the oracle will use (for the cpu_baseline "cores"). */
 int oracle_num_threads(void) {
 #ifdef _OPENMP
