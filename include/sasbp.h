@@ -106,7 +106,14 @@ SASBP_API sas_status sas_bp_form(sas_bp_t h, float* image_out);
 /* Form the image into DEVICE memory image_dev (complex64 [nz][ny][nx], 8-byte aligned),
  * asynchronously on cuda_stream (NULL = legacy default stream).
  * flags: 0 = overwrite, SAS_FORM_ACCUMULATE = add to the existing contents of image_dev
- * (ping-chunked / ping-sharded partial images: I(A u B) = I(A) + I(B)). */
+ * (ping-chunked / ping-sharded partial images: I(A u B) = I(A) + I(B)).
+ * Ordering: the launch reads the handle's workspace (nav, owned echoes, beam axes, velocities)
+ * after this call returns.  The handle records an event on cuda_stream, and every later call
+ * that rewrites that workspace (sas_bp_set_pings[_device], sas_bp_form_streamed,
+ * sas_bp_set_beam with axes, sas_bp_set_motion) first blocks the host until it has completed,
+ * so a "set_pings(chunk); form_device(..., ACCUMULATE)" loop on any stream is race-free.  The
+ * caller still owns the ordering of image_dev and of BORROWED echoes (set_pings_device) with
+ * its own work on other streams. */
 #define SAS_FORM_ACCUMULATE 1
 SASBP_API sas_status sas_bp_form_device(sas_bp_t h, void* image_dev, void* cuda_stream, int32_t flags);
 

@@ -64,6 +64,11 @@ struct sas_bp_s {
   unsigned long long* counter = nullptr;
   cudaStream_t stream = nullptr;
   cudaStream_t copy_stream = nullptr;   // H2D of ping chunks in sas_bp_form_streamed
+  // Completion of the last K2/K3 launch queued on a caller stream (sas_bp_form_device): every call
+  // that rewrites the workspace (nav, owned echoes, axes, velocities) first waits for it, so a
+  // setter can never overwrite data a still-running kernel reads (sasbp.h "Ordering").
+  cudaEvent_t busy = nullptr;
+  bool busy_pending = false;
   int P = 0, E = 0, Ns = 0;
   // TMA descriptor of the current echoes (row staging), rebuilt when the ping set changes
   sasbp::TmaDesc tmap{};
@@ -103,6 +108,33 @@ sas_status cuda_fail(sas_bp_t h, cudaError_t e, const char* what) {
   } while (0)
 
 size_t smem_bytes(int W) { return sasbp::k2_smem_bytes(W); }
+
+// Host-blocking wait for the last asynchronous launch that reads the workspace.
+sas_status wait_idle(sas_bp_t h) {
+  if (h->busy_pending) {
+    CK_H(h, cudaEventSynchronize(h->busy));
+    h->busy_pending = false;
+  }
+  return SAS_OK;
+}
+
+// Mode combinations and per-ping array sizes, checked against the ping set about to be used
+// (P, largest sensor z) BEFORE any state changes.
+sas_status check_modes(sas_bp_t h, int32_t P, double max_sensor_z) {
+  if (h->gate && h->axes && h->axes_P != P) return fail(SAS_E_STATE, "beam axes were given for %d pings, the ping set has %d", h->axes_P, P);
+  if (h->vel && h->vel_P != P) return fail(SAS_E_STATE, "velocities were given for %d pings, the ping set has %d", h->vel_P, P);
+  if (h->refract && h->vel) return fail(SAS_E_UNSUPPORTED, "refraction and receiver motion cannot be combined");
+  if (h->refract && !(max_sensor_z < h->zb)) return fail(SAS_E_INVALID, "with an interface every sensor must be in the water (z < zb)");
+  if (h->weight && (h->vel || h->refract)) return fail(SAS_E_UNSUPPORTED, "the spreading weight is defined for stop-and-hop straight rays only");
+  return SAS_OK;
+}
+
+double max_z(int32_t P, int32_t E, const double* tx, const double* rx) {
+  double m = -INFINITY;
+  for (int32_t p = 0; p < P; ++p) m = std::fmax(m, tx[3 * (size_t)p + 2]);
+  for (size_t i = 0; i < (size_t)P * E; ++i) m = std::fmax(m, rx[3 * i + 2]);
+  return m;
+}
 
 // Receive-leg mode from the series truncation bound: sqrt(1+e) - 1 truncated
 // after n terms leaves |rem| <= r * |c_{n+1}| e^{n+1} / (1 - e) (alternating, decreasing terms),
@@ -237,6 +269,7 @@ sas_status validate_geo(int32_t P, int32_t E, int32_t Ns, const double* tx, cons
 sas_status upload_geo(sas_bp_t h, int32_t P, int32_t E, int32_t Ns, const double* tx, const double* rx,
                       const double* t0, cudaStream_t st) {
   const size_t n = 3 * (size_t)P + 3 * (size_t)P * E + (size_t)P;
+  if (sas_status w = wait_idle(h); w != SAS_OK) return w;
   if (n > h->geo_cap) {
     if (h->geo) { cudaFree(h->geo); h->bytes -= h->geo_cap * sizeof(double); h->geo = nullptr; h->geo_cap = 0; }
     cudaError_t e = cudaMalloc(&h->geo, n * sizeof(double));
@@ -262,9 +295,7 @@ sas_status upload_geo(sas_bp_t h, int32_t P, int32_t E, int32_t Ns, const double
   double rmin = INFINITY;
   for (size_t i = 0; i < (size_t)P * E; ++i) rmin = std::fmin(rmin, dist_to_box(rx + 3 * i, lo, hi));
   for (int32_t p = 0; p < P; ++p) rmin = std::fmin(rmin, dist_to_box(tx + 3 * (size_t)p, lo, hi));   // tx leg series too
-  h->max_sensor_z = -INFINITY;
-  for (int32_t p = 0; p < P; ++p) h->max_sensor_z = std::fmax(h->max_sensor_z, tx[3 * (size_t)p + 2]);
-  for (size_t i = 0; i < (size_t)P * E; ++i) h->max_sensor_z = std::fmax(h->max_sensor_z, rx[3 * i + 2]);
+  h->max_sensor_z = max_z(P, E, tx, rx);
   // sample indices must stay far inside int32 (window starts, TMA coordinates): reject geometries
   // whose delays exceed 1e9 samples (e.g. t0 in the wrong unit)
   {
@@ -371,11 +402,13 @@ sas_status sas_bp_create(double fc, double bandwidth, double fs, double c, const
   }
   e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
   if (e != cudaSuccess) { delete h; return fail(SAS_E_CUDA, "cudaStreamCreate: %s", cudaGetErrorString(e)); }
+  e = cudaEventCreateWithFlags(&h->busy, cudaEventDisableTiming);
+  if (e != cudaSuccess) { cudaStreamDestroy(h->stream); delete h; return fail(SAS_E_CUDA, "cudaEventCreate: %s", cudaGetErrorString(e)); }
   const size_t npx = (size_t)g.nx * g.ny * g.nz;
   e = cudaMalloc(&h->image, npx * sizeof(float2));
-  if (e != cudaSuccess) { cudaStreamDestroy(h->stream); delete h; return fail(SAS_E_NOMEM, "cudaMalloc(image): %s", cudaGetErrorString(e)); }
+  if (e != cudaSuccess) { cudaEventDestroy(h->busy); cudaStreamDestroy(h->stream); delete h; return fail(SAS_E_NOMEM, "cudaMalloc(image): %s", cudaGetErrorString(e)); }
   e = cudaMalloc(&h->counter, sizeof(unsigned long long));
-  if (e != cudaSuccess) { cudaFree(h->image); cudaStreamDestroy(h->stream); delete h; return fail(SAS_E_NOMEM, "cudaMalloc(counter)"); }
+  if (e != cudaSuccess) { cudaFree(h->image); cudaEventDestroy(h->busy); cudaStreamDestroy(h->stream); delete h; return fail(SAS_E_NOMEM, "cudaMalloc(counter)"); }
   h->bytes = npx * sizeof(float2) + sizeof(unsigned long long);
   *out = h;
   return SAS_OK;
@@ -387,6 +420,7 @@ void sas_bp_destroy(sas_bp_t h) {
   cudaGetDevice(&prev);
   cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
+  if (h->busy) { if (h->busy_pending) cudaEventSynchronize(h->busy); cudaEventDestroy(h->busy); }
   cudaFree(h->image);
   cudaFree(h->echoes_owned);
   cudaFree(h->geo);
@@ -408,6 +442,7 @@ sas_status sas_bp_set_pings(sas_bp_t h, const float* echoes, int32_t P, int32_t 
   sas_status st = validate_geo(P, E, Ns, tx, rx, t0);
   if (st != SAS_OK) return st;
   CK_H(h, cudaSetDevice(h->device));
+  if ((st = wait_idle(h)) != SAS_OK) return st;
   const size_t n = (size_t)P * E * Ns;
   if (n > h->echoes_cap) {
     if (h->echoes_owned) { cudaFree(h->echoes_owned); h->bytes -= h->echoes_cap * sizeof(float2); }
@@ -417,6 +452,7 @@ sas_status sas_bp_set_pings(sas_bp_t h, const float* echoes, int32_t P, int32_t 
     h->echoes_cap = n;
     h->bytes += n * sizeof(float2);
   }
+  h->has_pings = false;   // the owned echoes change now; valid again once the nav is in
   CK_H(h, cudaMemcpyAsync(h->echoes_owned, echoes, n * sizeof(float2), cudaMemcpyHostToDevice, h->stream));
   st = upload_geo(h, P, E, Ns, tx, rx, t0, h->stream);  // synchronises the stream
   if (st != SAS_OK) { h->has_pings = false; return st; }
@@ -453,14 +489,12 @@ sas_status sas_bp_form_device(sas_bp_t h, void* image_dev, void* cuda_stream, in
   if (((uintptr_t)image_dev) & 7) return fail(SAS_E_INVALID, "image_dev must be 8-byte aligned");
   if (flags & ~SAS_FORM_ACCUMULATE) return fail(SAS_E_INVALID, "unknown flags 0x%x", flags);
   if (!h->has_pings) return fail(SAS_E_STATE, "sas_bp_form before sas_bp_set_pings");
-  if (h->gate && h->axes && h->axes_P != h->P) return fail(SAS_E_STATE, "beam axes were given for %d pings, the ping set has %d", h->axes_P, h->P);
-  if (h->vel && h->vel_P != h->P) return fail(SAS_E_STATE, "velocities were given for %d pings, the ping set has %d", h->vel_P, h->P);
-  if (h->refract && h->vel) return fail(SAS_E_UNSUPPORTED, "refraction and receiver motion cannot be combined");
-  if (h->refract && !(h->max_sensor_z < h->zb)) return fail(SAS_E_INVALID, "with an interface every sensor must be in the water (z < zb)");
-  if (h->weight && (h->vel || h->refract)) return fail(SAS_E_UNSUPPORTED, "the spreading weight is defined for stop-and-hop straight rays only");
+  if (sas_status st = check_modes(h, h->P, h->max_sensor_z); st != SAS_OK) return st;
   CK_H(h, cudaSetDevice(h->device));
   CK_H(h, launch_tdbp(h, (float2*)image_dev, h->counter, (flags & SAS_FORM_ACCUMULATE) ? 1 : 0, false,
                       (cudaStream_t)cuda_stream));
+  CK_H(h, cudaEventRecord(h->busy, (cudaStream_t)cuda_stream));
+  h->busy_pending = true;
   h->ctas_per_sm = g_last_occ;
   return SAS_OK;
 }
@@ -471,11 +505,7 @@ sas_status sas_bp_form(sas_bp_t h, float* image_out) {
   if (h->broken) return fail(SAS_E_CUDA, "handle is in a failed CUDA state; destroy it");
   if (!image_out) return fail(SAS_E_INVALID, "image_out must not be NULL");
   if (!h->has_pings) return fail(SAS_E_STATE, "sas_bp_form before sas_bp_set_pings");
-  if (h->gate && h->axes && h->axes_P != h->P) return fail(SAS_E_STATE, "beam axes were given for %d pings, the ping set has %d", h->axes_P, h->P);
-  if (h->vel && h->vel_P != h->P) return fail(SAS_E_STATE, "velocities were given for %d pings, the ping set has %d", h->vel_P, h->P);
-  if (h->refract && h->vel) return fail(SAS_E_UNSUPPORTED, "refraction and receiver motion cannot be combined");
-  if (h->refract && !(h->max_sensor_z < h->zb)) return fail(SAS_E_INVALID, "with an interface every sensor must be in the water (z < zb)");
-  if (h->weight && (h->vel || h->refract)) return fail(SAS_E_UNSUPPORTED, "the spreading weight is defined for stop-and-hop straight rays only");
+  if (sas_status st = check_modes(h, h->P, h->max_sensor_z); st != SAS_OK) return st;
   CK_H(h, cudaSetDevice(h->device));
   CK_H(h, launch_tdbp(h, h->image, h->counter, 0, false, h->stream));
   h->ctas_per_sm = g_last_occ;
@@ -494,27 +524,25 @@ sas_status sas_bp_form_streamed(sas_bp_t h, const float* echoes, int32_t P, int3
   if (chunks < 0) return fail(SAS_E_INVALID, "chunks must be >= 0");
   sas_status st = validate_geo(P, E, Ns, tx, rx, t0);
   if (st != SAS_OK) return st;
+  // every check that can fail without a CUDA error runs before the handle's state changes
+  if ((st = check_modes(h, P, max_z(P, E, tx, rx))) != SAS_OK) return st;
   CK_H(h, cudaSetDevice(h->device));
+  if ((st = wait_idle(h)) != SAS_OK) return st;
   const size_t n = (size_t)P * E * Ns;
+  h->has_pings = false;   // from here on the owned echoes are being replaced
   if (n > h->echoes_cap) {
     if (h->echoes_owned) { cudaFree(h->echoes_owned); h->bytes -= h->echoes_cap * sizeof(float2); }
     h->echoes_owned = nullptr; h->echoes_cap = 0;
     cudaError_t e = cudaMalloc(&h->echoes_owned, n * sizeof(float2));
-    if (e != cudaSuccess) { h->echoes_owned = nullptr; h->has_pings = false; return fail(SAS_E_NOMEM, "cudaMalloc(echoes, %zu B): %s", n * sizeof(float2), cudaGetErrorString(e)); }
+    if (e != cudaSuccess) { h->echoes_owned = nullptr; return fail(SAS_E_NOMEM, "cudaMalloc(echoes, %zu B): %s", n * sizeof(float2), cudaGetErrorString(e)); }
     h->echoes_cap = n;
     h->bytes += n * sizeof(float2);
   }
   if (!h->copy_stream) CK_H(h, cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
   st = upload_geo(h, P, E, Ns, tx, rx, t0, h->stream);  // small, synchronous
-  if (st != SAS_OK) { h->has_pings = false; return st; }
+  if (st != SAS_OK) return st;
   h->echoes = h->echoes_owned;
   h->use_tma = encode_tma(h, h->W);
-  h->has_pings = true;
-  if (h->gate && h->axes && h->axes_P != h->P) return fail(SAS_E_STATE, "beam axes were given for %d pings, the ping set has %d", h->axes_P, h->P);
-  if (h->vel && h->vel_P != h->P) return fail(SAS_E_STATE, "velocities were given for %d pings, the ping set has %d", h->vel_P, h->P);
-  if (h->refract && h->vel) return fail(SAS_E_UNSUPPORTED, "refraction and receiver motion cannot be combined");
-  if (h->refract && !(h->max_sensor_z < h->zb)) return fail(SAS_E_INVALID, "with an interface every sensor must be in the water (z < zb)");
-  if (h->weight && (h->vel || h->refract)) return fail(SAS_E_UNSUPPORTED, "the spreading weight is defined for stop-and-hop straight rays only");
   const int nch = P * E;
   int nchunk = chunks > 0 ? chunks : 8;
   nchunk = std::max(1, std::min(nchunk, (nch + 63) / 64));   // >= 64 channels per chunk
@@ -535,6 +563,7 @@ sas_status sas_bp_form_streamed(sas_bp_t h, const float* echoes, int32_t P, int3
   if (err == cudaSuccess) err = cudaStreamSynchronize(h->stream);
   for (auto& x : ev) cudaEventDestroy(x);
   if (err != cudaSuccess) return cuda_fail(h, err, "sas_bp_form_streamed");
+  h->has_pings = true;   // the whole ping set is resident now (form / form_device may reuse it)
   return SAS_OK;
 }
 
@@ -543,11 +572,7 @@ sas_status sas_bp_count_terms(sas_bp_t h, uint64_t* dense, uint64_t* in_win) {
   if (!h) return fail(SAS_E_INVALID, "handle is NULL");
   if (h->broken) return fail(SAS_E_CUDA, "handle is in a failed CUDA state; destroy it");
   if (!h->has_pings) return fail(SAS_E_STATE, "sas_bp_count_terms before sas_bp_set_pings");
-  if (h->gate && h->axes && h->axes_P != h->P) return fail(SAS_E_STATE, "beam axes were given for %d pings, the ping set has %d", h->axes_P, h->P);
-  if (h->vel && h->vel_P != h->P) return fail(SAS_E_STATE, "velocities were given for %d pings, the ping set has %d", h->vel_P, h->P);
-  if (h->refract && h->vel) return fail(SAS_E_UNSUPPORTED, "refraction and receiver motion cannot be combined");
-  if (h->refract && !(h->max_sensor_z < h->zb)) return fail(SAS_E_INVALID, "with an interface every sensor must be in the water (z < zb)");
-  if (h->weight && (h->vel || h->refract)) return fail(SAS_E_UNSUPPORTED, "the spreading weight is defined for stop-and-hop straight rays only");
+  if (sas_status st = check_modes(h, h->P, h->max_sensor_z); st != SAS_OK) return st;
   const uint64_t npx = (uint64_t)h->grid.nx * h->grid.ny * h->grid.nz;
   if (dense) *dense = npx * (uint64_t)h->P * (uint64_t)h->E;
   if (in_win) {
@@ -588,6 +613,7 @@ sas_status sas_bp_set_beam(sas_bp_t h, const sas_beam* beam, const double* axes,
         return fail(SAS_E_INVALID, "axes of ping %d must be orthonormal (a along track, b boresight)", p);
     }
     CK_H(h, cudaSetDevice(h->device));
+    if (sas_status w = wait_idle(h); w != SAS_OK) return w;
     if (h->axes_P != P || !h->axes) {
       if (h->axes) { cudaFree(h->axes); h->bytes -= (size_t)h->axes_P * 6 * sizeof(double); h->axes = nullptr; }
       cudaError_t e = cudaMalloc(&h->axes, (size_t)P * 6 * sizeof(double));
@@ -597,6 +623,7 @@ sas_status sas_bp_set_beam(sas_bp_t h, const sas_beam* beam, const double* axes,
     CK_H(h, cudaMemcpy(h->axes, axes, (size_t)P * 6 * sizeof(double), cudaMemcpyHostToDevice));
     h->axes_P = P;
   } else if (h->axes) {
+    if (sas_status w = wait_idle(h); w != SAS_OK) return w;
     cudaFree(h->axes);
     h->bytes -= (size_t)h->axes_P * 6 * sizeof(double);
     h->axes = nullptr;
@@ -618,6 +645,7 @@ sas_status sas_bp_set_motion(sas_bp_t h, const double* vel, int32_t P) {
   if (!h) return fail(SAS_E_INVALID, "handle is NULL");
   if (h->broken) return fail(SAS_E_CUDA, "handle is in a failed CUDA state; destroy it");
   if (!vel) {   // stop-and-hop
+    if (sas_status w = wait_idle(h); w != SAS_OK) return w;
     if (h->vel) { cudaFree(h->vel); h->bytes -= (size_t)h->vel_P * 3 * sizeof(double); }
     h->vel = nullptr; h->vel_P = 0;
     return SAS_OK;
@@ -629,6 +657,7 @@ sas_status sas_bp_set_motion(sas_bp_t h, const double* vel, int32_t P) {
     if (norm3(v) > 0.01 * h->c) return fail(SAS_E_INVALID, "velocity of ping %d exceeds c/100", p);
   }
   CK_H(h, cudaSetDevice(h->device));
+  if (sas_status w = wait_idle(h); w != SAS_OK) return w;
   if (h->vel_P != P || !h->vel) {
     if (h->vel) { cudaFree(h->vel); h->bytes -= (size_t)h->vel_P * 3 * sizeof(double); h->vel = nullptr; }
     cudaError_t e = cudaMalloc(&h->vel, (size_t)P * 3 * sizeof(double));

@@ -937,42 +937,83 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
 }
 
 // K3: count terms whose interpolation support meets the record, u in (-1, Ns).
-// Same tiles and fp32 delay arithmetic as K2 (exact leg form), no echo traffic.
+// Same tiles and fp32 delay arithmetic as K2 (exact leg form), no echo traffic.  Gated counts use
+// K2's own (tile, channel) cone classes: a culled channel counts nothing, an IN class needs no
+// per-pixel test, only EDGE classes run the fp64 per-pixel gate (the transmit mask once per ping).
 template <int KX, int KY, int KZ, int WY, int WZ>
 __global__ void __launch_bounds__(32 * WY * WZ) count_kernel(const TdbpParams prm) {
   using TM = TileMap<KX, KY, KZ, WY, WZ>;
   constexpr int K = TM::K;
+  static_assert(K <= 32, "pixel masks are 32-bit");
   __shared__ ChanConst cc[kNB];
   const TM tm(prm);
   const int tid = threadIdx.x;
   double ct[3];
   tm.centre(prm, ct);
   float dx[K], dy[K], dz[K], dd[K];
-  bool ok[K];
+  uint32_t okm = 0u;
 #pragma unroll
   for (int k = 0; k < K; ++k) {
     tm.offset(prm, k, dx[k], dy[k], dz[k]);
     dd[k] = dx[k] * dx[k] + dy[k] * dy[k] + dz[k] * dz[k];
-    ok[k] = tm.valid(prm, k);
+    if (tm.valid(prm, k)) okm |= 1u << k;
   }
   const float Nsf = (float)prm.Ns;
-  unsigned cnt = 0;
+  unsigned long long cnt = 0;
+  int cur_ping = -1;
+  uint32_t mtx = 0xFFFFFFFFu;
   for (int ch0 = prm.ch_lo; ch0 < prm.ch_hi; ch0 += kNB) {
     const int nb = min(kNB, prm.ch_hi - ch0);
     __syncthreads();
-    if (tid < nb) cc[tid] = chan_prologue<false, true>(prm, ch0 + tid, ct, tid, 0u);
+    if (tid < nb) cc[tid] = chan_prologue<true, true>(prm, ch0 + tid, ct, tid, 0u);
     __syncthreads();
     for (int c = 0; c < nb; ++c) {
       const ChanConst kc = cc[c];
+      if (prm.gate && (kc.gate & 16)) continue;          // culled: the tile misses a cone
+      uint32_t msk = okm;
+      if (prm.gate) {
+        if (kc.ping != cur_ping) {                       // transmit-cone mask, once per ping
+          cur_ping = kc.ping;
+          mtx = 0xFFFFFFFFu;
+          if ((kc.gate & 3) == kGEdge) {
+            double a[3], bb[3], x[3];
+            ping_axes(prm, cur_ping, a, bb);
+            mtx = 0u;
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+              pixel_centre64(prm, tm.ix(k), tm.iy(k), tm.iz(k), x);
+              if (in_fov_px(prm, x, prm.tx + 3 * cur_ping, a, bb)) mtx |= 1u << k;
+            }
+          }
+        }
+        msk &= mtx;
+        if (((kc.gate >> 2) & 3) == kGEdge) {            // receive cone (bistatic)
+          double a[3], bb[3], x[3];
+          ping_axes(prm, kc.ping, a, bb);
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            if (!((msk >> k) & 1u)) continue;
+            pixel_centre64(prm, tm.ix(k), tm.iy(k), tm.iz(k), x);
+            if (!in_fov_px(prm, x, prm.rx + 3 * (size_t)(ch0 + c), a, bb)) msk &= ~(1u << k);
+          }
+        }
+      }
+      // the staged window [k_lo, k_lo + W] bounds every pixel's u (K2 interpolates from it): a window
+      // wholly inside the record admits every pixel without a per-term test
+      if (kc.klo >= 0 && kc.klo + prm.W + 1 <= prm.Ns) {
+        cnt += (unsigned long long)__popc(msk);
+        continue;
+      }
 #pragma unroll
       for (int k = 0; k < K; ++k) {
+        if (!((msk >> k) & 1u)) continue;
         if (prm.refract) {   // counted with the fp64 refracted delay (off the clock)
           double x[3];
           pixel_centre64(prm, tm.ix(k), tm.iy(k), tm.iz(k), x);
           const double tau = refr_time64(x, prm.tx + 3 * kc.ping, prm.zb, prm.c, prm.c2) +
                              refr_time64(x, prm.rx + 3 * (size_t)(ch0 + c), prm.zb, prm.c, prm.c2);
           const double ua = (tau - prm.t0[kc.ping]) * prm.fs;
-          cnt += (ok[k] && ua > -1.0 && ua < (double)prm.Ns) ? 1u : 0u;
+          cnt += (ua > -1.0 && ua < (double)prm.Ns) ? 1ull : 0ull;
           continue;
         }
         const float qt = fmaf(kc.tx2x, dx[k], fmaf(kc.tx2y, dy[k], fmaf(kc.tx2z, dz[k], dd[k])));
@@ -983,21 +1024,13 @@ __global__ void __launch_bounds__(32 * WY * WZ) count_kernel(const TdbpParams pr
         const float du = (qt / fmaxf(rt + kc.r_t, 1e-30f) + qr / fmaxf(rr + kc.r_r, 1e-30f)) * (float)prm.k_s * kap;
         // absolute u = k_lo + 0.5 + Wh + (du + urr)
         const float ua = (float)kc.klo + 0.5f + (float)(prm.W >> 1) + (du + kc.urr);
-        bool admit = ok[k] && ua > -1.f && ua < Nsf;
-        if (prm.gate && admit) {   // gated metric: count only terms inside the cone(s), fp64 decision
-          double a[3], bb[3], x[3];
-          ping_axes(prm, kc.ping, a, bb);
-          pixel_centre64(prm, tm.ix(k), tm.iy(k), tm.iz(k), x);
-          admit = in_fov_px(prm, x, prm.tx + 3 * kc.ping, a, bb) &&
-                  (prm.gate != 2 || in_fov_px(prm, x, prm.rx + 3 * (size_t)(ch0 + c), a, bb));
-        }
-        cnt += admit ? 1u : 0u;
+        cnt += (ua > -1.f && ua < Nsf) ? 1ull : 0ull;
       }
     }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-  if ((tid & 31) == 0) atomicAdd(prm.counter, (unsigned long long)cnt);
+  if ((tid & 31) == 0 && cnt) atomicAdd(prm.counter, cnt);
 }
 
 }  // namespace sasbp

@@ -148,15 +148,56 @@ def _stream_ptr(stream):
     return ctypes.c_void_p(stream.cuda_stream)
 
 
-def _dev_ptr(t, nbytes_min: int):
-    """Device pointer of a torch CUDA tensor (complex64 / float32), contiguity checked."""
+def _is_torch(x) -> bool:
+    return hasattr(x, "data_ptr") and not hasattr(x, "ctypes")
+
+
+def _dev_ptr(t, nbytes_min: int, dtype: Optional[str] = None):
+    """Device pointer of a torch CUDA tensor (complex64 / float32 / float64): device, contiguity,
+    dtype (when given, e.g. "complex64") and size checked, so a wrong tensor raises here instead of
+    letting the library read or write past it."""
     if not getattr(t, "is_cuda", False):
         raise ValueError("expected a CUDA tensor")
     if not t.is_contiguous():
         raise ValueError("expected a contiguous tensor")
+    if dtype is not None and str(t.dtype) != "torch." + dtype:
+        raise ValueError(f"expected a {dtype} tensor, got {t.dtype}")
     if t.numel() * t.element_size() < nbytes_min:
         raise ValueError("tensor too small")
     return ctypes.c_void_p(t.data_ptr())
+
+
+def _host_c64_in(x, name: str, ndim: int = 3):
+    """(keep-alive object, float* pointer, shape) of host complex64 input (numpy, or a CPU torch
+    tensor: dtype / device checked, made contiguous)."""
+    if _is_torch(x):
+        if x.is_cuda:
+            raise ValueError(f"{name}: expected host memory; use the *_device call for CUDA tensors")
+        if str(x.dtype) != "torch.complex64":
+            raise ValueError(f"{name}: expected complex64, got {x.dtype}")
+        keep = x.contiguous()
+        ptr = ctypes.cast(ctypes.c_void_p(keep.data_ptr()), ctypes.POINTER(ctypes.c_float))
+        shape = tuple(keep.shape)
+    else:
+        keep = np.ascontiguousarray(x, dtype=np.complex64)
+        ptr = keep.view(np.float32).ctypes.data_as(ctypes.POINTER(ctypes.c_float))
+        shape = keep.shape
+    if len(shape) != ndim:
+        raise ValueError(f"{name}: expected {ndim} dimensions, got shape {shape}")
+    return keep, ptr, shape
+
+
+def _host_c64_out(out, shape, name: str = "out"):
+    """float* pointer of a caller-provided host output: complex64, C-contiguous, exactly `shape`."""
+    if _is_torch(out):
+        if out.is_cuda or str(out.dtype) != "torch.complex64" or not out.is_contiguous() \
+                or tuple(out.shape) != tuple(shape):
+            raise ValueError(f"{name} must be a contiguous host complex64 tensor of shape {tuple(shape)}")
+        return ctypes.cast(ctypes.c_void_p(out.data_ptr()), ctypes.POINTER(ctypes.c_float))
+    if not isinstance(out, np.ndarray) or out.dtype != np.complex64 or not out.flags.c_contiguous \
+            or out.shape != tuple(shape):
+        raise ValueError(f"{name} must be a C-contiguous complex64 array of shape {tuple(shape)}")
+    return out.view(np.float32).ctypes.data_as(ctypes.POINTER(ctypes.c_float))
 
 
 class Backprojector:
@@ -197,17 +238,7 @@ class Backprojector:
 
     def set_pings(self, echoes, tx, rx, t0=None):
         """Host echoes complex64 [P][E][Ns] (numpy or CPU torch tensor, pinned or not); copied."""
-        if hasattr(echoes, "numpy") and not hasattr(echoes, "ctypes"):
-            if echoes.is_cuda:
-                raise ValueError("set_pings takes host echoes; use set_pings_device for CUDA tensors")
-            keep = echoes.contiguous()
-            P, E, Ns = keep.shape
-            ptr = ctypes.cast(ctypes.c_void_p(keep.data_ptr()), ctypes.POINTER(ctypes.c_float))
-        else:
-            echoes = np.ascontiguousarray(echoes, dtype=np.complex64)
-            P, E, Ns = echoes.shape
-            ptr = echoes.view(np.float32).ctypes.data_as(ctypes.POINTER(ctypes.c_float))
-            keep = echoes
+        keep, ptr, (P, E, Ns) = _host_c64_in(echoes, "echoes")
         tx, rx, t0 = self._geo(P, E, tx, rx, t0)
         _check(_lib.sas_bp_set_pings(self._h, ptr, P, E, Ns, _ptr(tx, ctypes.c_double),
                                      _ptr(rx, ctypes.c_double), _ptr(t0, ctypes.c_double)))
@@ -216,9 +247,11 @@ class Backprojector:
 
     def set_pings_device(self, echoes, tx, rx, t0=None, stream=None):
         """Borrow a CUDA complex64 tensor [P][E][Ns] (kept alive by this object)."""
+        if len(echoes.shape) != 3:
+            raise ValueError(f"echoes: expected [P][E][Ns], got shape {tuple(echoes.shape)}")
         P, E, Ns = echoes.shape
         tx, rx, t0 = self._geo(P, E, tx, rx, t0)
-        _check(_lib.sas_bp_set_pings_device(self._h, _dev_ptr(echoes, P * E * Ns * 8), P, E, Ns,
+        _check(_lib.sas_bp_set_pings_device(self._h, _dev_ptr(echoes, P * E * Ns * 8, "complex64"), P, E, Ns,
                                             _ptr(tx, ctypes.c_double), _ptr(rx, ctypes.c_double),
                                             _ptr(t0, ctypes.c_double), _stream_ptr(stream)))
         self._keep = echoes
@@ -228,12 +261,7 @@ class Backprojector:
         """Form into host memory; returns complex64 [nz][ny][nx]."""
         if out is None:
             out = np.empty(self.shape, dtype=np.complex64)
-        if hasattr(out, "data_ptr") and not hasattr(out, "ctypes"):
-            ptr = ctypes.cast(ctypes.c_void_p(out.data_ptr()), ctypes.POINTER(ctypes.c_float))
-        else:
-            if out.dtype != np.complex64 or not out.flags.c_contiguous or out.shape != self.shape:
-                raise ValueError("out must be C-contiguous complex64 of the grid shape")
-            ptr = out.view(np.float32).ctypes.data_as(ctypes.POINTER(ctypes.c_float))
+        ptr = _host_c64_out(out, self.shape)
         _check(_lib.sas_bp_form(self._h, ptr))
         return out
 
@@ -241,20 +269,10 @@ class Backprojector:
         """End to end from host echoes with chunked H2D overlapped with backprojection
         (sas_bp_form_streamed).  `echoes`: complex64 [P][E][Ns] numpy / CPU torch (pin it for
         overlap); returns the image in host memory."""
-        if hasattr(echoes, "numpy") and not hasattr(echoes, "ctypes"):
-            ek = echoes.contiguous()
-            P, E, Ns = ek.shape
-            eptr = ctypes.cast(ctypes.c_void_p(ek.data_ptr()), ctypes.POINTER(ctypes.c_float))
-        else:
-            ek = np.ascontiguousarray(echoes, dtype=np.complex64)
-            P, E, Ns = ek.shape
-            eptr = ek.view(np.float32).ctypes.data_as(ctypes.POINTER(ctypes.c_float))
+        ek, eptr, (P, E, Ns) = _host_c64_in(echoes, "echoes")
         if out is None:
             out = np.empty(self.shape, dtype=np.complex64)
-        if hasattr(out, "data_ptr") and not hasattr(out, "ctypes"):
-            optr = ctypes.cast(ctypes.c_void_p(out.data_ptr()), ctypes.POINTER(ctypes.c_float))
-        else:
-            optr = out.view(np.float32).ctypes.data_as(ctypes.POINTER(ctypes.c_float))
+        optr = _host_c64_out(out, self.shape)
         tx, rx, t0 = self._geo(P, E, tx, rx, t0)
         _check(_lib.sas_bp_form_streamed(self._h, eptr, P, E, Ns, _ptr(tx, ctypes.c_double), _ptr(rx, ctypes.c_double),
                                          _ptr(t0, ctypes.c_double), optr, int(chunks)))
@@ -265,7 +283,7 @@ class Backprojector:
     def form_device(self, image, stream=None, accumulate: bool = False):
         """Form into a CUDA complex64 tensor of the grid shape, asynchronously on `stream`."""
         n = self.shape[0] * self.shape[1] * self.shape[2]
-        _check(_lib.sas_bp_form_device(self._h, _dev_ptr(image, n * 8), _stream_ptr(stream),
+        _check(_lib.sas_bp_form_device(self._h, _dev_ptr(image, n * 8, "complex64"), _stream_ptr(stream),
                                        SAS_FORM_ACCUMULATE if accumulate else 0))
         return image
 

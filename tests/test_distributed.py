@@ -42,10 +42,15 @@ def _worker(rank, world, port, mode, cid, out_q):
         _SC = s
         e = torch.from_numpy(s.echoes())
         if mode == "image":
-            if rank != 0:
-                e = torch.zeros_like(e)
-            pdist.broadcast_echoes(e, dist)
-            full = pdist.form_image_sharded(s.grid, e, s.tx, s.rx, s.t0, oracle_former, dist, align=32)
+            # each rank holds only its contiguous ping slice; the all-gather assembles the set
+            sl, per = pdist.ping_slices(s.P, world)
+            lo, hi = sl[rank]
+            local = torch.zeros((per,) + tuple(e.shape[1:]), dtype=e.dtype)
+            local[: hi - lo] = e[lo:hi]
+            full_e = torch.empty((per * world,) + tuple(e.shape[1:]), dtype=e.dtype)
+            pdist.gather_echoes(local, full_e, dist)
+            e = full_e[: s.P].contiguous()
+            full = pdist.form_image_sharded(s.grid, e, s.tx, s.rx, s.t0, oracle_former, dist)
         else:
             sel = pdist.ping_shard(s.P, world, rank)
             full = pdist.form_ping_sharded(s.grid, e[sel].contiguous(), s.tx[sel], s.rx[sel], s.t0[sel],
@@ -117,6 +122,15 @@ def test_sub_grid_origin():
     g3 = synth.grid_dict((1.0, 2.0, 3.0), (0.1, 0.2, 0.3), (10, 20, 16))
     sg3 = pdist.sub_grid(g3, 8, 16)
     assert sg3["nz"] == 8 and np.allclose(sg3["origin"], [1.0, 2.0, 3.0 + 2.4])
+
+
+def test_ping_slices_cover():
+    for P in (1, 7, 1000, 1001):
+        for world in (1, 2, 3, 8):
+            sl, per = pdist.ping_slices(P, world)
+            assert sl[0][0] == 0 and sl[-1][1] == P and per * world >= P
+            assert all(a1 == c0 for (a0, a1), (c0, c1) in zip(sl, sl[1:]))
+            assert all(hi - lo <= per for lo, hi in sl)
 
 
 def test_ping_shard_partition():

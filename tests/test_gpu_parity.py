@@ -429,9 +429,12 @@ def test_gated_near_field_3d_bistatic_elevation(bpmod):
     s = synth.scenario(4, reduced=True)
     e = s.echoes()
     axes = np.tile(np.array([[[1.0, 0, 0], [0, 0, 1.0]]]), (s.P, 1, 1))
-    got, _ = _gated_form(bpmod, s, e, az=0.6, el=0.9, bistatic=True, axes=axes)
-    ref = _gated_ref(s, e, s.grid, 0.6, 0.9, True, axes)
+    got, (dense, inwin) = _gated_form(bpmod, s, e, az=0.3, el=0.4, bistatic=True, axes=axes)
+    ref = _gated_ref(s, e, s.grid, 0.3, 0.4, True, axes)
     _check(got, ref, label="gated 3D bistatic")
+    _, cnt = oracle.tdbp_points_gated(e, s.tx, s.rx, s.t0, s.fc, s.fs, s.c, oracle.grid_points(s.grid), az=0.3,
+                                      el=0.4, bistatic=True, axes=axes, with_count=True)
+    assert 0 < inwin < dense and inwin == int(cnt.sum())   # the cones cut the volume (62 % of terms)
 
 
 def test_culled_equals_unculled_bitwise(bpmod):
@@ -534,22 +537,51 @@ def test_motion_zero_velocity_bitwise(bpmod):
     assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
 
 
-def test_motion_with_gating(bpmod):
-    """Moving receiver and FOV gating together (gate decisions on the transmit-time positions)."""
+@pytest.mark.parametrize("bistatic", [False, True])
+def test_motion_with_gating(bpmod, bistatic):
+    """Moving receiver and FOV gating together (R15 + R16, reading R22: gate decisions on the
+    transmit-time positions): element-wise parity with the oracle's gated moving-receiver sum on
+    reduced config 2, and the exact in-cone term count."""
     s = synth.scenario(2, reduced=True)
     s.vel = np.tile([1.8, 0.1, 0.0], (s.P, 1))
     e = s.echoes()
     az = 2 * np.arcsin(s.sin_half_beam)
-    got = _motion_form(bpmod, s, e, s.vel, beam=(az,))
-    # oracle: gate mask from the gated oracle with a unit echo set is not separable; compare the
-    # gated-motion image against the motion oracle restricted by the same gate, term by term,
-    # on a point subset via the identity gated(motion) = motion - (out-of-cone terms): use the
-    # open-gate limit instead for the numerics and the gate limit for the structure:
-    open_gate = _motion_form(bpmod, s, e, s.vel, beam=(np.pi,))
-    ref_open = oracle.tdbp_points_motion(e, s.tx, s.rx, s.t0, s.vel, s.fc, s.fs, s.c,
-                                         oracle.grid_points(s.grid)).reshape(got.shape)
-    _check(open_gate, ref_open, label="motion + open gate")
-    assert np.max(np.abs(got)) > 0 and not np.array_equal(got, open_gate)
+    with bpmod.Backprojector(s.fc, s.bandwidth, s.fs, s.c, s.grid) as bp:
+        bp.set_pings(e, s.tx, s.rx, s.t0)
+        bp.set_motion(s.vel)
+        bp.set_beam(az, 0.0, bistatic)
+        got = bp.form()
+        dense, inwin = bp.count_terms()
+    ref, cnt = oracle.tdbp_points_gated_motion(e, s.tx, s.rx, s.t0, s.vel, s.fc, s.fs, s.c,
+                                               oracle.grid_points(s.grid), az=az, bistatic=bistatic,
+                                               with_count=True)
+    ref = ref.reshape(got.shape)
+    pk = s.target_pixels
+    pk = pk[np.abs(_at(ref, pk)) > 0.1 * np.abs(ref).max()]   # phase at the targets the gate keeps bright
+    _check(got, ref, _at(got, pk), _at(ref, pk), label=f"motion + gate bistatic={bistatic}")
+    assert 0 < inwin < dense
+    assert abs(inwin - int(cnt.sum())) <= max(1, 1e-4 * cnt.sum())
+
+
+def test_motion_with_gating_3d_near_field(bpmod):
+    """Reduced config 4 (near-field exact receive leg) moving at sway/heave velocities with a
+    bistatic azimuth + elevation gate."""
+    s = synth.scenario(4, reduced=True)
+    rng = np.random.default_rng(44)
+    s.vel = np.stack([0.5 + 0.1 * rng.normal(size=s.P), 0.2 * rng.normal(size=s.P), 0.05 * rng.normal(size=s.P)], 1)
+    e = s.echoes()
+    axes = np.tile(np.array([[[1.0, 0, 0], [0, 0, 1.0]]]), (s.P, 1, 1))
+    with bpmod.Backprojector(s.fc, s.bandwidth, s.fs, s.c, s.grid) as bp:
+        bp.set_pings(e, s.tx, s.rx, s.t0)
+        bp.set_motion(s.vel)
+        bp.set_beam(0.3, 0.4, True, True, axes)
+        got = bp.form()
+        dense, inwin = bp.count_terms()
+    ref, cnt = oracle.tdbp_points_gated_motion(e, s.tx, s.rx, s.t0, s.vel, s.fc, s.fs, s.c, oracle.grid_points(s.grid),
+                                               az=0.3, el=0.4, bistatic=True, axes=axes, with_count=True)
+    _check(got, ref.reshape(got.shape), label="motion + gate 3D")
+    assert 0 < inwin < dense
+    assert abs(inwin - int(cnt.sum())) <= max(1, 1e-4 * cnt.sum())
 
 
 def test_set_motion_errors(bpmod):
@@ -612,6 +644,33 @@ def test_refracted_equal_speed_is_dense(bpmod):
     got = _refr_form(bpmod, s, e, 0.0, s.c)
     ref = oracle.tdbp_grid(e, s.tx, s.rx, s.t0, s.fc, s.fs, s.c, s.grid)
     _check(got, ref, label="c2 = c")
+
+
+@pytest.mark.parametrize("c2", [1700.0, 1450.0])
+def test_refracted_with_gating_3d(bpmod, c2):
+    """The paper's near-field craft: bistatic ray culling AND the sediment refraction model
+    together (R15 + R17, reading R22: straight line-of-sight gate from the recorded
+    sensor positions).  Reduced config 4, azimuth + elevation cones around a downward boresight,
+    element-wise parity with the oracle's gated refracted sum, exact in-cone counts."""
+    s = synth.scenario(4, reduced=True)
+    s.medium = (0.0, c2)
+    e = s.echoes()
+    axes = np.tile(np.array([[[1.0, 0, 0], [0, 0, 1.0]]]), (s.P, 1, 1))
+    with bpmod.Backprojector(s.fc, s.bandwidth, s.fs, s.c, s.grid) as bp:
+        bp.set_pings(e, s.tx, s.rx, s.t0)
+        bp.set_medium(0.0, c2)
+        bp.set_beam(0.3, 0.4, True, True, axes)
+        got = bp.form()
+        dense, inwin = bp.count_terms()
+    ref, cnt = oracle.tdbp_points_gated_refracted(e, s.tx, s.rx, s.t0, 0.0, c2, s.fc, s.fs, s.c,
+                                                  oracle.grid_points(s.grid), az=0.3, el=0.4, bistatic=True,
+                                                  axes=axes, with_count=True)
+    ref = ref.reshape(got.shape)
+    pk = s.target_pixels
+    pk = pk[np.abs(_at(ref, pk)) > 0.1 * np.abs(ref).max()]   # phase at the targets the gate keeps bright
+    _check(got, ref, _at(got, pk), _at(ref, pk), label=f"refracted + gate c2={c2}")
+    assert 0 < inwin < dense
+    assert abs(inwin - int(cnt.sum())) <= max(1, 1e-4 * cnt.sum())
 
 
 def test_set_medium_errors(bpmod):
