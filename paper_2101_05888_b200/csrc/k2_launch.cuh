@@ -19,6 +19,7 @@ enum K2Variant { kV2D = 0, kV2D_DZ = 1, kV3D = 2 };
 
 struct K2Launch {
   bool tma;          // TMA row staging (else cp.async)
+  bool axis;         // 3D grid with diagonal steps: compact per-pixel geometry (AXIS instantiations, TMA only)
   int mode;          // receive-leg mode (kSeries3 / kSeries4 / kExact); prm.refract selects kRefract
   bool count;        // K3 instead of K2
   cudaStream_t st;
@@ -61,6 +62,13 @@ cudaError_t launch_family(const TdbpParams& prm, const TmaDesc& tmap, const K2La
   if (WEIGHT) {   // spreading weight (R18): stop-and-hop, straight rays only (checked on the host)
     if (prm.vel || prm.refract) return cudaErrorNotSupported;
     auto go = [&](auto kern) { return launch_k(kern, nt, prm, tmap, smem, L); };
+    if constexpr (KZ > 1) if (L.tma && L.axis) {   // compact geometry: 3D volumes only
+      switch (L.mode) {
+        case kSeries3: return go(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kSeries3, true, GATE, false, true, WEIGHT>);
+        case kSeries4: return go(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kSeries4, true, GATE, false, true, WEIGHT>);
+        default: return go(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kExact, true, GATE, false, true, WEIGHT>);
+      }
+    }
     if (L.tma) {
       switch (L.mode) {
         case kSeries3: return go(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kSeries3, true, GATE, false, false, WEIGHT>);
@@ -74,23 +82,26 @@ cudaError_t launch_family(const TdbpParams& prm, const TmaDesc& tmap, const K2La
       default: return go(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kExact, false, GATE, false, false, WEIGHT>);
     }
   }
-  auto pick = [&](auto tma_tag, auto motion_tag) -> cudaError_t {
+  auto pick = [&](auto tma_tag, auto motion_tag, auto axis_tag) -> cudaError_t {
     constexpr bool T = decltype(tma_tag)::value;
     constexpr bool M = decltype(motion_tag)::value;
+    constexpr bool AX = decltype(axis_tag)::value;
     if (prm.refract) {
       if (M) return cudaErrorNotSupported;   // rejected on the host before launch
-      return launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kRefract, T, GATE, false>, nt, prm, tmap, smem, L);
+      return launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kRefract, T, GATE, false, AX>, nt, prm, tmap, smem, L);
     }
     switch (L.mode) {
-      case kSeries3: return launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kSeries3, T, GATE, M>, nt, prm, tmap, smem, L);
-      case kSeries4: return launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kSeries4, T, GATE, M>, nt, prm, tmap, smem, L);
-      default: return launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kExact, T, GATE, M>, nt, prm, tmap, smem, L);
+      case kSeries3: return launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kSeries3, T, GATE, M, AX>, nt, prm, tmap, smem, L);
+      case kSeries4: return launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kSeries4, T, GATE, M, AX>, nt, prm, tmap, smem, L);
+      default: return launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kExact, T, GATE, M, AX>, nt, prm, tmap, smem, L);
     }
   };
   using TT = std::true_type;
   using FF = std::false_type;
-  if (L.tma) return prm.vel ? pick(TT{}, TT{}) : pick(TT{}, FF{});
-  return prm.vel ? pick(FF{}, TT{}) : pick(FF{}, FF{});
+  if constexpr (KZ > 1)   // compact geometry: 3D volumes only
+    if (L.tma && L.axis) return prm.vel ? pick(TT{}, TT{}, TT{}) : pick(TT{}, FF{}, TT{});
+  if (L.tma) return prm.vel ? pick(TT{}, TT{}, FF{}) : pick(TT{}, FF{}, FF{});
+  return prm.vel ? pick(FF{}, TT{}, FF{}) : pick(FF{}, FF{}, FF{});
 }
 
 // entry points, one per translation unit (k2_*.cu)
@@ -121,4 +132,13 @@ cudaError_t k2_launch_3d_w(const TdbpParams& prm, const TmaDesc& tmap, const K2L
 #else
 #define SASBP_T2D SASBP_KX2D, SASBP_KY2D, 1, SASBP_WY2D, 1
 #endif
-#define SASBP_T3D 2, 2, 2, 1, 4
+#ifndef SASBP_KY3D
+#define SASBP_KY3D 2   // voxels per thread along y (3D)
+#endif
+#ifndef SASBP_KZ3D
+#define SASBP_KZ3D 2   // voxels per thread along z (3D); KY3D * KZ3D = 4 (8 voxels per thread)
+#endif
+#ifndef SASBP_WZ3D
+#define SASBP_WZ3D 4   // warps per 3D CTA, stacked along z
+#endif
+#define SASBP_T3D 2, SASBP_KY3D, SASBP_KZ3D, 1, SASBP_WZ3D

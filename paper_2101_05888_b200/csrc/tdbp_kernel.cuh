@@ -42,6 +42,9 @@ namespace sasbp {
 #ifndef SASBP_MINB
 #define SASBP_MINB 4   // resident 4-warp CTAs per SM the register allocation targets
 #endif
+#ifndef SASBP_MINB_AXIS
+#define SASBP_MINB_AXIS 4   // the same for axis-aligned grids (A/B on config 4: 5 CTAs/SM -0.7 %)
+#endif
 #ifndef SASBP_CUNROLL2
 #define SASBP_CUNROLL2 0
 #endif
@@ -516,12 +519,14 @@ __device__ __forceinline__ void tma_load_row(uint32_t dst, const void* tmap, int
 // Ns); box = box_samples(W) x 1; out-of-bounds samples read as zero (reading R2).
 struct __align__(64) TmaDesc { unsigned char bytes[128]; };
 
-// HAS_DZ = false means the grid is a z-level plane (step_x, step_y have no z component); then
-// both pixels of an x-pair share their y offset whenever step_x has no y component (AXIS).
+// HAS_DZ = false means the grid is a z-level plane (step_x, step_y have no z component).  AXIS =
+// true for grids with diagonal steps (each step along its own axis): the pixel offsets are kept
+// per column / row / plane instead of per pixel pair (fewer registers, same arithmetic).
 // WEIGHT = true multiplies every term by the spreading weight R_tx R_rx (NEXT-4, reading R18).
 template <int KX, int KY, int KZ, int WY, int WZ, bool HAS_DZ, int MODE, bool USE_TMA, bool GATE = false,
           bool MOTION = false, bool AXIS = false, bool WEIGHT = false>
-__global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp_kernel(const TdbpParams prm,
+__global__ void __launch_bounds__(32 * WY * WZ, (AXIS ? SASBP_MINB_AXIS : SASBP_MINB) * 4 / (WY * WZ))
+    tdbp_kernel(const TdbpParams prm,
                                                                           const __grid_constant__ TmaDesc tmap) {
   using TM = TileMap<KX, KY, KZ, WY, WZ>;
   constexpr int NP = TM::NP;
@@ -545,8 +550,13 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
   double ct[3];
   tm.centre(prm, ct);
 
-  float2 DX[NP], DY[NP], DZ[NP], DD[NP], BT[NP];
-  float DYS[NP];
+  // Per-pixel geometry.  General grids keep the offsets of every pixel pair; axis-aligned grids
+  // (diagonal steps, AXIS) keep dx per x-pair column, dy per ky row and dz per kz plane -- the
+  // same arithmetic from ~20 fewer registers (occupancy).  Pixel k = ((kz KY + ky) KX + kx), pair
+  // p = k / 2: x-pair column p % NXP, row (p / NXP) % KY, plane p / (NXP KY).
+  constexpr int NXP = KX / 2;
+  float2 DX[AXIS ? NXP : NP], DY[AXIS ? 1 : NP], DZ[AXIS ? 1 : NP], DD[NP], BT[NP];
+  float DYA[AXIS ? KY : 1], DZA[AXIS ? KZ : 1];
   float2 A[2 * NP], B[2 * NP];
 #pragma unroll
   for (int p = 0; p < NP; ++p) {
@@ -554,12 +564,18 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
     tm.offset(prm, 2 * p, dx0, dy0, dz0);
     tm.offset(prm, 2 * p + 1, dx1, dy1, dz1);
     if (!HAS_DZ) { dz0 = 0.f; dz1 = 0.f; }
-    DX[p] = make_float2(dx0, dx1); DY[p] = make_float2(dy0, dy1); DZ[p] = make_float2(dz0, dz1);
-    DYS[p] = dy0;
+    if constexpr (AXIS) {
+      DX[p % NXP] = make_float2(dx0, dx1); DYA[(p / NXP) % KY] = dy0; DZA[p / (NXP * KY)] = dz0;
+    } else {
+      DX[p] = make_float2(dx0, dx1); DY[p] = make_float2(dy0, dy1); DZ[p] = make_float2(dz0, dz1);
+    }
     DD[p] = make_float2(dx0 * dx0 + dy0 * dy0 + dz0 * dz0, dx1 * dx1 + dy1 * dy1 + dz1 * dz1);
     BT[p] = f2(0.f);
     A[2 * p] = f2(0.f); A[2 * p + 1] = f2(0.f); B[2 * p] = f2(0.f); B[2 * p + 1] = f2(0.f);
   }
+  auto dxp = [&](int p) -> float2 { if constexpr (AXIS) return DX[p % NXP]; else return DX[p]; };
+  auto dyp = [&](int p) -> float2 { if constexpr (AXIS) return f2(DYA[(p / NXP) % KY]); else return DY[p]; };
+  auto dzp = [&](int p) -> float2 { if constexpr (AXIS) return f2(DZA[p / (NXP * KY)]); else return DZ[p]; };
 
   const float kph = (float)(6.283185307179586 * prm.k_r);
   const float kfs = (float)prm.k_s;
@@ -785,16 +801,16 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
           if (MODE == kRefract) {   // Fermat time through the interface minus the tile reference
-            const float t0v = refr_time32(DX[p].x - kc.tx2x, DY[p].x - kc.tx2y, DZ[p].x - kc.tx2z, zbr - kc.tx2z,
-                                          DZ[p].x - zbr, k1r, k2r);
-            const float t1v = refr_time32(DX[p].y - kc.tx2x, DY[p].y - kc.tx2y, DZ[p].y - kc.tx2z, zbr - kc.tx2z,
-                                          DZ[p].y - zbr, k1r, k2r);
+            const float t0v = refr_time32(dxp(p).x - kc.tx2x, dyp(p).x - kc.tx2y, dzp(p).x - kc.tx2z, zbr - kc.tx2z,
+                                          dzp(p).x - zbr, k1r, k2r);
+            const float t1v = refr_time32(dxp(p).y - kc.tx2x, dyp(p).y - kc.tx2y, dzp(p).y - kc.tx2z, zbr - kc.tx2z,
+                                          dzp(p).y - zbr, k1r, k2r);
             BT[p] = make_float2(t0v - kc.r_t, t1v - kc.r_t);
             continue;
           }
-          float2 q = __ffma2_rn(f2(kc.tx2y), AXIS ? f2(DYS[p]) : DY[p], DD[p]);
-          q = __ffma2_rn(f2(kc.tx2x), DX[p], q);
-          if (HAS_DZ) q = __ffma2_rn(f2(kc.tx2z), DZ[p], q);
+          float2 q = __ffma2_rn(f2(kc.tx2y), dyp(p), DD[p]);
+          q = __ffma2_rn(f2(kc.tx2x), dxp(p), q);
+          if (HAS_DZ) q = __ffma2_rn(f2(kc.tx2z), dzp(p), q);
 #if SASBP_TX_SERIES
           if (MODE == kSeries3 || MODE == kSeries4) {   // far field: the rx leg's series, no MUFU
             float2 h = MODE == kSeries4 ? __ffma2_rn(f2(ta3), q, f2(ta2)) : f2(ta2);
@@ -833,17 +849,17 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
       const float rrk = WEIGHT ? kc.r_r * kfs * inv_ks2 : 0.f;
 #pragma unroll
       for (int p = 0; p < NP; ++p) {
-        float2 q = __ffma2_rn(f2(kc.uy2), AXIS ? f2(DYS[p]) : DY[p], DD[p]);
-        q = __ffma2_rn(f2(kc.ux2), DX[p], q);
-        if (HAS_DZ) q = __ffma2_rn(f2(kc.uz2), DZ[p], q);
+        float2 q = __ffma2_rn(f2(kc.uy2), dyp(p), DD[p]);
+        q = __ffma2_rn(f2(kc.ux2), dxp(p), q);
+        if (HAS_DZ) q = __ffma2_rn(f2(kc.uz2), dzp(p), q);
         float2 U;
         float2 wgt = f2(1.f);
         float2 srr = f2(0.f);   // exact-mode moving receiver: |x - rx'| per pixel
         if (MODE == kRefract) {
-          const float r0 = refr_time32(DX[p].x - kc.ux2, DY[p].x - kc.uy2, DZ[p].x - kc.uz2, zbr - kc.uz2,
-                                       DZ[p].x - zbr, k1r, k2r);
-          const float r1 = refr_time32(DX[p].y - kc.ux2, DY[p].y - kc.uy2, DZ[p].y - kc.uz2, zbr - kc.uz2,
-                                       DZ[p].y - zbr, k1r, k2r);
+          const float r0 = refr_time32(dxp(p).x - kc.ux2, dyp(p).x - kc.uy2, dzp(p).x - kc.uz2, zbr - kc.uz2,
+                                       dzp(p).x - zbr, k1r, k2r);
+          const float r1 = refr_time32(dxp(p).y - kc.ux2, dyp(p).y - kc.uy2, dzp(p).y - kc.uz2, zbr - kc.uz2,
+                                       dzp(p).y - zbr, k1r, k2r);
           U = __fadd2_rn(make_float2(r0 - kc.a1, r1 - kc.a1), BT[p]);
         } else if (MODE == kExact) {
           const float2 r2 = __fadd2_rn(q, f2(kc.r2_r));
@@ -876,17 +892,17 @@ __global__ void __launch_bounds__(32 * WY * WZ, SASBP_MINB * 4 / (WY * WZ)) tdbp
         }
 #if SASBP_BININDEX
         if (MOTION) {   // moving receiver: U' = dU / (1 + w.v/c) ~ dU (kap0 + kg.d)
-          float2 kap = __ffma2_rn(f2(kc.kgy), DY[p], f2(kc.kap0));
-          kap = __ffma2_rn(f2(kc.kgx), DX[p], kap);
-          if (HAS_DZ) kap = __ffma2_rn(f2(kc.kgz), DZ[p], kap);
+          float2 kap = __ffma2_rn(f2(kc.kgy), dyp(p), f2(kc.kap0));
+          kap = __ffma2_rn(f2(kc.kgx), dxp(p), kap);
+          if (HAS_DZ) kap = __ffma2_rn(f2(kc.kgz), dzp(p), kap);
           U = __fmul2_rn(U, kap);
         }
         const float2 T = __fadd2_rn(U, f2(urrv));            // exponent-aligned window coordinate V
 #else
         if (MOTION) {   // moving receiver: U = dU / (1 + w.v/c) ~ dU (kap0 + kg.d) + urr
-          float2 kap = __ffma2_rn(f2(kc.kgy), DY[p], f2(kc.kap0));
-          kap = __ffma2_rn(f2(kc.kgx), DX[p], kap);
-          if (HAS_DZ) kap = __ffma2_rn(f2(kc.kgz), DZ[p], kap);
+          float2 kap = __ffma2_rn(f2(kc.kgy), dyp(p), f2(kc.kap0));
+          kap = __ffma2_rn(f2(kc.kgx), dxp(p), kap);
+          if (HAS_DZ) kap = __ffma2_rn(f2(kc.kgz), dzp(p), kap);
           if (MODE == kExact) {   // exact: kappa = |x - rx'| / (|x - rx'| + (u + d).v / c)
             const float2 dn = __fadd2_rn(srr, kap);
             kap = __fmul2_rn(srr, make_float2(rcp_approx(dn.x), rcp_approx(dn.y)));
