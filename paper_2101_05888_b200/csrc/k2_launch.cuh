@@ -62,7 +62,7 @@ cudaError_t launch_family(const TdbpParams& prm, const TmaDesc& tmap, const K2La
   if (WEIGHT) {   // spreading weight (R18): stop-and-hop, straight rays only (checked on the host)
     if (prm.vel || prm.refract) return cudaErrorNotSupported;
     auto go = [&](auto kern) { return launch_k(kern, nt, prm, tmap, smem, L); };
-    if constexpr (KZ > 1) if (L.tma && L.axis) {   // compact geometry: 3D volumes only
+    if constexpr (KZ > 1 || SASBP_AXIS2D) if (L.tma && L.axis) {   // compact geometry: 3D volumes only
       switch (L.mode) {
         case kSeries3: return go(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kSeries3, true, GATE, false, true, WEIGHT>);
         case kSeries4: return go(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kSeries4, true, GATE, false, true, WEIGHT>);
@@ -98,7 +98,7 @@ cudaError_t launch_family(const TdbpParams& prm, const TmaDesc& tmap, const K2La
   };
   using TT = std::true_type;
   using FF = std::false_type;
-  if constexpr (KZ > 1)   // compact geometry: 3D volumes only
+  if constexpr (KZ > 1 || SASBP_AXIS2D)   // compact geometry: 3D volumes only
     if (L.tma && L.axis) return prm.vel ? pick(TT{}, TT{}, TT{}) : pick(TT{}, FF{}, TT{});
   if (L.tma) return prm.vel ? pick(TT{}, TT{}, FF{}) : pick(TT{}, FF{}, FF{});
   return prm.vel ? pick(FF{}, TT{}, FF{}) : pick(FF{}, FF{}, FF{});

@@ -381,7 +381,7 @@ sas_status sas_bp_create(double fc, double bandwidth, double fs, double c, const
   const bool flat_z = (g.nz == 1) && g.step_x[2] == 0.0 && g.step_y[2] == 0.0;
   // 3D grids with each step along its own axis (off-diagonal components exactly zero) run the
   // compact-geometry instantiation (A/B on config 4: +7.9 %; on 2D planes it lost 1.8 %)
-  h->axis = g.nz > 1 && g.step_x[1] == 0.0 && g.step_x[2] == 0.0 && g.step_y[0] == 0.0 && g.step_y[2] == 0.0 &&
+  h->axis = (g.nz > 1 || SASBP_AXIS2D) && g.step_x[1] == 0.0 && g.step_x[2] == 0.0 && g.step_y[0] == 0.0 && g.step_y[2] == 0.0 &&
             g.step_z[0] == 0.0 && g.step_z[1] == 0.0;
   if (g.nz == 1) { h->variant = flat_z ? V2D : V2D_DZ; h->TX = 8 * SASBP_KX2D; h->TY = 4 * SASBP_KY2D * SASBP_WY2D; h->TZ = 1; }
   else { h->variant = V3D; h->TX = 16; h->TY = 4 * SASBP_KY3D; h->TZ = SASBP_KZ3D * SASBP_WZ3D; }

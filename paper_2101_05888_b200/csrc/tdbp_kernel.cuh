@@ -51,6 +51,12 @@ namespace sasbp {
 #ifndef SASBP_CC_LDS
 #define SASBP_CC_LDS 0   // A/B knob: channel constants via explicit ld.shared (see lds_struct)
 #endif
+#ifndef SASBP_AXIS_PAIRS
+#define SASBP_AXIS_PAIRS 0   // A/B knob: AXIS kernels keep dy / dz per row as register pairs
+#endif
+#ifndef SASBP_AXIS2D
+#define SASBP_AXIS2D 0       // A/B knob: instantiate / select the AXIS kernels for 2D planes as well
+#endif
 #ifndef SASBP_CC_PREFETCH
 // dense series kernels on axis-aligned 3D grids: load the next channel's hot constants one channel
 // ahead (A/B config 4: +1.6 %; the register-tighter 2D kernel lost 1.5 % with it)
@@ -565,7 +571,8 @@ __global__ void __launch_bounds__(32 * WY * WZ, (AXIS ? SASBP_MINB_AXIS : SASBP_
   // same arithmetic from ~20 fewer registers (occupancy).  Pixel k = ((kz KY + ky) KX + kx), pair
   // p = k / 2: x-pair column p % NXP, row (p / NXP) % KY, plane p / (NXP KY).
   constexpr int NXP = KX / 2;
-  float2 DX[AXIS ? NXP : NP], DY[AXIS ? 1 : NP], DZ[AXIS ? 1 : NP], DD[NP], BT[NP];
+  constexpr bool AXP = AXIS && SASBP_AXIS_PAIRS;   // dy, dz as register pairs (else broadcast scalars)
+  float2 DX[AXIS ? NXP : NP], DY[AXP ? KY : (AXIS ? 1 : NP)], DZ[AXP ? KZ : (AXIS ? 1 : NP)], DD[NP], BT[NP];
   float DYA[AXIS ? KY : 1], DZA[AXIS ? KZ : 1];
   float2 A[2 * NP], B[2 * NP];
 #pragma unroll
@@ -574,7 +581,9 @@ __global__ void __launch_bounds__(32 * WY * WZ, (AXIS ? SASBP_MINB_AXIS : SASBP_
     tm.offset(prm, 2 * p, dx0, dy0, dz0);
     tm.offset(prm, 2 * p + 1, dx1, dy1, dz1);
     if (!HAS_DZ) { dz0 = 0.f; dz1 = 0.f; }
-    if constexpr (AXIS) {
+    if constexpr (AXP) {
+      DX[p % NXP] = make_float2(dx0, dx1); DY[(p / NXP) % KY] = f2(dy0); DZ[p / (NXP * KY)] = f2(dz0);
+    } else if constexpr (AXIS) {
       DX[p % NXP] = make_float2(dx0, dx1); DYA[(p / NXP) % KY] = dy0; DZA[p / (NXP * KY)] = dz0;
     } else {
       DX[p] = make_float2(dx0, dx1); DY[p] = make_float2(dy0, dy1); DZ[p] = make_float2(dz0, dz1);
@@ -584,8 +593,12 @@ __global__ void __launch_bounds__(32 * WY * WZ, (AXIS ? SASBP_MINB_AXIS : SASBP_
     A[2 * p] = f2(0.f); A[2 * p + 1] = f2(0.f); B[2 * p] = f2(0.f); B[2 * p + 1] = f2(0.f);
   }
   auto dxp = [&](int p) -> float2 { if constexpr (AXIS) return DX[p % NXP]; else return DX[p]; };
-  auto dyp = [&](int p) -> float2 { if constexpr (AXIS) return f2(DYA[(p / NXP) % KY]); else return DY[p]; };
-  auto dzp = [&](int p) -> float2 { if constexpr (AXIS) return f2(DZA[p / (NXP * KY)]); else return DZ[p]; };
+  auto dyp = [&](int p) -> float2 {
+    if constexpr (AXP) return DY[(p / NXP) % KY]; else if constexpr (AXIS) return f2(DYA[(p / NXP) % KY]); else return DY[p];
+  };
+  auto dzp = [&](int p) -> float2 {
+    if constexpr (AXP) return DZ[p / (NXP * KY)]; else if constexpr (AXIS) return f2(DZA[p / (NXP * KY)]); else return DZ[p];
+  };
 
   const float kph = (float)(6.283185307179586 * prm.k_r);
   const float kfs = (float)prm.k_s;
