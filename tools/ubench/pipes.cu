@@ -15,14 +15,29 @@
 constexpr int CH = 8;        // independent chains per thread
 constexpr int ITERS = 1 << 16;
 
-__device__ unsigned long long g_cycles[4096];
+// per block: SM clock64() at loop start / end, %smid, %globaltimer (ns) at start / end.  The
+// per-SM throughput is taken over each SM's span [min start, max end] of clock64 (a per-SM
+// counter; blocks of one SM need not start together), and the clock over the same span in ns.
+__device__ unsigned long long g_c0[4096], g_c1[4096], g_n0[4096], g_n1[4096];
+__device__ unsigned g_sm[4096];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t)); return t;
+}
+__device__ __forceinline__ unsigned smid() { unsigned s; asm volatile("mov.u32 %0, %smid;" : "=r"(s)); return s; }
+__device__ __forceinline__ void rec(unsigned long long t0, unsigned long long t1, unsigned long long n0) {
+  const unsigned long long n1 = gtimer();
+  if (threadIdx.x == 0) {
+    g_c0[blockIdx.x] = t0; g_c1[blockIdx.x] = t1; g_n0[blockIdx.x] = n0; g_n1[blockIdx.x] = n1;
+    g_sm[blockIdx.x] = smid();
+  }
+}
 
 __global__ void k_ffma(float* out, float a, float b) {
   float x[CH];
 #pragma unroll
   for (int i = 0; i < CH; ++i) x[i] = threadIdx.x * 1e-3f + i;
   float y = a * 0.5f, z = b * 0.25f;
-  unsigned long long t0 = clock64();
+  unsigned long long n0 = gtimer(), t0 = clock64();
   for (int it = 0; it < ITERS; ++it) {
 #pragma unroll
     for (int i = 0; i < CH; ++i) x[i] = fmaf(x[i], y, z);
@@ -32,7 +47,7 @@ __global__ void k_ffma(float* out, float a, float b) {
 #pragma unroll
   for (int i = 0; i < CH; ++i) s += x[i];
   if (s == 1234.5f) out[0] = s;
-  if (threadIdx.x == 0) g_cycles[blockIdx.x] = t1 - t0;
+  rec(t0, t1, n0);
 }
 
 __global__ void k_ffma_imm(float* out, float a) {
@@ -40,7 +55,7 @@ __global__ void k_ffma_imm(float* out, float a) {
 #pragma unroll
   for (int i = 0; i < CH; ++i) x[i] = threadIdx.x * 1e-3f + i;
   float y = a * 0.5f;
-  unsigned long long t0 = clock64();
+  unsigned long long n0 = gtimer(), t0 = clock64();
   for (int it = 0; it < ITERS; ++it) {
 #pragma unroll
     for (int i = 0; i < CH; ++i) x[i] = fmaf(x[i], y, 0.7071f);
@@ -50,7 +65,7 @@ __global__ void k_ffma_imm(float* out, float a) {
 #pragma unroll
   for (int i = 0; i < CH; ++i) s += x[i];
   if (s == 1234.5f) out[0] = s;
-  if (threadIdx.x == 0) g_cycles[blockIdx.x] = t1 - t0;
+  rec(t0, t1, n0);
 }
 
 __device__ __forceinline__ unsigned long long ffma2(unsigned long long a, unsigned long long b,
@@ -69,7 +84,7 @@ __global__ void k_ffma2(float* out, float a, float b) {
   }
   float2 yv = make_float2(a * 0.5f, a * 0.25f), zv = make_float2(b * 0.25f, b);
   unsigned long long y = *reinterpret_cast<unsigned long long*>(&yv), z = *reinterpret_cast<unsigned long long*>(&zv);
-  unsigned long long t0 = clock64();
+  unsigned long long n0 = gtimer(), t0 = clock64();
   for (int it = 0; it < ITERS; ++it) {
 #pragma unroll
     for (int i = 0; i < CH; ++i) x[i] = ffma2(x[i], y, z);
@@ -79,7 +94,7 @@ __global__ void k_ffma2(float* out, float a, float b) {
 #pragma unroll
   for (int i = 0; i < CH; ++i) { float2 v = *reinterpret_cast<float2*>(&x[i]); s += v.x + v.y; }
   if (s == 1234.5f) out[0] = s;
-  if (threadIdx.x == 0) g_cycles[blockIdx.x] = t1 - t0;
+  rec(t0, t1, n0);
 }
 
 // sin + cos of the same argument: 2 MUFU per chain step (+ FMUL.RZ + FADD)
@@ -87,7 +102,7 @@ __global__ void k_sincos(float* out, float a) {
   float x[CH];
 #pragma unroll
   for (int i = 0; i < CH; ++i) x[i] = threadIdx.x * 1e-3f + i;
-  unsigned long long t0 = clock64();
+  unsigned long long n0 = gtimer(), t0 = clock64();
   for (int it = 0; it < ITERS / 4; ++it) {
 #pragma unroll
     for (int i = 0; i < CH; ++i) x[i] = __sinf(x[i]) + __cosf(x[i]);
@@ -97,14 +112,14 @@ __global__ void k_sincos(float* out, float a) {
 #pragma unroll
   for (int i = 0; i < CH; ++i) s += x[i];
   if (s == 1234.5f) out[0] = s;
-  if (threadIdx.x == 0) g_cycles[blockIdx.x] = t1 - t0;
+  rec(t0, t1, n0);
 }
 
 __global__ void k_rsqrt(float* out, float a) {
   float x[CH];
 #pragma unroll
   for (int i = 0; i < CH; ++i) x[i] = threadIdx.x * 1e-3f + i + 1.f;
-  unsigned long long t0 = clock64();
+  unsigned long long n0 = gtimer(), t0 = clock64();
   for (int it = 0; it < ITERS / 4; ++it) {
 #pragma unroll
     for (int i = 0; i < CH; ++i) x[i] = rsqrtf(x[i]);
@@ -114,7 +129,7 @@ __global__ void k_rsqrt(float* out, float a) {
 #pragma unroll
   for (int i = 0; i < CH; ++i) s += x[i];
   if (s == 1234.5f) out[0] = s;
-  if (threadIdx.x == 0) g_cycles[blockIdx.x] = t1 - t0;
+  rec(t0, t1, n0);
 }
 
 __global__ void k_lds128(float* out, int stride) {
@@ -125,7 +140,7 @@ __global__ void k_lds128(float* out, int stride) {
   int idx[CH];
 #pragma unroll
   for (int i = 0; i < CH; ++i) idx[i] = (threadIdx.x * stride + i * 37) & 1023;
-  unsigned long long t0 = clock64();
+  unsigned long long n0 = gtimer(), t0 = clock64();
   for (int it = 0; it < ITERS / 4; ++it) {
 #pragma unroll
     for (int i = 0; i < CH; ++i) {
@@ -136,7 +151,30 @@ __global__ void k_lds128(float* out, int stride) {
   }
   unsigned long long t1 = clock64();
   if (acc.x + acc.y + acc.z + acc.w == 1234.5f) out[0] = acc.x;
-  if (threadIdx.x == 0) g_cycles[blockIdx.x] = t1 - t0;
+  rec(t0, t1, n0);
+}
+
+// integer ALU pipe: one LOP3 (xor3) per step (a chain of adds is folded by ptxas into IMAD/LEA,
+// so no add probe)
+template <int OP>
+__global__ void k_int(float* out, unsigned y, unsigned z) {
+  unsigned x[CH];
+#pragma unroll
+  for (int i = 0; i < CH; ++i) x[i] = threadIdx.x * 7u + i;
+  unsigned long long n0 = gtimer(), t0 = clock64();
+  for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+    for (int i = 0; i < CH; ++i) {
+      if (OP == 0) asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(x[i]) : "r"(y), "r"(z));
+      else asm volatile("add.u32 %0, %0, %1;" : "+r"(x[i]) : "r"(y));
+    }
+  }
+  unsigned long long t1 = clock64();
+  unsigned s = 0;
+#pragma unroll
+  for (int i = 0; i < CH; ++i) s += x[i];
+  if (s == 12345u) out[0] = (float)s;
+  rec(t0, t1, n0);
 }
 
 template <typename F>
@@ -151,17 +189,34 @@ static int run(const char* name, F launch, int blocks, int threads, double ops_p
   CK(cudaEventRecord(e1));
   CK(cudaEventSynchronize(e1));
   float ms = 0; CK(cudaEventElapsedTime(&ms, e0, e1));
-  unsigned long long cyc[4096];
-  CK(cudaMemcpyFromSymbol(cyc, g_cycles, sizeof(unsigned long long) * blocks));
-  double cmax = 0, csum = 0;
-  for (int i = 0; i < blocks; ++i) { cmax = cyc[i] > cmax ? cyc[i] : cmax; csum += cyc[i]; }
+  static unsigned long long c0[4096], c1[4096], n0[4096], n1[4096];
+  static unsigned sm[4096];
+  CK(cudaMemcpyFromSymbol(c0, g_c0, sizeof(unsigned long long) * blocks));
+  CK(cudaMemcpyFromSymbol(c1, g_c1, sizeof(unsigned long long) * blocks));
+  CK(cudaMemcpyFromSymbol(n0, g_n0, sizeof(unsigned long long) * blocks));
+  CK(cudaMemcpyFromSymbol(n1, g_n1, sizeof(unsigned long long) * blocks));
+  CK(cudaMemcpyFromSymbol(sm, g_sm, sizeof(unsigned) * blocks));
   double total_ops = ops_per_thread * threads * (double)blocks;
-  double blocks_per_sm = (double)blocks / sms;
-  // per-SM per-clock from in-kernel cycle counts (all blocks co-resident: blocks <= sms*occ)
-  double per_sm_clk = ops_per_thread * threads * blocks_per_sm / (csum / blocks);
-  double eff_ghz = (csum / blocks) / (ms * 1e-3) / 1e9;
+  // per SM: ops of its blocks / (max end - min start) in its own clock64 cycles; clock = the same
+  // span's cycles / its globaltimer ns.  Averaged over the SMs that ran blocks.
+  double rate_sum = 0, ghz_sum = 0;
+  int nsm = 0;
+  for (int m = 0; m < 1024; ++m) {
+    unsigned long long a = ~0ull, b = 0, na = ~0ull, nb = 0;
+    int k = 0;
+    for (int i = 0; i < blocks; ++i)
+      if (sm[i] == (unsigned)m) {
+        ++k; a = c0[i] < a ? c0[i] : a; b = c1[i] > b ? c1[i] : b;
+        na = n0[i] < na ? n0[i] : na; nb = n1[i] > nb ? n1[i] : nb;
+      }
+    if (!k || b <= a || nb <= na) continue;
+    rate_sum += ops_per_thread * threads * k / (double)(b - a);
+    ghz_sum += (double)(b - a) / (double)(nb - na);
+    ++nsm;
+  }
+  double per_sm_clk = nsm ? rate_sum / nsm : 0, eff_ghz = nsm ? ghz_sum / nsm : 0;
   printf("{\"probe\":\"%s\",\"blocks\":%d,\"threads\":%d,\"ms\":%.4f,\"Gops_per_s\":%.1f,"
-         "\"ops_per_sm_per_clk\":%.2f,\"kernel_clock_ghz_est\":%.3f,\"sms\":%d,\"max_clk_mhz\":%.0f}\n",
+         "\"ops_per_sm_per_clk\":%.2f,\"sm_clock_ghz\":%.3f,\"sms\":%d,\"max_clk_mhz\":%.0f}\n",
          name, blocks, threads, ms, total_ops / (ms * 1e-3) / 1e9, per_sm_clk, eff_ghz, sms,
          clk_khz / 1e3);
   return 0;
@@ -187,6 +242,7 @@ int main() {
   if (run("mufu_rsq", [&] { k_rsqrt<<<B, T>>>(out, 1.f); }, B, T, (double)(ITERS / 4) * CH, sms, clk_khz)) return 1;
   // LDS.128: count 16-byte loads
   if (run("lds128", [&] { k_lds128<<<B, T>>>(out, 1); }, B, T, (double)(ITERS / 4) * CH, sms, clk_khz)) return 1;
+  if (run("int_lop3", [&] { k_int<0><<<B, T>>>(out, 0x9e3779b9u, 0x7f4a7c15u); }, B, T, (double)ITERS * CH, sms, clk_khz)) return 1;
   CK(cudaGetLastError());
   return 0;
 }
