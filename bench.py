@@ -9,8 +9,10 @@ interpolation, phase ramp, accumulation, image write, and for N > 1 the combine 
 over config 4 of BASELINE.json by default -- the 3D volumetric config the north star's targets
 name (near-field, 1000 pings x 256 elements x 1024 samples, 512 x 512 x 128 voxels; synthetic,
 seeded inputs from synth/).  N = 1 times one GPU; under torchrun (N > 1) the work is sharded
-across ranks, strong scaling: --shard image (bands of the grid, echoes all-gathered over
-NVLink, bands gathered to rank 0) or --shard ping (pings r::G, NCCL reduce of the image).
+across ranks, strong scaling: --shard ping (default; pings r::G, NCCL reduce of the image) or
+--shard image (bands of the grid, echoes all-gathered over NVLink, bands gathered to rank 0).
+The default is the scheme DESIGN.md §6 predicts to scale better from 1-GPU timings of every
+rank's launch (tools/predict_scaling.py: config 4 at N = 8, eta 0.999 ping vs 0.973 image).
 
 value  : N_u (terms whose interpolation support meets the record, K3; = dense for configs 1-4)
          / device time of the timed steps (CUDA events on the launching stream, max over
@@ -46,8 +48,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="sasbp", choices=["sasbp", "reference"])
     ap.add_argument("--config", type=int, default=4)
-    ap.add_argument("--shard", default="image", choices=["image", "ping"],
-                    help="N > 1 partitioning (SURVEY §8(e)): image bands or interleaved pings")
+    ap.add_argument("--shard", default="ping", choices=["image", "ping"],
+                    help="N > 1 partitioning (SURVEY §8(e)): interleaved pings + NCCL reduce (default: the "
+                         "scheme predicted to scale better, profiles/scaling_pred_r02.jsonl) or image bands")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -489,11 +492,12 @@ def run_sasbp(args):
         k1_ms = time_short_kernel(lambda: pkg.rangecompress_device(echoes_d, rep_d, out_d, stream=stream), stream)
         k1_bytes = 16 * P * E * Ns
         hbm = _measured_hbm()
-        k1 = {"kernel": "rc_fft_kernel (overlap-save, L=4096)", "Nr": nr, "ms": k1_ms,
+        k1 = {"kernel": ("rc_fft_kernel<PACK> (overlap-save, L=4096, %d records per transform)" % (4096 // (Ns + nr - 1))
+                         if Ns + nr - 1 <= 2048 else "rc_fft_kernel (overlap-save, L=4096)"), "Nr": nr, "ms": k1_ms,
               "achieved": k1_bytes / (k1_ms * 1e-3) / 1e9, "unit": "GB/s", "bound": "hbm", "peak": hbm[0],
               "peak_source": hbm[1], "frac": k1_bytes / (k1_ms * 1e-3) / 1e9 / hbm[0],
               "algorithmic_bytes": k1_bytes, "note": "16 B per sample: read raw + write compressed once",
-              "traffic": _profile_traffic("ncu_k1_r01.json", None)}
+              "traffic": _profile_traffic(f"ncu_k1_cfg{args.config}.json", args.config)}
         del out_d
 
     # ---- NEXT-4: spreading-weighted K2 on the same workload; K1b x4 upsampling and K0 basebanding
@@ -556,7 +560,8 @@ def run_sasbp(args):
                              "unit": "GB/s", "bound": "hbm", "peak": hbm[0], "peak_source": hbm[1],
                              "frac": up_bytes / (up_ms * 1e-3) / 1e9 / hbm[0],
                              "note": "8 B read + 32 B written per input sample"},
-            "whitening": {"gain_kernel": "wh_periodogram_kernel (M = 64 direct DFT per block) + wh_gain_kernel",
+            "whitening": {"gain_kernel": "wh_periodogram_reg_kernel<4> (M = 64: 16-point register DFT x radix-4 across "
+                                         "4 lanes per block) + wh_gain_kernel",
                           "gain_ms": wg_ms, "gain_GB_per_s": 8 * nch * Ns / (wg_ms * 1e-3) / 1e9,
                           "gain_frac_hbm": 8 * nch * Ns / (wg_ms * 1e-3) / 1e9 / hbm[0],
                           "whitened_k1_ms": wc_ms,
@@ -576,7 +581,7 @@ def run_sasbp(args):
         cpu["cpu_model"] = host_cpu_model()
 
     if rank == 0:
-        traffic = _profile_traffic("ncu_tdbp_latest.json", args.config)
+        traffic = _profile_traffic(f"ncu_tdbp_cfg{args.config}.json", args.config)
         last3 = step_ms[-3:]
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

@@ -144,6 +144,9 @@ SASBP_API sas_status sas_bp_count_terms(sas_bp_t h, uint64_t* dense, uint64_t* i
  *             device echoes, or SASBP_NO_TMA=1 in the environment at set_pings time)
  *   batch     channels (ping x element) staged per pipeline step
  *   ctas_per_sm  resident CTAs per SM of the last form's kernel (0 before the first form)
+ *   tail_split   2 when the last form split its last, at most half-full wave of tiles into two
+ *                channel halves per tile (partial images added atomically into the zeroed image;
+ *                never for SAS_FORM_ACCUMULATE), else 1 (0 before the first form)
  * Errors: SAS_E_INVALID for NULL; rx_mode / tma are -1 before the first set_pings. */
 typedef struct {
   int32_t tile[3];
@@ -152,6 +155,7 @@ typedef struct {
   int32_t tma;
   int32_t batch;
   int32_t ctas_per_sm;
+  int32_t tail_split;
 } sas_bp_plan;
 SASBP_API sas_status sas_bp_get_plan(sas_bp_t h, sas_bp_plan* out);
 

@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(256) baseband_blocked_kernel(const float* __re
                                                                double fc, const double* __restrict__ t0p,
                                                                const float* __restrict__ h, int Nh, int D_rt, int Apad,
                                                                int Nout, int MO, long long runs, float2 rot1,
-                                                               float2* __restrict__ out) {
+                                                               float2* __restrict__ out, int vec4) {
   const int D = DT ? DT : D_rt;
   extern __shared__ __align__(16) unsigned char bb_smem[];
   float2* hs = reinterpret_cast<float2*>(bb_smem);            // [D][Apad] (h, h)
@@ -231,9 +231,54 @@ __global__ void __launch_bounds__(256) baseband_blocked_kernel(const float* __re
   // Slot k0 + u B (B = blockDim) of phase q is sample nlo + (k0 + u B) D + q; its padded shared
   // position is bb_pad(k0) + u (B + B/8) (B is a multiple of 8).  Paired FP32 for the phasor
   // rotation (w <- w rot) and the mix (v w).
-  const int Lfull = (Lq / (kU * (int)blockDim.x)) * (kU * (int)blockDim.x);
   const int Bd = blockDim.x;
   const float2 rotp = make_float2(-rot.y, rot.x);
+  if (DT == 4 && vec4) {
+    // D = 4, 16-byte aligned channel rows (vec4, checked on the host): aligned float4 loads
+    // a = nlo - o + 4 k (o = nlo mod 4), kU = 8 per thread in flight (128 B, 4x the scalar path's
+    // bytes per load).  Component j is local input i = 4 k + j - o, i.e. phase q = i & 3 of slot
+    // i >> 2; the phasor is exact (fp64) at j = 0 and rotated for j = 1..3.  Loads wholly inside
+    // 0..Nin-1 are one LDG.128, the few at the record edges are guarded scalars (zero outside).
+    const int o = nlo & 3;
+    const int a0 = nlo - o;
+    const int nk = Lq + (o ? 1 : 0);           // float4s covering local inputs [0, 4 Lq)
+    for (int k0 = threadIdx.x; k0 < nk; k0 += kU * Bd) {
+      float4 v[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int k = k0 + u * Bd;
+        const int a = a0 + 4 * k;
+        v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (k < nk) {
+          if (a >= 0 && a + 3 < Nin) {
+            v[u] = __ldcs(reinterpret_cast<const float4*>(xc + a));
+          } else {
+            if (a >= 0 && a < Nin) v[u].x = __ldcs(xc + a);
+            if (a + 1 >= 0 && a + 1 < Nin) v[u].y = __ldcs(xc + a + 1);
+            if (a + 2 >= 0 && a + 2 < Nin) v[u].z = __ldcs(xc + a + 2);
+            if (a + 3 >= 0 && a + 3 < Nin) v[u].w = __ldcs(xc + a + 3);
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int k = k0 + u * Bd;
+        if (k >= nk) break;
+        double ph = fma((double)(a0 + 4 * k), kr, bp);   // cycles at component 0, fp64
+        ph -= rint(ph);
+        float2 w;
+        __sincosf(-6.283185307179586f * (float)ph, &w.y, &w.x);
+        const float vv[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (j) w = __ffma2_rn(make_float2(w.y, w.y), rotp, __fmul2_rn(make_float2(w.x, w.x), rot));
+          const int i = 4 * k + j - o;
+          if (i >= 0 && i < 4 * Lq) sz[(i & 3) * LqP + bb_pad(i >> 2)] = __fmul2_rn(make_float2(vv[j], vv[j]), w);
+        }
+      }
+    }
+  } else {
+  const int Lfull = (Lq / (kU * (int)blockDim.x)) * (kU * (int)blockDim.x);
   const bool interior = nlo >= 0 && nlo + Lq * D <= Nin;   // no bounds checks needed (CTA-uniform)
   for (int k0 = threadIdx.x; k0 < Lfull; k0 += kU * Bd) {
     float2 w[kU];
@@ -282,6 +327,7 @@ __global__ void __launch_bounds__(256) baseband_blocked_kernel(const float* __re
       }
       sz[q * LqP + bb_pad(k)] = z;
     }
+  }
   }
   __syncthreads();
   const int t0 = threadIdx.x * kBbR;
@@ -420,10 +466,13 @@ static sas_status bb_launch(const float* x, int32_t P, int32_t E, int32_t Nin, d
     if (e == cudaSuccess) {
       auto kern = D == 2 ? baseband_blocked_kernel<2> : D == 4 ? baseband_blocked_kernel<4>
                 : D == 8 ? baseband_blocked_kernel<8> : baseband_blocked_kernel<0>;
+      // float4 staging: D = 4 and every channel row 16-byte aligned (SASBP_BB_VEC4=0 disables, A/B)
+      const char* nv = getenv("SASBP_BB_VEC4");
+      const int vec4 = (D == 4 && (Nin % 4) == 0 && (((uintptr_t)x) & 15) == 0 && !(nv && nv[0] == '0')) ? 1 : 0;
       kern<<<(unsigned)blocks, threads, smem, st>>>(
           x, E, Nin, kr, fc, t0, h, Nh, D, Apad, Nout, MOb, runs,
           make_float2((float)std::cos(2.0 * 3.141592653589793 * kr), (float)-std::sin(2.0 * 3.141592653589793 * kr)),
-          out);
+          out, vec4);
       e = cudaGetLastError();
     }
     if (e != cudaSuccess) return cond_fail(SAS_E_CUDA, "baseband_blocked_kernel", e);

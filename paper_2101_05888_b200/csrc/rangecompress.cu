@@ -214,14 +214,11 @@ __device__ __forceinline__ void load_smem(float2 v[16], const float2* sm, int j)
   for (int r = 0; r < 16; ++r) v[r] = sm[pad(j + r * kFT)];
 }
 
-// forward FFT of x[n0 .. n0+L) (zero past Ns); bin j + 256 r is left in slot sig(r)
-__device__ __forceinline__ void fft_forward(float2 v[16], const float2* __restrict__ x, int n0, int Ns, float2* sm,
-                                            const float2* __restrict__ tw, int j) {
+// forward FFT of the block whose element i = j + 256 r is ld(i); bin j + 256 r is left in slot sig(r)
+template <class LD>
+__device__ __forceinline__ void fft_forward_ld(float2 v[16], LD ld, float2* sm, const float2* __restrict__ tw, int j) {
 #pragma unroll
-  for (int r = 0; r < 16; ++r) {
-    const int n = n0 + j + r * kFT;
-    v[r] = ((unsigned)n < (unsigned)Ns) ? __ldg(x + n) : make_float2(0.f, 0.f);   // zero outside 0..Ns-1
-  }
+  for (int r = 0; r < 16; ++r) v[r] = ld(j + r * kFT);
   pass_store<false, 1>(v, sm, tw, j);
   __syncthreads();
   load_smem(v, sm, j);
@@ -230,6 +227,15 @@ __device__ __forceinline__ void fft_forward(float2 v[16], const float2* __restri
   __syncthreads();
   load_smem(v, sm, j);
   pass_regs<false, 256>(v, tw, j);
+}
+
+// forward FFT of x[n0 .. n0+L) (zero outside 0..Ns-1)
+__device__ __forceinline__ void fft_forward(float2 v[16], const float2* __restrict__ x, int n0, int Ns, float2* sm,
+                                            const float2* __restrict__ tw, int j) {
+  fft_forward_ld(v, [&](int i) {
+    const int n = n0 + i;
+    return ((unsigned)n < (unsigned)Ns) ? __ldg(x + n) : make_float2(0.f, 0.f);
+  }, sm, tw, j);
 }
 
 __global__ void __launch_bounds__(kFT) rc_twiddle_kernel(float2* tw) {
@@ -253,17 +259,37 @@ __global__ void __launch_bounds__(kFT) rc_prep_kernel(const float2* __restrict__
   for (int r = 0; r < 16; ++r) H[j + r * kFT] = make_float2(v[sig(r)].x * sc, -v[sig(r)].y * sc);
 }
 
+// PACK = false: block blockIdx.x of channel blockIdx.y, outputs n0 .. n0 + V (records longer than
+// the block).  PACK = true (short records, S = Ns + Nr - 1 <= L): the block holds kpb whole
+// channels, channel c's span x[lag0 .. lag0 + S) at positions [c S, (c + 1) S) -- the Nr - 1 zeros
+// after each record keep the circular correlation of one channel from reaching the next, so each
+// output n < Ns at position c S + n is alias free (c S + n + Nr - 1 < (c + 1) S <= L).  The same
+// transform then serves kpb channels instead of one (config 4: Ns = 1024, Nr = 160, 3 per block).
+template <bool PACK>
 __global__ void __launch_bounds__(kFT, RC_MINB) rc_fft_kernel(const float2* __restrict__ raw, int Ns, int V, int lag0,
                                                         const float2* __restrict__ H, const float2* __restrict__ tw_g,
-                                                        float2* __restrict__ out) {
+                                                        float2* __restrict__ out, long long nch, int S, int kpb,
+                                                        uint32_t mS) {
   __shared__ float2 sm[kPad];
   const int j = threadIdx.x;
-  const size_t ch = blockIdx.y;
-  const int n0 = blockIdx.x * V;
-  const float2* x = raw + ch * Ns;
   const float2* tw = tw_g;
   float2 v[16];
-  fft_forward(v, x, n0 + lag0, Ns, sm, tw, j);
+  size_t ch = 0;
+  int n0 = 0, kc = 0;
+  if (PACK) {
+    ch = (size_t)blockIdx.x * kpb;
+    kc = (int)min((long long)kpb, nch - (long long)ch);   // channels in this block
+    const float2* x = raw + ch * Ns;
+    fft_forward_ld(v, [&](int i) {
+      const int c = S == 1 ? i : (int)__umulhi((uint32_t)i, mS);   // i / S (exact: i S < 2^32; S = 1 has no 32-bit magic)
+      const int n = i - c * S + lag0;
+      return (c < kc && (unsigned)n < (unsigned)Ns) ? __ldg(x + (size_t)c * Ns + n) : make_float2(0.f, 0.f);
+    }, sm, tw, j);
+  } else {
+    ch = blockIdx.y;
+    n0 = blockIdx.x * V;
+    fft_forward(v, raw + ch * Ns, n0 + lag0, Ns, sm, tw, j);
+  }
   // spectrum product in registers (slot sig(r) holds bin j + 256 r)
 #pragma unroll
   for (int r = 0; r < 16; ++r) v[sig(r)] = cmul(v[sig(r)], __ldg(H + j + r * kFT));
@@ -283,8 +309,14 @@ __global__ void __launch_bounds__(kFT, RC_MINB) rc_fft_kernel(const float2* __re
 #pragma unroll
   for (int r = 0; r < 16; ++r) {
     const int i = j + r * kFT;
-    const int n = n0 + i;
-    if (i < V && n < Ns) y[n] = v[sig(r)];
+    if (PACK) {
+      const int c = S == 1 ? i : (int)__umulhi((uint32_t)i, mS);
+      const int n = i - c * S;
+      if (c < kc && n < Ns) y[(size_t)c * Ns + n] = v[sig(r)];
+    } else {
+      const int n = n0 + i;
+      if (i < V && n < Ns) y[n] = v[sig(r)];
+    }
   }
 }
 
@@ -347,11 +379,25 @@ static sas_status rc_launch_fft(const float2* raw, long nch, int32_t Ns, const f
   rc_prep_kernel<<<1, kFT, 0, st>>>(rep, Nr, tw, H);
   e = cudaGetLastError();
   const int V = kL - Nr + 1;
-  const unsigned blocks = (unsigned)((Ns + V - 1) / V);
-  for (long c0 = 0; c0 < nch && e == cudaSuccess; c0 += 65535) {
-    const unsigned n = (unsigned)((nch - c0) < 65535 ? (nch - c0) : 65535);
-    rc_fft_kernel<<<dim3(blocks, n), kFT, 0, st>>>(raw + c0 * Ns, Ns, V, lag0, H, tw, out + c0 * Ns);
-    e = cudaGetLastError();
+  const int S = Ns + Nr - 1;             // a record's span including the Nr - 1 zeros after it
+  const char* nopack = getenv("SASBP_RC_NOPACK");
+  if (S <= kL / 2 && !(nopack && nopack[0] == '1')) {   // >= 2 whole records per transform
+    const int kpb = kL / S;
+    const uint32_t mS = 0xFFFFFFFFu / (uint32_t)S + 1u;   // i / S as a multiply-high
+    const long long nblk = (nch + kpb - 1) / kpb;
+    for (long long b0 = 0; b0 < nblk && e == cudaSuccess; b0 += 0x7FFFFFFFLL) {
+      const long long nb = (nblk - b0) < 0x7FFFFFFFLL ? (nblk - b0) : 0x7FFFFFFFLL;
+      rc_fft_kernel<true><<<(unsigned)nb, kFT, 0, st>>>(raw + b0 * kpb * Ns, Ns, V, lag0, H, tw, out + b0 * kpb * Ns,
+                                                       nch - b0 * kpb, S, kpb, mS);
+      e = cudaGetLastError();
+    }
+  } else {
+    const unsigned blocks = (unsigned)((Ns + V - 1) / V);
+    for (long c0 = 0; c0 < nch && e == cudaSuccess; c0 += 65535) {
+      const unsigned n = (unsigned)((nch - c0) < 65535 ? (nch - c0) : 65535);
+      rc_fft_kernel<false><<<dim3(blocks, n), kFT, 0, st>>>(raw + c0 * Ns, Ns, V, lag0, H, tw, out + c0 * Ns, nch, 0, 0, 0u);
+      e = cudaGetLastError();
+    }
   }
   cudaFreeAsync(H, st);
   if (e != cudaSuccess) return rc_cuda_fail("rc_fft_kernel launch", e);
@@ -589,6 +635,9 @@ __device__ __forceinline__ void dftR(float2 (&z)[R]) {
   }
 }
 
+#ifndef WH_SWZ
+#define WH_SWZ 1   // XOR-swizzled transpose + padded twiddle rows (0: the round-1 layout, for A/B)
+#endif
 #ifndef WH_MINB
 #define WH_MINB 3   // 3 CTAs per SM (72 registers, twiddles in shared memory): A/B best of 2-4 without spills
 #endif
@@ -599,16 +648,18 @@ __global__ void __launch_bounds__(kWhThreads, WH_MINB) wh_periodogram_reg_kernel
   constexpr int GS = 17 * R;                                     // padded complex per group
   __shared__ float2 T[G * GS];
   __shared__ float red[M];
-  __shared__ float2 wtab[R * 16];   // W_M^{r k1}, shared (frees 32 registers per thread)
+  constexpr int WR = WH_SWZ ? 17 : 16;
+  __shared__ float2 wtab[R * WR];   // W_M^{r k1} at r * 17 + k1 (row pad: the R lanes of a group read
+                                    // rows r in the same step -- conflict-free), shared (frees 32 registers)
   const int r = threadIdx.x % R, g = threadIdx.x / R;
   for (int k = threadIdx.x; k < M; k += kWhThreads) red[k] = 0.f;
   for (int i = threadIdx.x; i < R * 16; i += kWhThreads) {
     float sn, cs;
     sincospif(-2.0f * (float)((i >> 4) * (i & 15)) / (float)M, &sn, &cs);
-    wtab[i] = make_float2(cs, sn);
+    wtab[(i >> 4) * WR + (i & 15)] = make_float2(cs, sn);
   }
   __syncthreads();
-  const float2* w = wtab + r * 16;
+  const float2* w = wtab + r * WR;
   float acc[16];
 #pragma unroll
   for (int i = 0; i < 16; ++i) acc[i] = 0.f;
@@ -634,13 +685,17 @@ __global__ void __launch_bounds__(kWhThreads, WH_MINB) wh_periodogram_reg_kernel
       __syncwarp();
       float2* Tg = T + g * GS;
 #pragma unroll
-      for (int k1 = 0; k1 < 16; ++k1) Tg[k1 * R + r] = cmul(v[sig(k1)], w[k1]);   // Z_r[k1]
+      // Z_r[k1] at row k1, column r XOR (k1 / S): the reads below take column q of rows r S + s
+      // (one row per lane r), which the swizzle spreads over R bank pairs; the writes (row k1,
+      // all r) stay a permutation of the row -- no bank conflicts either way (GS = 17 R
+      // separates the groups of a half-warp)
+      for (int k1 = 0; k1 < 16; ++k1) Tg[k1 * R + (WH_SWZ ? (r ^ ((k1 / S) & (R - 1))) : r)] = cmul(v[sig(k1)], w[k1]);
       __syncwarp();
 #pragma unroll
       for (int s = 0; s < S; ++s) {
         float2 z[R];
 #pragma unroll
-        for (int q = 0; q < R; ++q) z[q] = Tg[(r * S + s) * R + q];
+        for (int q = 0; q < R; ++q) z[q] = Tg[(r * S + s) * R + (WH_SWZ ? (q ^ r) : q)];
         dftR<R>(z);
 #pragma unroll
         for (int k2 = 0; k2 < R; ++k2) acc[s * R + k2] = fmaf(z[k2].x, z[k2].x, fmaf(z[k2].y, z[k2].y, acc[s * R + k2]));

@@ -25,6 +25,7 @@ namespace {
 
 thread_local char g_err[512] = "";
 thread_local int g_last_occ = 0;   // resident CTAs per SM of the last K2 launch on this thread
+thread_local int g_last_split = 0; // wave-tail split factor of the last K2 launch on this thread
 
 sas_status fail(sas_status st, const char* fmt, ...) {
   va_list ap;
@@ -76,6 +77,7 @@ struct sas_bp_s {
   bool use_tma = false;
   int tma_W = -1;        // window the descriptor's box was encoded for (a launch with another W re-encodes)
   int ctas_per_sm = 0;   // measured occupancy of the last form
+  int tail_split = 0;    // wave-tail split of the last form
   // field-of-view gating (sas_bp_set_beam; NEXT-1)
   int gate = 0, cull = 0, az_on = 0, el_on = 0;
   double half_az = 0, sin_half_az = 0, half_el = 0, tan_half_el = 0;
@@ -211,6 +213,7 @@ cudaError_t launch_tdbp(sas_bp_t h, float2* image, unsigned long long* counter, 
   }
   prm.fc = h->fc; prm.fs = h->fs; prm.c = h->c;
   prm.k_s = h->fs / h->c; prm.k_c = h->fc / h->c; prm.k_r = h->fc / h->fs; prm.inv_e = 1.0 / h->E;
+  prm.kph_f = (float)(6.283185307179586 * prm.k_r); prm.kfs_f = (float)prm.k_s;
   prm.hw = h->hw;
   prm.P = h->P; prm.E = h->E; prm.Ns = h->Ns;
   prm.nx = h->grid.nx; prm.ny = h->grid.ny; prm.nz = h->grid.nz;
@@ -237,8 +240,9 @@ cudaError_t launch_tdbp(sas_bp_t h, float2* image, unsigned long long* counter, 
   if (tma && h->tma_W != prm.W) tma = encode_tma(h, prm.W);
   const char* na = getenv("SASBP_NO_AXIS");   // A/B and test switch: force the general-geometry kernel
   const bool no_axis = na && na[0] == '1';
-  sasbp::K2Launch L{tma, h->axis && !no_axis, h->mode, count, st, &g_last_occ};
+  sasbp::K2Launch L{tma, h->axis && !no_axis, h->mode, count, st, &g_last_occ, &g_last_split};
   g_last_occ = 0;
+  g_last_split = 0;
   const bool g = prm.gate && !count;
   if (h->weight && !count) {
     switch (h->variant) {
@@ -503,6 +507,7 @@ sas_status sas_bp_form_device(sas_bp_t h, void* image_dev, void* cuda_stream, in
   CK_H(h, cudaEventRecord(h->busy, (cudaStream_t)cuda_stream));
   h->busy_pending = true;
   h->ctas_per_sm = g_last_occ;
+  h->tail_split = g_last_split;
   return SAS_OK;
 }
 
@@ -516,6 +521,7 @@ sas_status sas_bp_form(sas_bp_t h, float* image_out) {
   CK_H(h, cudaSetDevice(h->device));
   CK_H(h, launch_tdbp(h, h->image, h->counter, 0, false, h->stream));
   h->ctas_per_sm = g_last_occ;
+  h->tail_split = g_last_split;
   const size_t npx = (size_t)h->grid.nx * h->grid.ny * h->grid.nz;
   CK_H(h, cudaMemcpyAsync(image_out, h->image, npx * sizeof(float2), cudaMemcpyDeviceToHost, h->stream));
   CK_H(h, cudaStreamSynchronize(h->stream));
@@ -704,6 +710,7 @@ sas_status sas_bp_get_plan(sas_bp_t h, sas_bp_plan* out) {
   out->tma = h->has_pings ? (h->use_tma ? 1 : 0) : -1;
   out->batch = sasbp::kNB;
   out->ctas_per_sm = h->ctas_per_sm;
+  out->tail_split = h->tail_split;
   return SAS_OK;
 }
 

@@ -28,6 +28,7 @@
 //    A += Re(ehat)(cos, sin), B += Im(ehat)(cos, sin); I = (A.x - B.y, A.y + B.x).
 #pragma once
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 #ifndef SASBP_FLAT_TRANSFORM
@@ -53,6 +54,19 @@ namespace sasbp {
 #endif
 #ifndef SASBP_AXIS_PAIRS
 #define SASBP_AXIS_PAIRS 0   // A/B knob: AXIS kernels keep dy / dz per row as register pairs
+#endif
+#ifndef SASBP_GATE_SPLIT
+#define SASBP_GATE_SPLIT 0   // A/B knob: gated kernels take the per-pixel mask selects only on edge channels
+#endif
+#ifndef SASBP_GATE_PREF
+#define SASBP_GATE_PREF 0   // A/B knob: gated series kernels load the next channel's hot constants one channel ahead
+#endif
+#ifndef SASBP_GATE_NOINLINE
+#define SASBP_GATE_NOINLINE 0   // A/B knob: the fp64 per-pixel cone tests of edge tiles as out-of-line calls
+#endif
+#ifndef SASBP_AXIS_SEPQ
+#define SASBP_AXIS_SEPQ 1   // AXIS kernels form q = |d|^2 + 2u.d per axis (x pair + y row + z plane):
+                            // 6 fewer FMA-pipe cycles per warp-channel on the 3D plan (A/B +0.6 %, profiles/ab_r02.txt)
 #endif
 #ifndef SASBP_AXIS2D
 #define SASBP_AXIS2D 0       // A/B knob: instantiate / select the AXIS kernels for 2D planes as well
@@ -103,6 +117,9 @@ struct TdbpParams {
   double k_c;             // fc / c   (carrier cycles per metre of path)
   double k_r;             // fc / fs  (carrier cycles per sample)
   double inv_e;           // 1 / E
+  float kph_f;            // (float)(2 pi k_r): radians of carrier phase per sample (host-computed, so
+                          // the kernel never re-derives it in fp64 under register pressure)
+  float kfs_f;            // (float)k_s
   double hw;              // half window in samples: 2 * d_max * fs / c
   int P, E, Ns;
   int nx, ny, nz;
@@ -111,6 +128,10 @@ struct TdbpParams {
   int accumulate;
   int ch_lo, ch_hi;       // channel range [ch_lo, ch_hi) of this launch (ch = p * E + e)
   int resident;           // co-resident CTAs of the launch (SMs x CTAs/SM) for the channel rotation
+  // wave-tail split: tiles [tail0, ntiles) are launched tsplit (= 2) times, each CTA summing half of
+  // the channels and adding its partial image with an atomic float2 add into a zeroed image (0 + a + b
+  // = 0 + b + a exactly: still deterministic); tsplit = 1 -> one CTA per tile
+  int tail0, tsplit;
   // field-of-view gating (NEXT-1, reading R15); gate = 0 -> dense sum
   int gate;               // 1 = gate at tx; 2 = gate at tx and at each rx (bistatic)
   int cull;               // skip (tile, channel) pairs whose tile sphere misses a cone
@@ -424,7 +445,8 @@ struct TileMap {
   static constexpr int NP = K / 2;  // x-adjacent pixel pairs per thread
   static constexpr int TX = 8 * KX, TY = 4 * KY * WY, TZ = KZ * WZ;
   int x0, y0, z0, lx, ly, wy, wz;
-  __device__ TileMap(const TdbpParams& prm) {
+  __device__ TileMap(const TdbpParams& prm, int tile = -1) {
+    if (tile < 0) tile = (int)blockIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     lx = lane >> 2; ly = lane & 3;          // quarter-warp = 4 (y) x 2 (x) pixel patch
     wy = warp % WY; wz = warp / WY;
@@ -432,7 +454,7 @@ struct TileMap {
     // so the CTAs resident at one time cover a compact patch of the image; their windows
     // of a channel then overlap and a channel comes from DRAM once per wave (L2 reuse).
     const int nxy = prm.tiles_x * prm.tiles_y;
-    const int b = blockIdx.x % nxy, bz = blockIdx.x / nxy;
+    const int b = tile % nxy, bz = tile / nxy;
     constexpr int G = SASBP_TILE_GROUP;
     const int sr = b / (G * prm.tiles_x);                       // super-row of G tile rows
     const int gh = min(G, prm.tiles_y - sr * G);
@@ -535,6 +557,27 @@ __device__ __forceinline__ void tma_load_row(uint32_t dst, const void* tmap, int
 // Ns); box = box_samples(W) x 1; out-of-bounds samples read as zero (reading R2).
 struct __align__(64) TmaDesc { unsigned char bytes[128]; };
 
+// Per-pixel fp64 cone masks of one thread's pixels (edge tiles only).  Out of line under
+// SASBP_GATE_NOINLINE: the fp64 temporaries then never compete with the pixel loop's registers
+// (the call saves what is live around it, once per edge ping / channel).
+#if SASBP_GATE_NOINLINE
+#define SASBP_MASK_FN __device__ __noinline__
+#else
+#define SASBP_MASK_FN __device__ __forceinline__
+#endif
+template <class TM, int NPIX>
+SASBP_MASK_FN uint32_t gate_mask(const TdbpParams* prm, const TM tm, int ping, const double* sensor, uint32_t in) {
+  double a[3], bb[3], x[3];
+  ping_axes(*prm, ping, a, bb);
+  uint32_t m = in;
+#pragma unroll
+  for (int k = 0; k < NPIX; ++k) {
+    pixel_centre64(*prm, tm.ix(k), tm.iy(k), tm.iz(k), x);
+    if (!in_fov_px(*prm, x, sensor, a, bb)) m &= ~(1u << k);
+  }
+  return m;
+}
+
 // HAS_DZ = false means the grid is a z-level plane (step_x, step_y have no z component).  AXIS =
 // true for grids with diagonal steps (each step along its own axis): the pixel offsets are kept
 // per column / row / plane instead of per pixel pair (fewer registers, same arithmetic).
@@ -542,7 +585,7 @@ struct __align__(64) TmaDesc { unsigned char bytes[128]; };
 template <int KX, int KY, int KZ, int WY, int WZ, bool HAS_DZ, int MODE, bool USE_TMA, bool GATE = false,
           bool MOTION = false, bool AXIS = false, bool WEIGHT = false>
 __global__ void __launch_bounds__(32 * WY * WZ, (AXIS ? SASBP_MINB_AXIS : SASBP_MINB) * 4 / (WY * WZ))
-    tdbp_kernel(const TdbpParams prm,
+    tdbp_kernel(const __grid_constant__ TdbpParams prm,
                                                                           const __grid_constant__ TmaDesc tmap) {
   using TM = TileMap<KX, KY, KZ, WY, WZ>;
   constexpr int NP = TM::NP;
@@ -561,7 +604,18 @@ __global__ void __launch_bounds__(32 * WY * WZ, (AXIS ? SASBP_MINB_AXIS : SASBP_
   const uint32_t win_base = (uint32_t)__cvta_generic_to_shared(win);
   const uint32_t raw_base = (uint32_t)__cvta_generic_to_shared(rawp);
 
-  const TM tm(prm);
+  // tile of this CTA and its channel range (a wave-tail tile is shared by tsplit CTAs)
+  int tile = (int)blockIdx.x, ch_lo = prm.ch_lo, ch_hi = prm.ch_hi;
+  bool red = false;
+  if (prm.tsplit > 1 && tile >= prm.tail0) {
+    const int r = tile - prm.tail0, sp = r % prm.tsplit;
+    const long long n = (long long)prm.ch_hi - prm.ch_lo;
+    tile = prm.tail0 + r / prm.tsplit;
+    ch_lo = prm.ch_lo + (int)(n * sp / prm.tsplit);
+    ch_hi = prm.ch_lo + (int)(n * (sp + 1) / prm.tsplit);
+    red = true;
+  }
+  const TM tm(prm, tile);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double ct[3];
   tm.centre(prm, ct);
@@ -572,8 +626,13 @@ __global__ void __launch_bounds__(32 * WY * WZ, (AXIS ? SASBP_MINB_AXIS : SASBP_
   // p = k / 2: x-pair column p % NXP, row (p / NXP) % KY, plane p / (NXP KY).
   constexpr int NXP = KX / 2;
   constexpr bool AXP = AXIS && SASBP_AXIS_PAIRS;   // dy, dz as register pairs (else broadcast scalars)
-  float2 DX[AXIS ? NXP : NP], DY[AXP ? KY : (AXIS ? 1 : NP)], DZ[AXP ? KZ : (AXIS ? 1 : NP)], DD[NP], BT[NP];
+  // SEPQ: q = (dx^2 + ux dx) + (dy^2 + uy dy) + (dz^2 + uz dz) evaluated per column / row / plane and
+  // added per pixel pair (the squares are kept per axis instead of |d|^2 per pair)
+  constexpr bool SEPQ = AXIS && !AXP && SASBP_AXIS_SEPQ;
+  float2 DX[AXIS ? NXP : NP], DY[AXP ? KY : (AXIS ? 1 : NP)], DZ[AXP ? KZ : (AXIS ? 1 : NP)], DD[SEPQ ? 1 : NP], BT[NP];
   float DYA[AXIS ? KY : 1], DZA[AXIS ? KZ : 1];
+  float2 DX2[SEPQ ? NXP : 1];
+  float DY2[SEPQ ? KY : 1], DZ2[SEPQ ? KZ : 1];
   float2 A[2 * NP], B[2 * NP];
 #pragma unroll
   for (int p = 0; p < NP; ++p) {
@@ -588,7 +647,11 @@ __global__ void __launch_bounds__(32 * WY * WZ, (AXIS ? SASBP_MINB_AXIS : SASBP_
     } else {
       DX[p] = make_float2(dx0, dx1); DY[p] = make_float2(dy0, dy1); DZ[p] = make_float2(dz0, dz1);
     }
-    DD[p] = make_float2(dx0 * dx0 + dy0 * dy0 + dz0 * dz0, dx1 * dx1 + dy1 * dy1 + dz1 * dz1);
+    if constexpr (SEPQ) {
+      DX2[p % NXP] = make_float2(dx0 * dx0, dx1 * dx1); DY2[(p / NXP) % KY] = dy0 * dy0; DZ2[p / (NXP * KY)] = dz0 * dz0;
+    } else {
+      DD[p] = make_float2(dx0 * dx0 + dy0 * dy0 + dz0 * dz0, dx1 * dx1 + dy1 * dy1 + dz1 * dz1);
+    }
     BT[p] = f2(0.f);
     A[2 * p] = f2(0.f); A[2 * p + 1] = f2(0.f); B[2 * p] = f2(0.f); B[2 * p + 1] = f2(0.f);
   }
@@ -599,9 +662,22 @@ __global__ void __launch_bounds__(32 * WY * WZ, (AXIS ? SASBP_MINB_AXIS : SASBP_
   auto dzp = [&](int p) -> float2 {
     if constexpr (AXP) return DZ[p / (NXP * KY)]; else if constexpr (AXIS) return f2(DZA[p / (NXP * KY)]); else return DZ[p];
   };
+  // q = 2 u.d + |d|^2 of pixel pair p for the leg with 2u = (ux, uy, uz)
+  auto qpair = [&](int p, float ux, float uy, float uz) -> float2 {
+    if constexpr (SEPQ) {
+      const float y = fmaf(DYA[(p / NXP) % KY], uy, DY2[(p / NXP) % KY]);
+      const float z = HAS_DZ ? fmaf(DZA[p / (NXP * KY)], uz, DZ2[p / (NXP * KY)]) : 0.f;
+      return __fadd2_rn(__ffma2_rn(DX[p % NXP], f2(ux), DX2[p % NXP]), f2(y + z));
+    } else {
+      float2 q = __ffma2_rn(f2(uy), dyp(p), DD[p]);
+      q = __ffma2_rn(f2(ux), dxp(p), q);
+      if (HAS_DZ) q = __ffma2_rn(f2(uz), dzp(p), q);
+      return q;
+    }
+  };
 
-  const float kph = (float)(6.283185307179586 * prm.k_r);
-  const float kfs = (float)prm.k_s;
+  const float kph = prm.kph_f;
+  const float kfs = prm.kfs_f;
   // spreading weight (R18): w = R_tx R_rx = (r_t k_s + dU_tx)(r_r k_s + dU_rx) / k_s^2, in samples
   const float inv_ks2 = (float)(1.0 / (prm.k_s * prm.k_s));
 #if SASBP_BININDEX
@@ -615,7 +691,7 @@ __global__ void __launch_bounds__(32 * WY * WZ, (AXIS ? SASBP_MINB_AXIS : SASBP_
   // refraction: interface height relative to the tile centre, slownesses in samples per metre
   const float zbr = MODE == kRefract ? (float)(prm.zb - ct[2]) : 0.f;
   const float k1r = (float)(prm.fs / prm.c), k2r = MODE == kRefract ? (float)(prm.fs / prm.c2) : 0.f;
-  const int nch = prm.ch_hi - prm.ch_lo;
+  const int nch = ch_hi - ch_lo;
   const int nbatch = (nch + kNB - 1) / kNB;
   // Channel order: every tile visits all batches, starting at a batch offset proportional to
   // its launch rank among the resident CTAs (blockIdx / resident).  CTAs that are resident at
@@ -657,7 +733,7 @@ __global__ void __launch_bounds__(32 * WY * WZ, (AXIS ? SASBP_MINB_AXIS : SASBP_
     if (sub < kBPW && bb < nbatch) {
       const int nbb = min(kNB, nch - bat(bb) * kNB);
       if (cl < nbb) {
-        const ChanConst k = chan_prologue<GATE, MOTION, MODE == kRefract>(prm, prm.ch_lo + bat(bb) * kNB + cl, ct, cl,
+        const ChanConst k = chan_prologue<GATE, MOTION, MODE == kRefract>(prm, ch_lo + bat(bb) * kNB + cl, ct, cl,
                                                                          win_base);
         cc[(bb % kRing) * kNB + cl] = k;
         live = !(k.gate & 16);
@@ -674,7 +750,7 @@ __global__ void __launch_bounds__(32 * WY * WZ, (AXIS ? SASBP_MINB_AXIS : SASBP_
   auto issue = [&](int b) {
     if (GATE && !blive[b % kRing]) return;   // dead batch: no loads, no mbarrier phase
     const int nb = min(kNB, nch - bat(b) * kNB);
-    const int ch0 = prm.ch_lo + bat(b) * kNB;
+    const int ch0 = ch_lo + bat(b) * kNB;
     const ChanConst* cb = cc + (b % kRing) * kNB;
     const int c0 = warp * kCW;
     const int mine = max(0, min(kCW, nb - c0));
@@ -787,16 +863,19 @@ __global__ void __launch_bounds__(32 * WY * WZ, (AXIS ? SASBP_MINB_AXIS : SASBP_
     // hot channel constants of the dense series kernels (ux2 uy2 uz2 kap0 | a0..a3 | urr phi0 | ping
     // woff), loaded one channel ahead so the loads' latency overlaps the previous channel's terms
 #if SASBP_CC_PREFETCH
-    constexpr bool kPref = AXIS && !GATE && !MOTION && !WEIGHT && (MODE == kSeries3 || MODE == kSeries4);
+    constexpr bool kPref = ((AXIS && !GATE) || (GATE && SASBP_GATE_PREF)) && !MOTION && !WEIGHT &&
+                           (MODE == kSeries3 || MODE == kSeries4);
 #else
     constexpr bool kPref = false;
 #endif
     const uint32_t cb_a = (uint32_t)__cvta_generic_to_shared(cb);
-    float4 pf0, pf1;
-    float2 pf2, pf5;
+    float4 pf0, pf1, pf5;
+    float2 pf2;
     auto hot = [&](int c) {
       const uint32_t a = cb_a + (uint32_t)c * (uint32_t)sizeof(ChanConst);
-      pf0 = lds128(a); pf1 = lds128(a + 16u); pf2 = lds64(a + 32u); pf5 = lds64(a + 80u);
+      pf0 = lds128(a); pf1 = lds128(a + 16u); pf2 = lds64(a + 32u);
+      if (GATE) pf5 = lds128(a + 80u);   // ping woff klo gate
+      else { const float2 t = lds64(a + 80u); pf5.x = t.x; pf5.y = t.y; }
     };
     if constexpr (kPref) hot(0);
 
@@ -808,13 +887,14 @@ __global__ void __launch_bounds__(32 * WY * WZ, (AXIS ? SASBP_MINB_AXIS : SASBP_
     for (int c = 0; c < nb; ++c) {
       ChanConst kc;
       if constexpr (kPref) {
-        const float4 r0 = pf0, r1 = pf1;
-        const float2 r2 = pf2, r5 = pf5;
+        const float4 r0 = pf0, r1 = pf1, r5 = pf5;
+        const float2 r2 = pf2;
         if (c + 1 < nb) hot(c + 1);
         kc.ux2 = r0.x; kc.uy2 = r0.y; kc.uz2 = r0.z; kc.kap0 = r0.w;
         kc.a0 = r1.x; kc.a1 = r1.y; kc.a2 = r1.z; kc.a3 = r1.w;
         kc.urr = r2.x; kc.phi0 = r2.y;
         kc.ping = __float_as_int(r5.x); kc.woff = __float_as_int(r5.y);
+        if (GATE) kc.gate = __float_as_int(r5.w);
       } else {
 #if SASBP_CC_LDS
         kc = lds_struct<ChanConst>(cb_s + (uint32_t)c * (uint32_t)sizeof(ChanConst));
@@ -830,16 +910,8 @@ __global__ void __launch_bounds__(32 * WY * WZ, (AXIS ? SASBP_MINB_AXIS : SASBP_
         }
         if (GATE) {   // transmit-cone mask of this thread's pixels for the new ping
           mtx = 0xFFu;
-          if ((kc.gate & 3) == kGEdge) {
-            double a[3], bb[3], x[3];
-            ping_axes(prm, cur_ping, a, bb);
-            mtx = 0u;
-#pragma unroll
-            for (int k = 0; k < 2 * NP; ++k) {
-              pixel_centre64(prm, tm.ix(k), tm.iy(k), tm.iz(k), x);
-              if (in_fov_px(prm, x, prm.tx + 3 * cur_ping, a, bb)) mtx |= 1u << k;
-            }
-          }
+          if ((kc.gate & 3) == kGEdge)
+            mtx = gate_mask<TM, 2 * NP>(&prm, tm, cur_ping, prm.tx + 3 * cur_ping, (1u << (2 * NP)) - 1u);
         }
         // transmit leg, exact range-relative form: dR = q / (sqrt(r^2 + q) + r), in samples
 #if SASBP_TX_SERIES
@@ -861,9 +933,7 @@ __global__ void __launch_bounds__(32 * WY * WZ, (AXIS ? SASBP_MINB_AXIS : SASBP_
             BT[p] = make_float2(t0v - kc.r_t, t1v - kc.r_t);
             continue;
           }
-          float2 q = __ffma2_rn(f2(kc.tx2y), dyp(p), DD[p]);
-          q = __ffma2_rn(f2(kc.tx2x), dxp(p), q);
-          if (HAS_DZ) q = __ffma2_rn(f2(kc.tx2z), dzp(p), q);
+          const float2 q = qpair(p, kc.tx2x, kc.tx2y, kc.tx2z);
 #if SASBP_TX_SERIES
           if (MODE == kSeries3 || MODE == kSeries4) {   // far field: the rx leg's series, no MUFU
             float2 h = MODE == kSeries4 ? __ffma2_rn(f2(ta3), q, f2(ta2)) : f2(ta2);
@@ -884,14 +954,8 @@ __global__ void __launch_bounds__(32 * WY * WZ, (AXIS ? SASBP_MINB_AXIS : SASBP_
       if (GATE) {
         msk = mtx;
         if (((kc.gate >> 2) & 3) == kGEdge) {   // receive-cone mask (bistatic), per channel
-          double a[3], bb[3], x[3];
-          ping_axes(prm, kc.ping, a, bb);
-          const int chg = prm.ch_lo + bat(b) * kNB + c;
-#pragma unroll
-          for (int k = 0; k < 2 * NP; ++k) {
-            pixel_centre64(prm, tm.ix(k), tm.iy(k), tm.iz(k), x);
-            if (!in_fov_px(prm, x, prm.rx + 3 * (size_t)chg, a, bb)) msk &= ~(1u << k);
-          }
+          const int chg = ch_lo + bat(b) * kNB + c;
+          msk = gate_mask<TM, 2 * NP>(&prm, tm, kc.ping, prm.rx + 3 * (size_t)chg, msk);
         }
         masked = (kc.gate & 3) == kGEdge || ((kc.gate >> 2) & 3) == kGEdge;   // warp-uniform
       }
@@ -900,96 +964,109 @@ __global__ void __launch_bounds__(32 * WY * WZ, (AXIS ? SASBP_MINB_AXIS : SASBP_
 #endif
       const float rtk = WEIGHT ? kc.r_t * kfs : 0.f;               // r_t, r_r in samples
       const float rrk = WEIGHT ? kc.r_r * kfs * inv_ks2 : 0.f;
+      // the pixel loop; MSK = per-pixel gate selects (edge channels).  With SASBP_GATE_SPLIT the
+      // selects are compiled into a second copy taken only by channels whose tile straddles a cone
+      // edge (warp-uniform branch); otherwise every channel of a gated kernel pays them.
+      auto pixels = [&](auto msk_tag) {
+        constexpr bool MSK = decltype(msk_tag)::value;
 #pragma unroll
-      for (int p = 0; p < NP; ++p) {
-        float2 q = __ffma2_rn(f2(kc.uy2), dyp(p), DD[p]);
-        q = __ffma2_rn(f2(kc.ux2), dxp(p), q);
-        if (HAS_DZ) q = __ffma2_rn(f2(kc.uz2), dzp(p), q);
-        float2 U;
-        float2 wgt = f2(1.f);
-        float2 srr = f2(0.f);   // exact-mode moving receiver: |x - rx'| per pixel
-        if (MODE == kRefract) {
-          const float r0 = refr_time32(dxp(p).x - kc.ux2, dyp(p).x - kc.uy2, dzp(p).x - kc.uz2, zbr - kc.uz2,
-                                       dzp(p).x - zbr, k1r, k2r);
-          const float r1 = refr_time32(dxp(p).y - kc.ux2, dyp(p).y - kc.uy2, dzp(p).y - kc.uz2, zbr - kc.uz2,
-                                       dzp(p).y - zbr, k1r, k2r);
-          U = __fadd2_rn(make_float2(r0 - kc.a1, r1 - kc.a1), BT[p]);
-        } else if (MODE == kExact) {
-          const float2 r2 = __fadd2_rn(q, f2(kc.r2_r));
-          const float den0 = leg_den(r2.x, kc.r_r);
-          const float den1 = leg_den(r2.y, kc.r_r);
-          if (MOTION) srr = __fadd2_rn(make_float2(den0, den1), f2(-kc.r_r));   // |x - rx'|
-          if (WEIGHT) {
-            const float2 dU = __fmul2_rn(__fmul2_rn(q, make_float2(rcp_approx(den0), rcp_approx(den1))), f2(kfs));
-            U = __fadd2_rn(dU, BT[p]);
-            wgt = __fmul2_rn(__fadd2_rn(BT[p], f2(rtk)), __ffma2_rn(dU, f2(inv_ks2), f2(rrk)));
+        for (int p = 0; p < NP; ++p) {
+          const float2 q = qpair(p, kc.ux2, kc.uy2, kc.uz2);
+          float2 U;
+          float2 wgt = f2(1.f);
+          float2 srr = f2(0.f);   // exact-mode moving receiver: |x - rx'| per pixel
+          if (MODE == kRefract) {
+            const float r0 = refr_time32(dxp(p).x - kc.ux2, dyp(p).x - kc.uy2, dzp(p).x - kc.uz2, zbr - kc.uz2,
+                                         dzp(p).x - zbr, k1r, k2r);
+            const float r1 = refr_time32(dxp(p).y - kc.ux2, dyp(p).y - kc.uy2, dzp(p).y - kc.uz2, zbr - kc.uz2,
+                                         dzp(p).y - zbr, k1r, k2r);
+            U = __fadd2_rn(make_float2(r0 - kc.a1, r1 - kc.a1), BT[p]);
+          } else if (MODE == kExact) {
+            const float2 r2 = __fadd2_rn(q, f2(kc.r2_r));
+            const float den0 = leg_den(r2.x, kc.r_r);
+            const float den1 = leg_den(r2.y, kc.r_r);
+            if (MOTION) srr = __fadd2_rn(make_float2(den0, den1), f2(-kc.r_r));   // |x - rx'|
+            if (WEIGHT) {
+              const float2 dU = __fmul2_rn(__fmul2_rn(q, make_float2(rcp_approx(den0), rcp_approx(den1))), f2(kfs));
+              U = __fadd2_rn(dU, BT[p]);
+              wgt = __fmul2_rn(__fadd2_rn(BT[p], f2(rtk)), __ffma2_rn(dU, f2(inv_ks2), f2(rrk)));
+            } else {
+              U = __ffma2_rn(__fmul2_rn(q, make_float2(rcp_approx(den0), rcp_approx(den1))), f2(kfs), BT[p]);
+            }
           } else {
-            U = __ffma2_rn(__fmul2_rn(q, make_float2(rcp_approx(den0), rcp_approx(den1))), f2(kfs), BT[p]);
+            float2 h;
+            if (MODE == kSeries4) {
+              h = __ffma2_rn(f2(kc.a3), q, f2(kc.a2));
+              h = __ffma2_rn(h, q, f2(kc.a1));
+            } else {
+              h = __ffma2_rn(f2(kc.a2), q, f2(kc.a1));
+            }
+            h = __ffma2_rn(h, q, f2(kc.a0));
+            if (WEIGHT) {
+              const float2 dU = __fmul2_rn(q, h);
+              U = __fadd2_rn(dU, BT[p]);
+              wgt = __fmul2_rn(__fadd2_rn(BT[p], f2(rtk)), __ffma2_rn(dU, f2(inv_ks2), f2(rrk)));
+            } else {
+              U = __ffma2_rn(q, h, BT[p]);
+            }
           }
-        } else {
-          float2 h;
-          if (MODE == kSeries4) {
-            h = __ffma2_rn(f2(kc.a3), q, f2(kc.a2));
-            h = __ffma2_rn(h, q, f2(kc.a1));
-          } else {
-            h = __ffma2_rn(f2(kc.a2), q, f2(kc.a1));
+  #if SASBP_BININDEX
+          if (MOTION) {   // moving receiver: U' = dU / (1 + w.v/c) ~ dU (kap0 + kg.d)
+            float2 kap = __ffma2_rn(f2(kc.kgy), dyp(p), f2(kc.kap0));
+            kap = __ffma2_rn(f2(kc.kgx), dxp(p), kap);
+            if (HAS_DZ) kap = __ffma2_rn(f2(kc.kgz), dzp(p), kap);
+            U = __fmul2_rn(U, kap);
           }
-          h = __ffma2_rn(h, q, f2(kc.a0));
-          if (WEIGHT) {
-            const float2 dU = __fmul2_rn(q, h);
-            U = __fadd2_rn(dU, BT[p]);
-            wgt = __fmul2_rn(__fadd2_rn(BT[p], f2(rtk)), __ffma2_rn(dU, f2(inv_ks2), f2(rrk)));
+          const float2 T = __fadd2_rn(U, f2(urrv));            // exponent-aligned window coordinate V
+  #else
+          if (MOTION) {   // moving receiver: U = dU / (1 + w.v/c) ~ dU (kap0 + kg.d) + urr
+            float2 kap = __ffma2_rn(f2(kc.kgy), dyp(p), f2(kc.kap0));
+            kap = __ffma2_rn(f2(kc.kgx), dxp(p), kap);
+            if (HAS_DZ) kap = __ffma2_rn(f2(kc.kgz), dzp(p), kap);
+            if (MODE == kExact) {   // exact: kappa = |x - rx'| / (|x - rx'| + (u + d).v / c)
+              const float2 dn = __fadd2_rn(srr, kap);
+              kap = __fmul2_rn(srr, make_float2(rcp_approx(dn.x), rcp_approx(dn.y)));
+            }
+            U = __ffma2_rn(U, kap, f2(kc.urr));
           } else {
-            U = __ffma2_rn(q, h, BT[p]);
+            U = __fadd2_rn(U, f2(kc.urr));                     // centred window coordinate
+          }
+          const float2 T = __fadd2_rn(U, f2(kMagic));          // rn(U) in the mantissa
+  #endif
+          const float2 ph = __ffma2_rn(U, f2(kph), f2(kc.phi0));
+  #pragma unroll
+          for (int s = 0; s < 2; ++s) {
+            const float Us = s ? U.y : U.x;
+            const float Ts = s ? T.y : T.x;
+            const float phs = s ? ph.y : ph.x;
+  #if SASBP_BININDEX
+            uint32_t addr = ((uint32_t)__float_as_int(Ts) >> vsh & vmask) + (uint32_t)kc.woff;
+  #else
+            uint32_t addr = (uint32_t)__float_as_int(Ts) * 16u + (uint32_t)kc.woff;
+  #endif
+            if (MSK && masked) {   // gated-out pixel: read the zero cell
+              const uint32_t mk = 0u - ((msk >> (2 * p + s)) & 1u);
+              addr = (addr & mk) | (zcell & ~mk);
+            }
+            const float4 w = lds128(addr);
+            float2 eh = __ffma2_rn(f2(Us), make_float2(w.z, w.w), make_float2(w.x, w.y));
+            if (WEIGHT) eh = __fmul2_rn(eh, f2(s ? wgt.y : wgt.x));
+            float sn, cs;
+            __sincosf(phs, &sn, &cs);
+            const float2 rot = make_float2(cs, sn);
+            A[2 * p + s] = __ffma2_rn(f2(eh.x), rot, A[2 * p + s]);
+            B[2 * p + s] = __ffma2_rn(f2(eh.y), rot, B[2 * p + s]);
           }
         }
-#if SASBP_BININDEX
-        if (MOTION) {   // moving receiver: U' = dU / (1 + w.v/c) ~ dU (kap0 + kg.d)
-          float2 kap = __ffma2_rn(f2(kc.kgy), dyp(p), f2(kc.kap0));
-          kap = __ffma2_rn(f2(kc.kgx), dxp(p), kap);
-          if (HAS_DZ) kap = __ffma2_rn(f2(kc.kgz), dzp(p), kap);
-          U = __fmul2_rn(U, kap);
-        }
-        const float2 T = __fadd2_rn(U, f2(urrv));            // exponent-aligned window coordinate V
+      };
+      if constexpr (GATE) {
+#if SASBP_GATE_SPLIT
+        if (masked) pixels(std::true_type{}); else pixels(std::false_type{});
 #else
-        if (MOTION) {   // moving receiver: U = dU / (1 + w.v/c) ~ dU (kap0 + kg.d) + urr
-          float2 kap = __ffma2_rn(f2(kc.kgy), dyp(p), f2(kc.kap0));
-          kap = __ffma2_rn(f2(kc.kgx), dxp(p), kap);
-          if (HAS_DZ) kap = __ffma2_rn(f2(kc.kgz), dzp(p), kap);
-          if (MODE == kExact) {   // exact: kappa = |x - rx'| / (|x - rx'| + (u + d).v / c)
-            const float2 dn = __fadd2_rn(srr, kap);
-            kap = __fmul2_rn(srr, make_float2(rcp_approx(dn.x), rcp_approx(dn.y)));
-          }
-          U = __ffma2_rn(U, kap, f2(kc.urr));
-        } else {
-          U = __fadd2_rn(U, f2(kc.urr));                     // centred window coordinate
-        }
-        const float2 T = __fadd2_rn(U, f2(kMagic));          // rn(U) in the mantissa
+        pixels(std::true_type{});
 #endif
-        const float2 ph = __ffma2_rn(U, f2(kph), f2(kc.phi0));
-#pragma unroll
-        for (int s = 0; s < 2; ++s) {
-          const float Us = s ? U.y : U.x;
-          const float Ts = s ? T.y : T.x;
-          const float phs = s ? ph.y : ph.x;
-#if SASBP_BININDEX
-          uint32_t addr = ((uint32_t)__float_as_int(Ts) >> vsh & vmask) + (uint32_t)kc.woff;
-#else
-          uint32_t addr = (uint32_t)__float_as_int(Ts) * 16u + (uint32_t)kc.woff;
-#endif
-          if (GATE && masked) {   // gated-out pixel: read the zero cell
-            const uint32_t mk = 0u - ((msk >> (2 * p + s)) & 1u);
-            addr = (addr & mk) | (zcell & ~mk);
-          }
-          const float4 w = lds128(addr);
-          float2 eh = __ffma2_rn(f2(Us), make_float2(w.z, w.w), make_float2(w.x, w.y));
-          if (WEIGHT) eh = __fmul2_rn(eh, f2(s ? wgt.y : wgt.x));
-          float sn, cs;
-          __sincosf(phs, &sn, &cs);
-          const float2 rot = make_float2(cs, sn);
-          A[2 * p + s] = __ffma2_rn(f2(eh.x), rot, A[2 * p + s]);
-          B[2 * p + s] = __ffma2_rn(f2(eh.y), rot, B[2 * p + s]);
-        }
+      } else {
+        pixels(std::false_type{});
       }
     }
   }
@@ -999,6 +1076,7 @@ __global__ void __launch_bounds__(32 * WY * WZ, (AXIS ? SASBP_MINB_AXIS : SASBP_
     if (tm.valid(prm, k)) {
       float2* o = prm.image + ((size_t)tm.iz(k) * prm.ny + tm.iy(k)) * prm.nx + tm.ix(k);
       float2 v = make_float2(A[k].x - B[k].y, A[k].y + B[k].x);
+      if (red) { atomicAdd(o, v); continue; }   // wave-tail partial (image zeroed by the launch)
       if (prm.accumulate) { const float2 a = *o; v.x += a.x; v.y += a.y; }
       *o = v;
     }
@@ -1014,7 +1092,9 @@ __global__ void __launch_bounds__(32 * WY * WZ) count_kernel(const TdbpParams pr
   using TM = TileMap<KX, KY, KZ, WY, WZ>;
   constexpr int K = TM::K;
   static_assert(K <= 32, "pixel masks are 32-bit");
-  __shared__ ChanConst cc[kNB];
+  constexpr int kCB = 32 * WY * WZ;   // channels per prologue batch: one per thread (the fp64
+                                      // prologue is most of K3's work; 16 lanes of 128 left 7/8 idle)
+  __shared__ ChanConst cc[kCB];
   const TM tm(prm);
   const int tid = threadIdx.x;
   double ct[3];
@@ -1031,8 +1111,8 @@ __global__ void __launch_bounds__(32 * WY * WZ) count_kernel(const TdbpParams pr
   unsigned long long cnt = 0;
   int cur_ping = -1;
   uint32_t mtx = 0xFFFFFFFFu;
-  for (int ch0 = prm.ch_lo; ch0 < prm.ch_hi; ch0 += kNB) {
-    const int nb = min(kNB, prm.ch_hi - ch0);
+  for (int ch0 = prm.ch_lo; ch0 < prm.ch_hi; ch0 += kCB) {
+    const int nb = min(kCB, prm.ch_hi - ch0);
     __syncthreads();
     if (tid < nb) cc[tid] = chan_prologue<true, true>(prm, ch0 + tid, ct, tid, 0u);
     __syncthreads();

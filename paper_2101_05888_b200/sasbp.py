@@ -36,7 +36,8 @@ class SasError(RuntimeError):
 
 class sas_bp_plan(ctypes.Structure):
     _fields_ = [("tile", ctypes.c_int32 * 3), ("window", ctypes.c_int32), ("rx_mode", ctypes.c_int32),
-                ("tma", ctypes.c_int32), ("batch", ctypes.c_int32), ("ctas_per_sm", ctypes.c_int32)]
+                ("tma", ctypes.c_int32), ("batch", ctypes.c_int32), ("ctas_per_sm", ctypes.c_int32),
+                ("tail_split", ctypes.c_int32)]
 
 
 class sas_beam(ctypes.Structure):
@@ -328,7 +329,7 @@ class Backprojector:
         _check(_lib.sas_bp_get_plan(self._h, ctypes.byref(p)))
         return {"tile": tuple(p.tile), "window": p.window, "rx_mode": ("series3", "series4", "exact", "refracted")[p.rx_mode]
                 if p.rx_mode >= 0 else None, "tma": None if p.tma < 0 else bool(p.tma), "batch": p.batch,
-                "ctas_per_sm": p.ctas_per_sm}
+                "ctas_per_sm": p.ctas_per_sm, "tail_split": p.tail_split}
 
     @property
     def workspace_bytes(self) -> int:

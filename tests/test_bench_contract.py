@@ -53,4 +53,4 @@ def test_bench_default_is_the_3d_config(monkeypatch):
     import bench
     monkeypatch.setattr(sys, "argv", ["bench.py"])
     a = bench.parse()
-    assert a.config == 4 and a.shard == "image" and a.gpus == 1
+    assert a.config == 4 and a.shard == "ping" and a.gpus == 1

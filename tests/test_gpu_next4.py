@@ -387,3 +387,25 @@ def test_weighted_streamed_matches_form(bpmod):
         bp.set_pings(e, s.tx, s.rx, s.t0)
         b = bp.form()
     assert np.max(np.abs(a - b)) <= 1e-5 * np.max(np.abs(b))
+
+
+@pytest.mark.parametrize("Nin,Nh,Nout", [(4096, 63, 1024), (4096, 3, 1024), (4096, 5, 1000), (4096, 7, 1030),
+                                         (8192, 1, 2048), (12, 9, 5), (4100, 201, 1025)])
+def test_baseband_vec4_staging(bpmod, Nin, Nh, Nout, monkeypatch):
+    """D = 4 with 16-byte aligned rows stages the passband input with aligned float4 loads; the
+    window start nlo = m0 D - (Nh - 1)/2 takes every residue mod 4 over these Nh (o = 0, 3, 2, 1),
+    record edges (nlo < 0, the end past Nin) and Nout not a multiple of the CTA's run.  Against the
+    fp64 oracle (R20) and the scalar staging path (SASBP_BB_VEC4=0)."""
+    rng = np.random.default_rng(Nin + Nh + Nout)
+    P, E = 3, 5
+    x = rng.normal(size=(P, E, Nin)).astype(np.float32)
+    h = (2.0 * _lowpass((Nh - 1) // 2, 0.1)) if Nh > 1 else np.array([1.0], dtype=np.float32)
+    t0 = 0.0123 + 1e-4 * np.arange(P)
+    fs, fc = 480e3, 120e3 + 17.0
+    got = bpmod.baseband(x, fs, fc, t0, h, 4, Nout)
+    ref = oracle.baseband(x, fs, fc, t0, h, 4, Nout)
+    scale = max(np.max(np.abs(ref)), 1e-30)
+    assert np.max(np.abs(got - ref)) <= TOL_FILT * scale
+    monkeypatch.setenv("SASBP_BB_VEC4", "0")
+    sc = bpmod.baseband(x, fs, fc, t0, h, 4, Nout)
+    assert np.max(np.abs(sc - ref)) <= TOL_FILT * scale
