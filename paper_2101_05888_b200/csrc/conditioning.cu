@@ -206,14 +206,15 @@ __global__ void __launch_bounds__(256) baseband_blocked_kernel(const float* __re
   const int D = DT ? DT : D_rt;
   extern __shared__ __align__(16) unsigned char bb_smem[];
   float2* hs = reinterpret_cast<float2*>(bb_smem);            // [D][Apad] (h, h)
-  float2* sz = hs + (size_t)D * Apad;                          // [D][LqP] padded polyphase input
+  float2* sz = hs + (size_t)D * Apad + 2;                      // [D][LqP] padded polyphase input (2 slack
+                                                               // slots before row 0: see the float4 staging)
   const long long b = blockIdx.x;
   const long long ch = b / runs;
   const int m0 = (int)(b - ch * runs) * MO;
   const int half = (Nh - 1) >> 1;
   const int nlo = m0 * D + half - (Nh - 1);    // local input i = n - nlo = t D + j
   const int Lq = MO + Apad;                     // samples per phase (+ slack for the last block)
-  const int LqP = bb_pad(Lq) + 1;
+  const int LqP = bb_pad(Lq) + 3;              // >= 3 slack slots after each row
   const float* xc = x + ch * (long long)Nin;
   const double bp = bb_base(t0p, ch / E, fc);
   for (int k = threadIdx.x; k < D * Apad; k += blockDim.x) {   // hq[q][a] = h[Nh - 1 - (a D + q)], zero padded
@@ -242,10 +243,14 @@ __global__ void __launch_bounds__(256) baseband_blocked_kernel(const float* __re
     const int o = nlo & 3;
     const int a0 = nlo - o;
     const int nk = Lq + (o ? 1 : 0);           // float4s covering local inputs [0, 4 Lq)
-    for (int k0 = threadIdx.x; k0 < nk; k0 += kU * Bd) {
-      float4 v[kU];
+    // kV = 9 float4s per thread per step: with 128 threads the 1024 + Apad + 1 float4s of a run
+    // (Apad <= 16) take ONE step; with 8, 17 threads of warp 0 ran a second, almost empty step
+    // that the other warps waited for at the barrier
+    constexpr int kV = 9;
+    for (int k0 = threadIdx.x; k0 < nk; k0 += kV * Bd) {
+      float4 v[kV];
 #pragma unroll
-      for (int u = 0; u < kU; ++u) {
+      for (int u = 0; u < kV; ++u) {
         const int k = k0 + u * Bd;
         const int a = a0 + 4 * k;
         v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -260,8 +265,20 @@ __global__ void __launch_bounds__(256) baseband_blocked_kernel(const float* __re
           }
         }
       }
+      // component j of float4 k lands in phase row (j - o) & 3 at slot k + sj, sj = (j - o) >> 2
+      // (0 or -1); for the slots of this thread's k = k0 + u Bd the padded position is
+      // base_j + u (Bd + Bd/8) (Bd a multiple of 8).  The two components that fall outside slots
+      // 0..Lq-1 (slot -1 of the first float4, slot Lq of the last) go to slack slots nobody reads
+      // (2 before row 0, >= 3 after every row), so the stores need no per-component test.
+      const int inc = Bd + (Bd >> 3);
+      int base[4];
 #pragma unroll
-      for (int u = 0; u < kU; ++u) {
+      for (int j = 0; j < 4; ++j) {
+        const int sj = (j - o) >> 2;
+        base[j] = ((j - o) & 3) * LqP + bb_pad(k0 + sj);
+      }
+#pragma unroll
+      for (int u = 0; u < kV; ++u) {
         const int k = k0 + u * Bd;
         if (k >= nk) break;
         double ph = fma((double)(a0 + 4 * k), kr, bp);   // cycles at component 0, fp64
@@ -272,8 +289,7 @@ __global__ void __launch_bounds__(256) baseband_blocked_kernel(const float* __re
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           if (j) w = __ffma2_rn(make_float2(w.y, w.y), rotp, __fmul2_rn(make_float2(w.x, w.x), rot));
-          const int i = 4 * k + j - o;
-          if (i >= 0 && i < 4 * Lq) sz[(i & 3) * LqP + bb_pad(i >> 2)] = __fmul2_rn(make_float2(vv[j], vv[j]), w);
+          sz[base[j] + u * inc] = __fmul2_rn(make_float2(vv[j], vv[j]), w);
         }
       }
     }
@@ -451,8 +467,8 @@ static sas_status bb_launch(const float* x, int32_t P, int32_t E, int32_t Nin, d
   for (; threads >= 32; threads >>= 1) {
     const long long MOb = (long long)threads * kBbR;
     const long long Lq = MOb + Apad;
-    const long long LqP = Lq + (Lq >> 3) + 1;
-    smem = ((size_t)D * Apad + (size_t)D * LqP) * sizeof(float2);
+    const long long LqP = Lq + (Lq >> 3) + 3;
+    smem = ((size_t)D * Apad + (size_t)D * LqP + 2) * sizeof(float2);
     if (smem <= 200 * 1024) break;
   }
   const char* force = getenv("SASBP_BB_SIMPLE");

@@ -52,7 +52,7 @@ cudaError_t launch_k(Kern kern, int threads, const TdbpParams& prm_in, const Tma
   unsigned grid = blocks;
   const int R = per_sm * sms;
   const char* nt = getenv("SASBP_NO_TAILSPLIT");
-  if (!(nt && nt[0] == '1') && !prm.accumulate && R > 0 && prm.ch_hi - prm.ch_lo >= 2) {
+  if (SASBP_TAILSPLIT && !(nt && nt[0] == '1') && !prm.accumulate && R > 0 && prm.ch_hi - prm.ch_lo >= 2) {
     const unsigned tail = blocks % (unsigned)R;
     if (tail > 0 && 2 * tail <= (unsigned)R) {
       prm.tail0 = (int)(blocks - tail);

@@ -265,8 +265,12 @@ __global__ void __launch_bounds__(kFT) rc_prep_kernel(const float2* __restrict__
 // after each record keep the circular correlation of one channel from reaching the next, so each
 // output n < Ns at position c S + n is alias free (c S + n + Nr - 1 < (c + 1) S <= L).  The same
 // transform then serves kpb channels instead of one (config 4: Ns = 1024, Nr = 160, 3 per block).
+#ifndef RC_MINB_PACK
+#define RC_MINB_PACK 2   // CTAs per SM for the packed-record instantiation: its index math spilled at 3
+                         // (80 registers, 148 B of spills); 2 CTAs / 128 registers: config 4 2.29 -> 2.23 ms
+#endif
 template <bool PACK>
-__global__ void __launch_bounds__(kFT, RC_MINB) rc_fft_kernel(const float2* __restrict__ raw, int Ns, int V, int lag0,
+__global__ void __launch_bounds__(kFT, PACK ? RC_MINB_PACK : RC_MINB) rc_fft_kernel(const float2* __restrict__ raw, int Ns, int V, int lag0,
                                                         const float2* __restrict__ H, const float2* __restrict__ tw_g,
                                                         float2* __restrict__ out, long long nch, int S, int kpb,
                                                         uint32_t mS) {

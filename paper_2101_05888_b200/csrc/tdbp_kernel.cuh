@@ -76,6 +76,23 @@ namespace sasbp {
 // ahead (A/B config 4: +1.6 %; the register-tighter 2D kernel lost 1.5 % with it)
 #define SASBP_CC_PREFETCH 1
 #endif
+#ifndef SASBP_GRIDCONST
+#define SASBP_GRIDCONST 1   // K2 params as __grid_constant__ (gate_mask() takes their address without a copy)
+#endif
+#if SASBP_GRIDCONST
+#define SASBP_PRM_QUAL const __grid_constant__
+#else
+#define SASBP_PRM_QUAL const
+#endif
+#ifndef SASBP_KPH_PARAM
+#define SASBP_KPH_PARAM 1   // 2 pi fc/fs and fs/c as host-computed floats (0: derived on the device)
+#endif
+#ifndef SASBP_TAILSPLIT
+#define SASBP_TAILSPLIT 1   // wave-tail split support in K2 (0: kernel without it, host never splits; A/B)
+#endif
+#ifndef SASBP_XFORM_CURSOR
+#define SASBP_XFORM_CURSOR 1   // window transform with per-lane cursors (0: indexed form, A/B)
+#endif
 #ifndef SASBP_DIV_MULHI
 #define SASBP_DIV_MULHI 1
 #endif
@@ -585,7 +602,7 @@ SASBP_MASK_FN uint32_t gate_mask(const TdbpParams* prm, const TM tm, int ping, c
 template <int KX, int KY, int KZ, int WY, int WZ, bool HAS_DZ, int MODE, bool USE_TMA, bool GATE = false,
           bool MOTION = false, bool AXIS = false, bool WEIGHT = false>
 __global__ void __launch_bounds__(32 * WY * WZ, (AXIS ? SASBP_MINB_AXIS : SASBP_MINB) * 4 / (WY * WZ))
-    tdbp_kernel(const __grid_constant__ TdbpParams prm,
+    tdbp_kernel(SASBP_PRM_QUAL TdbpParams prm,
                                                                           const __grid_constant__ TmaDesc tmap) {
   using TM = TileMap<KX, KY, KZ, WY, WZ>;
   constexpr int NP = TM::NP;
@@ -607,7 +624,7 @@ __global__ void __launch_bounds__(32 * WY * WZ, (AXIS ? SASBP_MINB_AXIS : SASBP_
   // tile of this CTA and its channel range (a wave-tail tile is shared by tsplit CTAs)
   int tile = (int)blockIdx.x, ch_lo = prm.ch_lo, ch_hi = prm.ch_hi;
   bool red = false;
-  if (prm.tsplit > 1 && tile >= prm.tail0) {
+  if (SASBP_TAILSPLIT && prm.tsplit > 1 && tile >= prm.tail0) {
     const int r = tile - prm.tail0, sp = r % prm.tsplit;
     const long long n = (long long)prm.ch_hi - prm.ch_lo;
     tile = prm.tail0 + r / prm.tsplit;
@@ -676,8 +693,13 @@ __global__ void __launch_bounds__(32 * WY * WZ, (AXIS ? SASBP_MINB_AXIS : SASBP_
     }
   };
 
+#if SASBP_KPH_PARAM
   const float kph = prm.kph_f;
   const float kfs = prm.kfs_f;
+#else
+  const float kph = (float)(6.283185307179586 * prm.k_r);
+  const float kfs = (float)prm.k_s;
+#endif
   // spreading weight (R18): w = R_tx R_rx = (r_t k_s + dU_tx)(r_r k_s + dU_rx) / k_s^2, in samples
   const float inv_ks2 = (float)(1.0 / (prm.k_s * prm.k_s));
 #if SASBP_BININDEX
@@ -817,8 +839,40 @@ __global__ void __launch_bounds__(32 * WY * WZ, (AXIS ? SASBP_MINB_AXIS : SASBP_
       }
     }
 #else
-    {  // warp w rewrites channels w, w+kWarps, ...: two cells per lane-step, flattened over
-       // (channel, cell pair) so the lanes stay busy across channel boundaries
+    if constexpr (SASBP_XFORM_CURSOR && !SASBP_BININDEX && !GATE) {
+       // warp w rewrites channels w, w+kWarps, ...: two cells per lane-step, flattened over
+       // (channel, cell pair) so the lanes stay busy across channel boundaries.  Each lane keeps
+       // cursors (raw source, cell destination, cell coordinate) and advances them by 32 pairs,
+       // wrapping to its next channel when it runs past the P2 pairs of one: no division and no
+       // re-derived smem offsets per step (the indexed form spent ~50 of 62 instructions per
+       // step on index math the compiler rematerialised under register pressure).
+      const int nmine = (nb - warp + kWarps - 1) / kWarps;
+      const int tot = nmine * P2;
+      int t = lane, q = 0;
+      while (t >= P2) { t -= P2; ++q; }
+      const unsigned char* rp = rawp + (warp + q * kWarps) * rsb + 16 * t;
+      float4* wp = win + (warp + q * kWarps) * W + 2 * t;
+      const ChanConst* gp = cc + (b % kRing) * kNB + warp + q * kWarps;
+      float j0 = (float)(Wh - 2 * t) + 0.5f;
+      const int rwrap = kWarps * (int)rsb - 16 * P2, wwrap = kWarps * W - 2 * P2;
+      for (int i = lane; i < tot; i += 32) {
+        if (!GATE || !(gp->gate & 16)) {
+          const float4 d01 = *reinterpret_cast<const float4*>(rp);
+          const float2 d2 = *reinterpret_cast<const float2*>(rp + 16);
+          const float2 d0 = make_float2(d01.x, d01.y), d1 = make_float2(d01.z, d01.w);
+          const float2 s0 = __fadd2_rn(d1, make_float2(-d0.x, -d0.y));
+          const float2 s1 = __fadd2_rn(d2, make_float2(-d1.x, -d1.y));
+          const float2 i0 = __ffma2_rn(s0, f2(j0), d0);
+          const float2 i1 = __ffma2_rn(s1, f2(j0 - 1.0f), d1);
+          wp[0] = make_float4(i0.x, i0.y, s0.x, s0.y);
+          if (2 * t + 1 < W) wp[1] = make_float4(i1.x, i1.y, s1.x, s1.y);
+        }
+        t += 32; rp += 512; wp += 64; j0 -= 64.f;
+        while (t >= P2) { t -= P2; rp += rwrap; wp += wwrap; j0 += (float)(2 * P2); gp += kWarps; }
+      }
+    } else {
+       // indexed form (the gated kernels: the cursor form cost them 7 % in register allocation,
+       // profiles/ab_r02.txt): flattened over (channel, cell pair) so the lanes stay busy
       const int nmine = (nb - warp + kWarps - 1) / kWarps;
       const int tot = nmine * P2;
       for (int i = lane; i < tot; i += 32) {

@@ -38,9 +38,14 @@ def child(lib, cfg, pings, forms, env_extra=None):
     b.record()
     torch.cuda.synchronize()
     ms = a.elapsed_time(b) / forms
+    try:   # clocks / power right after the timed forms (a throttled box shows here)
+        q = subprocess.run(["nvidia-smi", "--query-gpu=clocks.sm,power.draw,clocks_event_reasons.active",
+                            "--format=csv,noheader"], capture_output=True, text=True, timeout=20).stdout.strip()
+    except Exception:
+        q = ""
     terms = bp.shape[0] * bp.shape[1] * bp.shape[2] * P * s.E
     print(json.dumps({"lib": lib, "config": cfg, "pings": P, "ms": ms, "Gterm_per_s": terms / ms / 1e6,
-                      "plan": bp.plan()}))
+                      "plan": bp.plan(), "smi": q}))
 
 
 def main():
@@ -70,7 +75,7 @@ def main():
                     continue
                 d = json.loads(line[0])
                 print(f"rep {rep} cfg {c} {os.path.basename(spec):36s} {d['ms']:9.2f} ms  {d['Gterm_per_s']:8.1f} Gterm/s  "
-                      f"occ {d['plan']['ctas_per_sm']}", flush=True)
+                      f"occ {d['plan']['ctas_per_sm']}  [{d.get('smi', '')}]", flush=True)
 
 
 if __name__ == "__main__":
