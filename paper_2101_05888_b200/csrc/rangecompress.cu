@@ -15,7 +15,9 @@
 // Direct path (2048 < Nr <= 8192): correlation in shared memory (FP32 complex MAC).
 #include "sasbp.h"
 
+#include <algorithm>
 #include <cstdarg>
+#include <cstdint>
 #include <cstdio>
 #include <cmath>
 #include <cstdlib>
@@ -324,6 +326,252 @@ __global__ void __launch_bounds__(kFT, PACK ? RC_MINB_PACK : RC_MINB) rc_fft_ker
   }
 }
 
+// ---------------------------------------------------------------- FFT overlap-save, pipelined (round 2)
+//
+// The same transform as rc_fft_kernel (same blocks, same spectrum product, same outputs), with the
+// block input staged through shared memory instead of loaded by each thread:
+//  * persistent CTAs (RC_PIPE_MINB per SM) walk the blocks with a grid stride;
+//  * each block's input lands in one of two staging buffers by 1D bulk copies (cp.async.bulk
+//    global -> shared, completion counted on the buffer's mbarrier): a long record's block window
+//    is one copy, a packed block's records one copy each, at their positions c S - lag0;
+//  * the copy of block t + 2 is issued as soon as every thread has read block t's input, so it
+//    streams in while blocks t and t + 1 are transformed (rc_fft_kernel issued its 16 loads per
+//    thread and waited: 3.2 long-scoreboard stall cycles per issued instruction, 58 % issue);
+//  * the packed layout's zero gaps are written once per CTA (copies never touch them); a ragged
+//    last block and long-record blocks at a channel edge zero their uncovered span after the wait;
+//  * shared-memory indices are compile-time offsets from one base per pass (pad() distributes over
+//    multiples of 16).
+// Requires Ns even and a 16-byte aligned raw pointer (then every copy is 16-byte aligned: records
+// start at even elements, windows at start = b V + lag0 with V even, and a buffer shift s = lag0 & 1
+// gives the smem side the same parity); otherwise rc_fft_kernel runs.
+#ifndef RC_PIPE_MINB
+#define RC_PIPE_MINB 2
+#endif
+#ifndef RC_PIPE_NBUF
+#define RC_PIPE_NBUF 1   // staging buffers per CTA (1: block t + 1 is copied while block t is transformed; A/B: 2 no faster)
+#endif
+constexpr int kNBuf = RC_PIPE_NBUF;
+#ifndef RC_PIPE_PP
+#define RC_PIPE_PP 1     // two exchange buffers in alternation (4 barriers per block instead of 8; A/B +0-2 %)
+#endif
+constexpr int kNX = RC_PIPE_PP ? 2 : 1;   // exchange buffers
+constexpr int kBufE = kL + 8;   // staging buffer: block element i at index s + i, s in {0, 1}; +1 rounding
+
+__device__ __forceinline__ uint32_t rc_smaddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void rc_bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
+}
+__device__ __forceinline__ void rc_expect(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void rc_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(bar), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void rc_fence_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// one Stockham pass as pass_store, shared indices as constant offsets: pad(base + r NS) =
+// pad(base) + r (NS = 1: base is a multiple of 16) or pad(base) + r * 17 NS / 16 (NS multiple of 16)
+template <bool INV, int NS>
+__device__ __forceinline__ void pass_store_c(float2 v[16], float2* sm, const float2* __restrict__ tw, int j) {
+  const int k = j & (NS - 1);
+  if (NS > 1) {
+    float2 w1 = twid(tw, (k * (256 / NS)) & (kL - 1));
+    if (INV) w1.y = -w1.y;
+    float2 wr = w1;
+#pragma unroll
+    for (int r = 1; r < 16; ++r) {
+      if (r > 1) wr = cmul(wr, w1);
+      v[r] = cmul(v[r], wr);
+    }
+  }
+  dft16<INV, false>(v);
+  float2* p = sm + pad((j - k) * 16 + k);
+  constexpr int kStep = NS == 1 ? 1 : NS + NS / 16;
+#pragma unroll
+  for (int r = 0; r < 16; ++r) p[r * kStep] = v[sig(r)];
+}
+// load_smem with constant offsets: pad(j + 256 r) = pad(j) + 272 r
+__device__ __forceinline__ void load_smem_c(float2 v[16], const float2* sm, int j) {
+  const float2* p = sm + pad(j);
+#pragma unroll
+  for (int r = 0; r < 16; ++r) v[r] = p[r * (kFT + kFT / 16)];
+}
+
+struct RcPipeArgs {
+  const float2* raw;   // [nch][Ns], 16-byte aligned, Ns even
+  const float2* H;     // [kL] spectrum of the filter (rc_prep_kernel)
+  const float2* tw;    // [kL] twiddles
+  float2* out;         // [nch][Ns]
+  long long nch;
+  long long nblk;      // blocks
+  int Ns, V, lag0;     // long records: V even (block b of a channel starts at bi V + lag0)
+  int bpc;             // long records: blocks per channel
+  int S, kpb;          // packed: record stride (even, >= Ns + Nr - 1) and records per block
+  uint32_t mS;         // packed: i / S as a multiply-high
+};
+
+template <bool PACK>
+__global__ void __launch_bounds__(kFT, RC_PIPE_MINB) rc_pipe_kernel(const __grid_constant__ RcPipeArgs a) {
+  extern __shared__ __align__(128) unsigned char rc_dsm[];
+  float2* buf = reinterpret_cast<float2*>(rc_dsm);          // [kNBuf][kBufE] staging
+  float2* sm = buf + kNBuf * kBufE;                          // [kNX][kPad] exchange
+  float2* sm2 = sm + (kNX - 1) * kPad;
+  (void)sm2;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + kNX * kPad);   // [2]
+  const int j = threadIdx.x;
+  const int s = a.lag0 & 1;
+  const uint32_t bar0 = rc_smaddr(bar), bar1 = rc_smaddr(bar + 1);
+
+  // block b -> copies into buffer kb (thread 0 only)
+  auto issue = [&](long long b, int kb) {
+    const uint32_t mb = kb ? bar1 : bar0;
+    float2* dst = buf + kb * kBufE;
+    if (PACK) {
+      const long long ch = b * a.kpb;
+      const int kc = (int)min((long long)a.kpb, a.nch - ch);
+      const uint32_t bytes = (uint32_t)a.Ns * 8u;
+      rc_expect(mb, bytes * (uint32_t)kc);
+      for (int c = 0; c < kc; ++c)
+        rc_bulk_g2s(rc_smaddr(dst + s + c * a.S - a.lag0), a.raw + (size_t)(ch + c) * a.Ns, bytes, mb);
+    } else {
+      const long long ch = b / a.bpc;
+      const int start = (int)(b - ch * a.bpc) * a.V + a.lag0;
+      const int i0 = max(0, -start), i1 = min(kL, a.Ns - start);
+      const int cs = (s + i0) & ~1;
+      int ce = (s + i1 + 1) & ~1;
+      if (start + ce - s > a.Ns) ce -= 2;   // never read past the channel end (tail element loaded in the edge fix)
+      const uint32_t bytes = ce > cs ? (uint32_t)(ce - cs) * 8u : 0u;
+      rc_expect(mb, bytes);
+      if (bytes) rc_bulk_g2s(rc_smaddr(dst + cs), a.raw + (size_t)ch * a.Ns + (start + cs - s), bytes, mb);
+    }
+  };
+
+  // one-time: zero both staging buffers (the packed gaps stay zero), init the mbarriers
+  for (int i = j; i < kNBuf * kBufE; i += kFT) buf[i] = make_float2(0.f, 0.f);
+  if (j == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar1));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  rc_fence_async();
+  __syncthreads();
+  const long long G = gridDim.x;
+  if (j == 0) {
+    if (blockIdx.x < a.nblk) issue(blockIdx.x, 0);
+    if (kNBuf > 1 && blockIdx.x + G < a.nblk) issue(blockIdx.x + G, 1);
+  }
+  float2 v[16];
+  int t = 0;
+  for (long long b = blockIdx.x; b < a.nblk; b += G, ++t) {
+    const int kb = kNBuf > 1 ? (t & 1) : 0;
+    float2* in = buf + kb * kBufE;
+    rc_wait(kb ? bar1 : bar0, (uint32_t)(kNBuf > 1 ? t >> 1 : t) & 1u);
+    long long ch;
+    int n0 = 0, kc = 0;
+    if (PACK) {
+      ch = b * a.kpb;
+      kc = (int)min((long long)a.kpb, a.nch - ch);
+      if (kc < a.kpb) {   // ragged last block: clear the slots of the missing records (stale data)
+        for (int i = s + kc * a.S; i < s + kL; i += kFT) if (i + j < s + kL) in[i + j] = make_float2(0.f, 0.f);
+        rc_fence_async();
+        __syncthreads();
+      }
+    } else {
+      ch = b / a.bpc;
+      n0 = (int)(b - ch * a.bpc) * a.V;
+      const int start = n0 + a.lag0;
+      const int i0 = max(0, -start), i1 = min(kL, a.Ns - start);
+      const bool fix = start + ((s + i1 + 1) & ~1) - s > a.Ns;   // issue() left the channel's last element out
+      if (i0 > 0 || i1 < kL || fix) {   // channel edge: zero the span outside the record, copy the tail element
+        for (int i = j; i < i0; i += kFT) in[s + i] = make_float2(0.f, 0.f);
+        for (int i = i1 + j; i < kL; i += kFT) in[s + i] = make_float2(0.f, 0.f);
+        if (j == 0 && fix) in[s + i1 - 1] = __ldg(a.raw + (size_t)ch * a.Ns + a.Ns - 1);
+        rc_fence_async();
+        __syncthreads();
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = in[s + j + r * kFT];
+#if RC_PIPE_PP
+    // two exchange buffers X = sm, Y = sm2 alternate, so one barrier per exchange suffices: a buffer
+    // is rewritten only after the barrier that follows its last reads
+    pass_store_c<false, 1>(v, sm, a.tw, j);
+    __syncthreads();   // every thread has read this input; X complete
+    if (j == 0 && b + kNBuf * G < a.nblk) issue(b + kNBuf * G, kb);
+    load_smem_c(v, sm, j);
+    pass_store_c<false, 16>(v, sm2, a.tw, j);
+    __syncthreads();
+    load_smem_c(v, sm2, j);
+    pass_regs<false, 256>(v, a.tw, j);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[sig(r)] = cmul(v[sig(r)], __ldg(a.H + j + r * kFT));
+    dft16<true, true>(v);
+    {
+      float2* p = sm + 17 * j;   // pad(16 j + r) = 17 j + r
+#pragma unroll
+      for (int r = 0; r < 16; ++r) p[r] = v[r];
+    }
+    __syncthreads();
+    load_smem_c(v, sm, j);
+    pass_store_c<true, 16>(v, sm2, a.tw, j);
+    __syncthreads();
+    load_smem_c(v, sm2, j);
+    pass_regs<true, 256>(v, a.tw, j);
+#else
+    __syncthreads();   // every thread has read this input and is done with the previous block's exchange reads
+    if (j == 0 && b + kNBuf * G < a.nblk) issue(b + kNBuf * G, kb);
+    // forward FFT (bin j + 256 r left in slot sig(r))
+    pass_store_c<false, 1>(v, sm, a.tw, j);
+    __syncthreads();
+    load_smem_c(v, sm, j);
+    __syncthreads();
+    pass_store_c<false, 16>(v, sm, a.tw, j);
+    __syncthreads();
+    load_smem_c(v, sm, j);
+    pass_regs<false, 256>(v, a.tw, j);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[sig(r)] = cmul(v[sig(r)], __ldg(a.H + j + r * kFT));
+    dft16<true, true>(v);
+    __syncthreads();
+    {
+      float2* p = sm + 17 * j;   // pad(16 j + r) = 17 j + r
+#pragma unroll
+      for (int r = 0; r < 16; ++r) p[r] = v[r];
+    }
+    __syncthreads();
+    load_smem_c(v, sm, j);
+    __syncthreads();
+    pass_store_c<true, 16>(v, sm, a.tw, j);
+    __syncthreads();
+    load_smem_c(v, sm, j);
+    pass_regs<true, 256>(v, a.tw, j);
+#endif
+    if (PACK) {
+      float2* y = a.out + (size_t)ch * a.Ns;
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        const int i = j + r * kFT;
+        const int c = (int)__umulhi((uint32_t)i, a.mS);
+        const int n = i - c * a.S;
+        if (c < kc && n < a.Ns) __stcs(y + (size_t)c * a.Ns + n, v[sig(r)]);
+      }
+    } else {
+      float2* y = a.out + (size_t)ch * a.Ns + n0;
+      const int lim = min(a.V, a.Ns - n0);
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        const int i = j + r * kFT;
+        if (i < lim) __stcs(y + i, v[sig(r)]);
+      }
+    }
+  }
+}
+
 sas_status rc_cuda_fail(const char* what, cudaError_t e) {
   char buf[256];
   snprintf(buf, sizeof(buf), "%s: %s", what, cudaGetErrorString(e));
@@ -385,7 +633,34 @@ static sas_status rc_launch_fft(const float2* raw, long nch, int32_t Ns, const f
   const int V = kL - Nr + 1;
   const int S = Ns + Nr - 1;             // a record's span including the Nr - 1 zeros after it
   const char* nopack = getenv("SASBP_RC_NOPACK");
-  if (S <= kL / 2 && !(nopack && nopack[0] == '1')) {   // >= 2 whole records per transform
+  const bool pack = S <= kL / 2 && !(nopack && nopack[0] == '1');   // >= 2 whole records per transform
+  const char* legacy = getenv("SASBP_RC_LEGACY");
+  if (e == cudaSuccess && (Ns & 1) == 0 && ((uintptr_t)raw & 15) == 0 && !(legacy && legacy[0] == '1')) {
+    RcPipeArgs a;
+    a.raw = raw; a.H = H; a.tw = tw; a.out = out; a.nch = nch; a.Ns = Ns; a.lag0 = lag0;
+    a.V = V & ~1;                        // even block stride: every window start has the parity of lag0
+    a.bpc = (Ns + a.V - 1) / a.V;
+    a.S = (S + 1) & ~1;                  // even record stride: every record starts at an even element
+    a.kpb = kL / a.S;
+    a.mS = 0xFFFFFFFFu / (uint32_t)a.S + 1u;
+    a.nblk = pack ? (nch + a.kpb - 1) / a.kpb : nch * (long long)a.bpc;
+    const size_t smem = ((size_t)kNBuf * kBufE + (size_t)kNX * kPad) * sizeof(float2) + 16;
+    int dev = 0, nsm = 0, occ = 0;
+    auto kern = pack ? rc_pipe_kernel<true> : rc_pipe_kernel<false>;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kFT, smem);
+    if (e == cudaSuccess) {
+      const long long grid = std::min<long long>(a.nblk, (long long)std::max(occ, 1) * nsm);
+      kern<<<(unsigned)grid, kFT, smem, st>>>(a);
+      e = cudaGetLastError();
+    }
+    cudaFreeAsync(H, st);
+    if (e != cudaSuccess) return rc_cuda_fail("rc_pipe_kernel launch", e);
+    return SAS_OK;
+  }
+  if (pack) {
     const int kpb = kL / S;
     const uint32_t mS = 0xFFFFFFFFu / (uint32_t)S + 1u;   // i / S as a multiply-high
     const long long nblk = (nch + kpb - 1) / kpb;

@@ -815,3 +815,30 @@ def test_wave_tail_split(bpmod, monkeypatch):
     scale = np.max(np.abs(b))
     assert np.max(np.abs(a - b)) <= 2e-6 * scale
     assert np.max(np.abs(acc - b)) <= 2e-6 * scale
+
+
+@pytest.mark.parametrize("Ns,Nr,nch,M", [(1024, 160, 257, 0), (10240, 600, 3, 0), (3000, 600, 4, 0), (4096, 1, 2, 0),
+                                          (8192, 2048, 2, 0), (6, 1, 5, 0), (2, 3, 7, 0), (3498, 600, 3, 0),
+                                          (10240, 600, 3, 64), (1024, 160, 31, 64), (3000, 41, 5, 4), (2, 1, 9, 4),
+                                          (4096, 600, 3, 2), (7000, 1793, 2, 256)])
+@pytest.mark.parametrize("impl", ["pipe", "legacy"])
+def test_rangecompress_pipelined_and_legacy(bpmod, Ns, Nr, nch, M, impl, monkeypatch):
+    """K1's bulk-staged persistent kernel (even Ns, aligned input; packed and long records, ragged
+    last blocks, channel-edge windows, odd start lags of the whitened filter) and the per-thread
+    load kernel (SASBP_RC_LEGACY=1) both equal the fp64 correlation (R14) / the oracle's whitening
+    cascade (R21)."""
+    if impl == "legacy":
+        monkeypatch.setenv("SASBP_RC_LEGACY", "1")
+    rng = np.random.default_rng(3 * Ns + Nr + nch + M)
+    rep = (rng.normal(size=Nr) + 1j * rng.normal(size=Nr)).astype(np.complex64) / np.float32(np.sqrt(2 * Nr))
+    raw = ((rng.normal(size=(nch, 1, Ns)) + 1j * rng.normal(size=(nch, 1, Ns))) / np.sqrt(2)).astype(np.complex64)
+    if M == 0:
+        got = bpmod.rangecompress(raw, rep)
+        ref = oracle.rangecompress(raw, rep)
+    else:
+        x = raw.reshape(nch, Ns)
+        G = (0.2 + rng.random(M)).astype(np.float32)
+        G /= G.max()
+        got = bpmod.rangecompress_whitened(x, rep, G)
+        ref = oracle.rangecompress_whitened(x, rep, G.astype(np.float64))
+    assert np.max(np.abs(got - ref)) <= 2e-5 * np.max(np.abs(ref))
