@@ -193,6 +193,28 @@ SASBP_API sas_status sas_bp_set_beam(sas_bp_t h, const sas_beam* beam, const dou
  * Errors: SAS_E_INVALID (non-finite or too fast), SAS_E_NOMEM, SAS_E_CUDA. */
 SASBP_API sas_status sas_bp_set_motion(sas_bp_t h, const double* vel, int32_t P);
 
+/* Tabled receiver trajectories (SURVEY §8(f) NEXT-2 "nav-time interpolation"; the paper keeps the
+ * navigation in a position look-up table, and assumes continual motion; reading
+ * R23): the position of receiver (p, e) during reception is given at K nodes t_k = k dt after
+ * ping p's transmit and interpolated by the cubic Hermite spline with central-difference tangents
+ * (second-order one-sided at the two ends; the end segments' cubics continue outside the table),
+ * which reproduces any quadratic motion exactly -- lever arms turning with the platform's
+ * attitude, sway / surge accelerations.  The transmitter stays at tx_p (instantaneous transmit,
+ * P:92) and the delay solves
+ *   tau = ( |x - tx_p| + |x - r_{p,e}(tau)| ) / c .
+ * The kernel solves it exactly in fp64 at each (tile, channel) reference and follows the
+ * trajectory's tangent line over the tile's delay spread (neglected: |r''| dtau^2 / 2, ~1e-7 m
+ * for 1 m/s^2 over 0.5 ms).  The ping set's rx positions remain the ones the FOV gate uses
+ * (reading R22).
+ *   lut  fp64 [P][E][K][3] NED metres, copied; NULL = no table (back to fixed receivers).
+ *        Replaces velocities set by sas_bp_set_motion (and vice versa: one motion model at a time).
+ *        P and E must match the ping set at form time (else SAS_E_STATE).
+ *   K    3..65536 nodes;  dt  node spacing in seconds (> 0).
+ * Errors: SAS_E_INVALID (non-finite values, K or dt out of range, a node step faster than c/100),
+ * SAS_E_NOMEM, SAS_E_CUDA.  Not combinable with sas_bp_set_medium or sas_bp_set_weighting
+ * (form returns SAS_E_UNSUPPORTED). */
+SASBP_API sas_status sas_bp_set_nav(sas_bp_t h, const double* lut, int32_t P, int32_t E, int32_t K, double dt);
+
 /* Sediment-water refraction (reading R17): a flat interface
  * at z = zb (NED, z down) with sound speed c (create) above and c2 below; each leg's travel time
  * follows Fermat's principle (Snell's law), straight in the water for points above the

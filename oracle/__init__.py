@@ -73,6 +73,19 @@ def _load():
         lib.oracle_tdbp_points_motion.restype = ctypes.c_int
         lib.oracle_delay_moving.argtypes = [f64p, f64p, f64p, f64p, ctypes.c_double]
         lib.oracle_delay_moving.restype = ctypes.c_double
+        lib.oracle_tdbp_points_nav.argtypes = [f32p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, f64p, f64p,
+                                               ctypes.c_int32, ctypes.c_double, f64p, ctypes.c_double,
+                                               ctypes.c_double, ctypes.c_double, f64p, ctypes.c_int64, f64p, i64p]
+        lib.oracle_tdbp_points_nav.restype = ctypes.c_int
+        lib.oracle_nav_eval.argtypes = [f64p, ctypes.c_int32, ctypes.c_double, ctypes.c_double, f64p]
+        lib.oracle_nav_eval.restype = None
+        lib.oracle_delay_nav.argtypes = [f64p, f64p, f64p, ctypes.c_int32, ctypes.c_double, ctypes.c_double]
+        lib.oracle_delay_nav.restype = ctypes.c_double
+        lib.oracle_tdbp_points_gated_nav.argtypes = [f32p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, f64p, f64p,
+                                                     f64p, ctypes.c_int32, ctypes.c_double, f64p, ctypes.c_double,
+                                                     ctypes.c_double, ctypes.c_double, f64p, ctypes.c_double,
+                                                     ctypes.c_double, ctypes.c_int32, f64p, ctypes.c_int64, f64p, i64p]
+        lib.oracle_tdbp_points_gated_nav.restype = ctypes.c_int
         lib.oracle_tdbp_points_refracted.argtypes = [f32p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                                                      f64p, f64p, f64p, ctypes.c_double, ctypes.c_double,
                                                      ctypes.c_double, ctypes.c_double, ctypes.c_double, f64p,
@@ -194,6 +207,73 @@ def tdbp_points_motion(echoes, tx, rx, t0, vel, fc, fs, c, pts, with_count=False
         raise ValueError("oracle_tdbp_points_motion: invalid arguments")
     res = out[:, 0] + 1j * out[:, 1]
     return (res, cnt) if with_count else res
+
+
+def tdbp_points_nav(echoes, tx, lut, dt, t0, fc, fs, c, pts, with_count=False):
+    """TDBP with each receiver on its tabled trajectory lut [P][E][K][3] (nodes dt apart from the
+    transmit; NEXT-2, reading R23)."""
+    lib = _load()
+    echoes = np.ascontiguousarray(echoes, dtype=np.complex64)
+    P, E, Ns = echoes.shape
+    tx = np.ascontiguousarray(tx, dtype=np.float64).reshape(P, 3)
+    lut = np.ascontiguousarray(lut, dtype=np.float64)
+    K = lut.shape[-2]
+    lut = lut.reshape(P, E, K, 3)
+    t0a = None if t0 is None else np.ascontiguousarray(t0, dtype=np.float64).reshape(P)
+    pts = np.ascontiguousarray(pts, dtype=np.float64).reshape(-1, 3)
+    N = pts.shape[0]
+    out = np.zeros((N, 2), dtype=np.float64)
+    cnt = np.zeros(N, dtype=np.int64) if with_count else None
+    rc = lib.oracle_tdbp_points_nav(_p(echoes.view(np.float32), ctypes.c_float), P, E, Ns, _p(tx, ctypes.c_double),
+                                    _p(lut, ctypes.c_double), K, float(dt),
+                                    None if t0a is None else _p(t0a, ctypes.c_double), float(fc), float(fs), float(c),
+                                    _p(pts, ctypes.c_double), N, _p(out, ctypes.c_double),
+                                    None if cnt is None else _p(cnt, ctypes.c_int64))
+    if rc != 0:
+        raise ValueError("oracle_tdbp_points_nav: invalid arguments")
+    res = out[:, 0] + 1j * out[:, 1]
+    return (res, cnt) if with_count else res
+
+
+def tdbp_points_gated_nav(echoes, tx, rx, lut, dt, t0, fc, fs, c, pts, az, el=0.0, bistatic=False, axes=None,
+                          with_count=False):
+    """Gated (R15) TDBP with tabled receiver trajectories (R23); gate on the recorded positions (R22)."""
+    lib = _load()
+    echoes, P, E, Ns, tx, rx, t0 = _echo_arrays(echoes, tx, rx, t0)
+    lut = np.ascontiguousarray(lut, dtype=np.float64)
+    K = lut.shape[-2]
+    lut = lut.reshape(P, E, K, 3)
+    pts = np.ascontiguousarray(pts, dtype=np.float64).reshape(-1, 3)
+    ax = None if axes is None else np.ascontiguousarray(axes, dtype=np.float64).reshape(P, 2, 3)
+    N = pts.shape[0]
+    out = np.zeros((N, 2), dtype=np.float64)
+    cnt = np.zeros(N, dtype=np.int64) if with_count else None
+    rc = lib.oracle_tdbp_points_gated_nav(_p(echoes, ctypes.c_float), P, E, Ns, _p(tx, ctypes.c_double),
+                                          _p(rx, ctypes.c_double), _p(lut, ctypes.c_double), K, float(dt),
+                                          _p(t0, ctypes.c_double), float(fc), float(fs), float(c),
+                                          _p(ax, ctypes.c_double), float(az), float(el), 1 if bistatic else 0,
+                                          _p(pts, ctypes.c_double), N, _p(out, ctypes.c_double),
+                                          _p(cnt, ctypes.c_int64))
+    if rc != 0:
+        raise ValueError("oracle_tdbp_points_gated_nav: invalid arguments")
+    res = out[:, 0] + 1j * out[:, 1]
+    return (res, cnt) if with_count else res
+
+
+def nav_eval(lut, dt, t):
+    """The R23 trajectory interpolant of one (ping, element) table lut [K][3] at time t."""
+    lut = np.ascontiguousarray(lut, dtype=np.float64).reshape(-1, 3)
+    r = np.zeros(3)
+    _load().oracle_nav_eval(_p(lut, ctypes.c_double), lut.shape[0], float(dt), float(t), _p(r, ctypes.c_double))
+    return r
+
+
+def delay_nav(x, tx, lut, dt, c):
+    """The R23 two-way delay of one point / transmitter / receiver table."""
+    a = [np.ascontiguousarray(q, dtype=np.float64).reshape(3) for q in (x, tx)]
+    lut = np.ascontiguousarray(lut, dtype=np.float64).reshape(-1, 3)
+    return float(_load().oracle_delay_nav(_p(a[0], ctypes.c_double), _p(a[1], ctypes.c_double),
+                                          _p(lut, ctypes.c_double), lut.shape[0], float(dt), float(c)))
 
 
 def tdbp_points_refracted(echoes, tx, rx, t0, zb, c2, fc, fs, c, pts, with_count=False):

@@ -34,7 +34,7 @@
  * S:195):  y[n] = sum_{m=0}^{Nr-1} x[n+m] * conj(r[m]),  x[k] = 0 for k >= Ns,
  * the direct O(Ns*Nr) correlation in fp64.
  *
- * NEXT rows: gating (R15), moving receiver (R16), sediment refraction (R17),
+ * NEXT rows: gating (R15), moving receiver (R16; tabled trajectories R23), sediment refraction (R17),
  * and the NEXT-4 interpolation / conditioning variants -- spreading weight R_tx R_rx (R18),
  * 8-tap windowed-sinc xU upsampling (R19), passband basebanding (R20) and spectral whitening
  * (R21).
@@ -709,4 +709,140 @@ int oracle_num_threads(void) {
 #else
   return 1;
 #endif
+}
+
+/*
+ * Receiver position during reception from a position table (NEXT-2, reading R23 in DESIGN.md;
+ * the paper keeps the navigation in a position look-up table, and its motion model
+ * assumes continual motion).  For one (ping, element) the table holds K >= 3 positions
+ * r_k at the times t_k = k dt after the ping's transmit; between nodes the position is the cubic
+ * Hermite spline through them with the tangents
+ *     m_k     = (r_{k+1} - r_{k-1}) / (2 dt)                 0 < k < K-1
+ *     m_0     = (-3 r_0 + 4 r_1 - r_2) / (2 dt)
+ *     m_{K-1} = (3 r_{K-1} - 4 r_{K-2} + r_{K-3}) / (2 dt)
+ * (all exact for quadratic motion, so a quadratic trajectory is reproduced exactly); before t_0
+ * and after t_{K-1} the first / last segment's cubic is continued.  On segment k with
+ * s = t/dt - k:
+ *     r(t) = h00(s) r_k + h10(s) dt m_k + h01(s) r_{k+1} + h11(s) dt m_{k+1},
+ *     h00 = (1 + 2s)(1 - s)^2,  h10 = s (1 - s)^2,  h01 = s^2 (3 - 2s),  h11 = s^2 (s - 1).
+ */
+static void nav_tangent_dt(const double* lut, int32_t K, int32_t k, double m[3]) {   /* dt * m_k */
+  for (int i = 0; i < 3; ++i) {
+    if (k == 0)
+      m[i] = 0.5 * (-3.0 * lut[i] + 4.0 * lut[3 + i] - lut[6 + i]);
+    else if (k == K - 1)
+      m[i] = 0.5 * (3.0 * lut[3 * (K - 1) + i] - 4.0 * lut[3 * (K - 2) + i] + lut[3 * (K - 3) + i]);
+    else
+      m[i] = 0.5 * (lut[3 * (k + 1) + i] - lut[3 * (k - 1) + i]);
+  }
+}
+
+static void nav_eval(const double* lut, int32_t K, double dt, double t, double r[3]) {
+  double s = t / dt;
+  int32_t k = (int32_t)floor(s);
+  if (k < 0) k = 0;
+  if (k > K - 2) k = K - 2;
+  s -= (double)k;
+  const double h00 = (1.0 + 2.0 * s) * (1.0 - s) * (1.0 - s);
+  const double h10 = s * (1.0 - s) * (1.0 - s);
+  const double h01 = s * s * (3.0 - 2.0 * s);
+  const double h11 = s * s * (s - 1.0);
+  double m0[3], m1[3];
+  nav_tangent_dt(lut, K, k, m0);
+  nav_tangent_dt(lut, K, k + 1, m1);
+  for (int i = 0; i < 3; ++i)
+    r[i] = h00 * lut[3 * k + i] + h10 * m0[i] + h01 * lut[3 * (k + 1) + i] + h11 * m1[i];
+}
+
+/*
+ * Two-way delay with the receiver on the tabled trajectory (R23): the echo from x reaches the
+ * element at tau, when it is at r(tau), the transmitter stationary at tx:
+ *     tau = ( |x - tx| + |x - r(tau)| ) / c ,
+ * fixed-point iteration from tau = (|x - tx| + |x - r(0)|)/c (a contraction for element speeds
+ * below c) until the update is below 1e-18 s.
+ */
+static double delay_nav(const double* x, const double* tx, const double* lut, int32_t K, double dt, double c) {
+  const double rt = dist3(x, tx);
+  double r[3];
+  nav_eval(lut, K, dt, 0.0, r);
+  double tau = (rt + dist3(x, r)) / c;
+  for (int it = 0; it < 200; ++it) {
+    nav_eval(lut, K, dt, tau, r);
+    const double nt = (rt + dist3(x, r)) / c;
+    const double d = fabs(nt - tau);
+    tau = nt;
+    if (d <= 1e-18) break;
+  }
+  return tau;
+}
+
+/*
+ * TDBP with tabled receiver trajectories at explicit points (NEXT-2, R23): the definition with
+ * the delay of delay_nav.  lut: fp64 [P][E][K][3] (NED metres), node spacing dt (s).
+ */
+int oracle_tdbp_points_nav(const float* echoes, int32_t P, int32_t E, int32_t Ns, const double* tx,
+                           const double* lut, int32_t K, double dt, const double* t0, double fc, double fs,
+                           double c, const double* pts, int64_t N, double* out, int64_t* n_in) {
+  if (P < 1 || E < 1 || Ns < 1 || N < 0 || K < 3 || !(dt > 0) || !(c > 0) || !(fs > 0) || !lut) return -1;
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int64_t i = 0; i < N; ++i) {
+    const double* x = pts + 3 * i;
+    double ar = 0.0, ai = 0.0;
+    int64_t cnt = 0;
+    for (int32_t p = 0; p < P; ++p) {
+      const double t0p = t0 ? t0[p] : 0.0;
+      for (int32_t e = 0; e < E; ++e) {
+        const int64_t ch = (int64_t)p * E + e;
+        const float* d = echoes + 2 * ch * (int64_t)Ns;
+        const double tau = delay_nav(x, tx + 3 * p, lut + 3 * (int64_t)K * ch, K, dt, c);
+        cnt += one_term_tau(x, d, Ns, tau, t0p, fc, fs, &ar, &ai);
+      }
+    }
+    out[2 * i] = ar;
+    out[2 * i + 1] = ai;
+    if (n_in) n_in[i] = cnt;
+  }
+  return 0;
+}
+
+/* The table interpolant and the delay alone (for the pins). */
+void oracle_nav_eval(const double* lut, int32_t K, double dt, double t, double* r) { nav_eval(lut, K, dt, t, r); }
+double oracle_delay_nav(const double* x, const double* tx, const double* lut, int32_t K, double dt, double c) {
+  return delay_nav(x, tx, lut, K, dt, c);
+}
+
+/*
+ * Gated TDBP with tabled receiver trajectories (NEXT-1 gate R15 with the NEXT-2 delay R23;
+ * reading R22): the FOV decision is the straight line-of-sight cone test from the positions
+ * recorded at the transmit instant (tx_p, rx_{p,e}); every admitted term takes delay_nav.
+ */
+int oracle_tdbp_points_gated_nav(const float* echoes, int32_t P, int32_t E, int32_t Ns, const double* tx,
+                                 const double* rx, const double* lut, int32_t K, double dt, const double* t0,
+                                 double fc, double fs, double c, const double* axes, double az, double el,
+                                 int32_t bistatic, const double* pts, int64_t N, double* out, int64_t* n_in) {
+  if (P < 1 || E < 1 || Ns < 1 || N < 0 || K < 3 || !(dt > 0) || !(c > 0) || !(fs > 0) || !lut) return -1;
+  static const double def_a[3] = {1.0, 0.0, 0.0}, def_b[3] = {0.0, 1.0, 0.0};
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int64_t i = 0; i < N; ++i) {
+    const double* x = pts + 3 * i;
+    double ar = 0.0, ai = 0.0;
+    int64_t cnt = 0;
+    for (int32_t p = 0; p < P; ++p) {
+      const double* a = axes ? axes + 6 * p : def_a;
+      const double* b = axes ? axes + 6 * p + 3 : def_b;
+      if (!in_fov(x, tx + 3 * p, a, b, az, el)) continue;
+      const double t0p = t0 ? t0[p] : 0.0;
+      for (int32_t e = 0; e < E; ++e) {
+        const int64_t ch = (int64_t)p * E + e;
+        if (bistatic && !in_fov(x, rx + 3 * ch, a, b, az, el)) continue;
+        const float* d = echoes + 2 * ch * (int64_t)Ns;
+        const double tau = delay_nav(x, tx + 3 * p, lut + 3 * (int64_t)K * ch, K, dt, c);
+        cnt += one_term_tau(x, d, Ns, tau, t0p, fc, fs, &ar, &ai);
+      }
+    }
+    out[2 * i] = ar;
+    out[2 * i + 1] = ai;
+    if (n_in) n_in[i] = cnt;
+  }
+  return 0;
 }

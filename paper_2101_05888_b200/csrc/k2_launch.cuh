@@ -83,7 +83,7 @@ cudaError_t launch_family(const TdbpParams& prm, const TmaDesc& tmap, const K2La
     return cudaGetLastError();
   }
   if (WEIGHT) {   // spreading weight (R18): stop-and-hop, straight rays only (checked on the host)
-    if (prm.vel || prm.refract) return cudaErrorNotSupported;
+    if (prm.vel || prm.nav || prm.refract) return cudaErrorNotSupported;
     auto go = [&](auto kern) { return launch_k(kern, nt, prm, tmap, smem, L); };
     if constexpr (KZ > 1 || SASBP_AXIS2D) if (L.tma && L.axis) {   // compact geometry: 3D volumes only
       switch (L.mode) {
@@ -122,9 +122,9 @@ cudaError_t launch_family(const TdbpParams& prm, const TmaDesc& tmap, const K2La
   using TT = std::true_type;
   using FF = std::false_type;
   if constexpr (KZ > 1 || SASBP_AXIS2D)   // compact geometry: 3D volumes only
-    if (L.tma && L.axis) return prm.vel ? pick(TT{}, TT{}, TT{}) : pick(TT{}, FF{}, TT{});
-  if (L.tma) return prm.vel ? pick(TT{}, TT{}, FF{}) : pick(TT{}, FF{}, FF{});
-  return prm.vel ? pick(FF{}, TT{}, FF{}) : pick(FF{}, FF{}, FF{});
+    if (L.tma && L.axis) return (prm.vel || prm.nav) ? pick(TT{}, TT{}, TT{}) : pick(TT{}, FF{}, TT{});
+  if (L.tma) return (prm.vel || prm.nav) ? pick(TT{}, TT{}, FF{}) : pick(TT{}, FF{}, FF{});
+  return (prm.vel || prm.nav) ? pick(FF{}, TT{}, FF{}) : pick(FF{}, FF{}, FF{});
 }
 
 // entry points, one per translation unit (k2_*.cu)

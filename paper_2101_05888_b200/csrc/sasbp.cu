@@ -86,6 +86,11 @@ struct sas_bp_s {
   // continuous receiver motion (sas_bp_set_motion; NEXT-2)
   double* vel = nullptr;
   int vel_P = 0;
+  // tabled receiver trajectories (sas_bp_set_nav; NEXT-2, R23): [P*E][K][3]
+  double* nav = nullptr;
+  int nav_P = 0, nav_E = 0, nav_K = 0;
+  double nav_dt = 0, nav_rmin = INFINITY;   // smallest node-to-grid distance (series truncation bound)
+  double rmin = INFINITY;                   // smallest sensor-to-grid distance of the ping set
   // sediment-water interface (sas_bp_set_medium; NEXT-3)
   int refract = 0;
   double zb = 0, c2 = 0;
@@ -123,12 +128,15 @@ sas_status wait_idle(sas_bp_t h) {
 
 // Mode combinations and per-ping array sizes, checked against the ping set about to be used
 // (P, largest sensor z) BEFORE any state changes.
-sas_status check_modes(sas_bp_t h, int32_t P, double max_sensor_z) {
+sas_status check_modes(sas_bp_t h, int32_t P, double max_sensor_z, int32_t E = -1) {
+  if (E < 0) E = h->E;
   if (h->gate && h->axes && h->axes_P != P) return fail(SAS_E_STATE, "beam axes were given for %d pings, the ping set has %d", h->axes_P, P);
   if (h->vel && h->vel_P != P) return fail(SAS_E_STATE, "velocities were given for %d pings, the ping set has %d", h->vel_P, P);
-  if (h->refract && h->vel) return fail(SAS_E_UNSUPPORTED, "refraction and receiver motion cannot be combined");
+  if (h->nav && (h->nav_P != P || h->nav_E != E))
+    return fail(SAS_E_STATE, "receiver tables were given for %d x %d channels, the ping set has %d x %d", h->nav_P, h->nav_E, P, E);
+  if (h->refract && (h->vel || h->nav)) return fail(SAS_E_UNSUPPORTED, "refraction and receiver motion cannot be combined");
   if (h->refract && !(max_sensor_z < h->zb)) return fail(SAS_E_INVALID, "with an interface every sensor must be in the water (z < zb)");
-  if (h->weight && (h->vel || h->refract)) return fail(SAS_E_UNSUPPORTED, "the spreading weight is defined for stop-and-hop straight rays only");
+  if (h->weight && (h->vel || h->nav || h->refract)) return fail(SAS_E_UNSUPPORTED, "the spreading weight is defined for stop-and-hop straight rays only");
   return SAS_OK;
 }
 
@@ -196,6 +204,24 @@ bool encode_tma(sas_bp_t h, int W) {
   return true;
 }
 
+// receive-leg mode of a launch: tabled receivers may come closer to the grid than the ping set's
+// positions, so the truncation bound takes the nearest table node as well
+int rx_mode(sas_bp_t h) {
+  if (!h->nav) return h->mode;
+  return choose_mode(h->d_max, std::fmin(h->rmin, h->nav_rmin), h->c / h->fc);
+}
+
+// bounding box of the pixel centres grown by the tile sphere radius
+void grid_box(sas_bp_t h, double lo[3], double hi[3]) {
+  const sas_grid& g = h->grid;
+  for (int a = 0; a < 3; ++a) {
+    double v0 = g.origin[a];
+    double ex = (g.nx - 1) * g.step_x[a], ey = (g.ny - 1) * g.step_y[a], ez = (g.nz - 1) * g.step_z[a];
+    lo[a] = v0 + std::fmin(ex, 0.0) + std::fmin(ey, 0.0) + std::fmin(ez, 0.0) - h->d_max;
+    hi[a] = v0 + std::fmax(ex, 0.0) + std::fmax(ey, 0.0) + std::fmax(ez, 0.0) + h->d_max;
+  }
+}
+
 cudaError_t launch_tdbp(sas_bp_t h, float2* image, unsigned long long* counter, int accumulate,
                         bool count, cudaStream_t st, int ch_lo = 0, int ch_hi = -1) {
   sasbp::TdbpParams prm{};
@@ -228,8 +254,9 @@ cudaError_t launch_tdbp(sas_bp_t h, float2* image, unsigned long long* counter, 
   prm.tan_half_el = h->tan_half_el; prm.half_el = h->half_el;
   prm.d_max = h->d_max;
   prm.vel = h->vel;
+  prm.nav = h->nav; prm.nav_k = h->nav_K; prm.nav_dt = h->nav_dt;
   prm.refract = h->refract; prm.zb = h->zb; prm.c2 = h->c2;
-  prm.mode = h->refract ? sasbp::kRefract : h->mode;
+  prm.mode = h->refract ? sasbp::kRefract : rx_mode(h);
   if (h->refract) {   // the window must cover the slowest medium: |grad tau| <= 2 / min(c, c2)
     prm.hw = 2.0 * h->d_max * h->fs / std::min(h->c, h->c2);
     prm.W = (int)std::ceil(2.0 * prm.hw + 4.0) + 3;
@@ -240,7 +267,7 @@ cudaError_t launch_tdbp(sas_bp_t h, float2* image, unsigned long long* counter, 
   if (tma && h->tma_W != prm.W) tma = encode_tma(h, prm.W);
   const char* na = getenv("SASBP_NO_AXIS");   // A/B and test switch: force the general-geometry kernel
   const bool no_axis = na && na[0] == '1';
-  sasbp::K2Launch L{tma, h->axis && !no_axis, h->mode, count, st, &g_last_occ, &g_last_split};
+  sasbp::K2Launch L{tma, h->axis && !no_axis, rx_mode(h), count, st, &g_last_occ, &g_last_split};
   g_last_occ = 0;
   g_last_split = 0;
   const bool g = prm.gate && !count;
@@ -321,6 +348,7 @@ sas_status upload_geo(sas_bp_t h, int32_t P, int32_t E, int32_t Ns, const double
       return fail(SAS_E_INVALID, "delays beyond 1e9 samples (check t0 units and sensor positions)");
   }
   h->mode = choose_mode(h->d_max, rmin, h->c / h->fc);
+  h->rmin = rmin;
   h->P = P; h->E = E; h->Ns = Ns;
   return SAS_OK;
 }
@@ -438,6 +466,7 @@ void sas_bp_destroy(sas_bp_t h) {
   cudaFree(h->counter);
   cudaFree(h->axes);
   cudaFree(h->vel);
+  cudaFree(h->nav);
   if (h->stream) cudaStreamDestroy(h->stream);
   if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
   if (prev >= 0) cudaSetDevice(prev);
@@ -538,7 +567,7 @@ sas_status sas_bp_form_streamed(sas_bp_t h, const float* echoes, int32_t P, int3
   sas_status st = validate_geo(P, E, Ns, tx, rx, t0);
   if (st != SAS_OK) return st;
   // every check that can fail without a CUDA error runs before the handle's state changes
-  if ((st = check_modes(h, P, max_z(P, E, tx, rx))) != SAS_OK) return st;
+  if ((st = check_modes(h, P, max_z(P, E, tx, rx), E)) != SAS_OK) return st;
   CK_H(h, cudaSetDevice(h->device));
   if ((st = wait_idle(h)) != SAS_OK) return st;
   const size_t n = (size_t)P * E * Ns;
@@ -679,6 +708,58 @@ sas_status sas_bp_set_motion(sas_bp_t h, const double* vel, int32_t P) {
   }
   CK_H(h, cudaMemcpy(h->vel, vel, (size_t)P * 3 * sizeof(double), cudaMemcpyHostToDevice));
   h->vel_P = P;
+  if (h->nav) {   // one motion model at a time: velocities replace a receiver table
+    cudaFree(h->nav);
+    h->bytes -= (size_t)h->nav_P * h->nav_E * h->nav_K * 3 * sizeof(double);
+    h->nav = nullptr; h->nav_P = h->nav_E = h->nav_K = 0; h->nav_dt = 0; h->nav_rmin = INFINITY;
+  }
+  return SAS_OK;
+}
+
+sas_status sas_bp_set_nav(sas_bp_t h, const double* lut, int32_t P, int32_t E, int32_t K, double dt) {
+  g_err[0] = 0;
+  if (!h) return fail(SAS_E_INVALID, "handle is NULL");
+  if (h->broken) return fail(SAS_E_CUDA, "handle is in a failed CUDA state; destroy it");
+  auto drop = [&]() {
+    if (h->nav) { cudaFree(h->nav); h->bytes -= (size_t)h->nav_P * h->nav_E * h->nav_K * 3 * sizeof(double); }
+    h->nav = nullptr; h->nav_P = h->nav_E = h->nav_K = 0; h->nav_dt = 0; h->nav_rmin = INFINITY;
+  };
+  if (!lut) {   // back to the ping set's fixed receivers (or velocities, if set)
+    if (sas_status w = wait_idle(h); w != SAS_OK) return w;
+    drop();
+    return SAS_OK;
+  }
+  if (P < 1 || E < 1) return fail(SAS_E_INVALID, "P and E must be >= 1");
+  if (K < 3 || K > 65536) return fail(SAS_E_INVALID, "K must be in 3..65536 (K = %d)", K);
+  if (!(dt > 0) || !std::isfinite(dt)) return fail(SAS_E_INVALID, "dt must be finite and > 0");
+  if ((double)P * E * K > 4.0e9) return fail(SAS_E_INVALID, "P*E*K too large");
+  const size_t nch = (size_t)P * E;
+  double lo[3], hi[3];
+  grid_box(h, lo, hi);
+  double rmin = INFINITY;
+  for (size_t ch = 0; ch < nch; ++ch) {
+    const double* L = lut + ch * (size_t)K * 3;
+    for (int32_t k = 0; k < K; ++k) {
+      if (!finite3(L + 3 * k)) return fail(SAS_E_INVALID, "non-finite table node %d of channel %zu", k, ch);
+      rmin = std::fmin(rmin, dist_to_box(L + 3 * k, lo, hi));
+      if (k > 0) {
+        const double d[3] = {L[3 * k] - L[3 * k - 3], L[3 * k + 1] - L[3 * k - 2], L[3 * k + 2] - L[3 * k - 1]};
+        if (norm3(d) > 0.01 * h->c * dt) return fail(SAS_E_INVALID, "channel %zu moves faster than c/100 between nodes %d and %d", ch, k - 1, k);
+      }
+    }
+  }
+  CK_H(h, cudaSetDevice(h->device));
+  if (sas_status w = wait_idle(h); w != SAS_OK) return w;
+  const size_t n = nch * (size_t)K * 3;
+  if (!h->nav || (size_t)h->nav_P * h->nav_E * h->nav_K * 3 != n) {
+    drop();
+    cudaError_t e = cudaMalloc(&h->nav, n * sizeof(double));
+    if (e != cudaSuccess) { h->nav = nullptr; return fail(SAS_E_NOMEM, "cudaMalloc(nav)"); }
+    h->bytes += n * sizeof(double);
+  }
+  CK_H(h, cudaMemcpy(h->nav, lut, n * sizeof(double), cudaMemcpyHostToDevice));
+  h->nav_P = P; h->nav_E = E; h->nav_K = K; h->nav_dt = dt; h->nav_rmin = rmin;
+  if (h->vel) { cudaFree(h->vel); h->bytes -= (size_t)h->vel_P * 3 * sizeof(double); h->vel = nullptr; h->vel_P = 0; }
   return SAS_OK;
 }
 
@@ -706,7 +787,7 @@ sas_status sas_bp_get_plan(sas_bp_t h, sas_bp_plan* out) {
   if (!h || !out) return fail(SAS_E_INVALID, "NULL argument");
   out->tile[0] = h->TX; out->tile[1] = h->TY; out->tile[2] = h->TZ;
   out->window = h->W;
-  out->rx_mode = h->has_pings ? (h->refract ? 3 : h->mode) : -1;
+  out->rx_mode = h->has_pings ? (h->refract ? 3 : rx_mode(h)) : -1;
   out->tma = h->has_pings ? (h->use_tma ? 1 : 0) : -1;
   out->batch = sasbp::kNB;
   out->ctas_per_sm = h->ctas_per_sm;

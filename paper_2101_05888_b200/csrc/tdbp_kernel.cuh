@@ -158,6 +158,11 @@ struct TdbpParams {
   double d_max;           // tile sphere radius (m)
   // continuous receiver motion (NEXT-2, reading R16): per-ping velocity [P][3] or NULL
   const double* vel;
+  // tabled receiver trajectories (NEXT-2, reading R23): [P*E][nav_k][3] positions nav_dt apart
+  // from the transmit, or NULL (vel and nav are never both set)
+  const double* nav;
+  int nav_k;
+  double nav_dt;
   // sediment-water interface (NEXT-3, reading R17): z = zb, sediment speed c2 (refract != 0)
   int refract;
   double zb, c2;
@@ -342,6 +347,29 @@ __device__ __forceinline__ void pixel_centre64(const TdbpParams& prm, int ix, in
                      __dmul_rn((double)iz, prm.sz[i]));
 }
 
+// Receiver position r and velocity v at time t on a channel's tabled trajectory L [K][3] (R23;
+// the paper's position LUT): the cubic Hermite spline through the nodes (dt apart) with
+// central-difference tangents inside and second-order one-sided tangents at the two ends, the
+// first / last segment's cubic continued outside the table.
+__device__ __forceinline__ void nav_pv(const double* __restrict__ L, int K, double dt, double t, double r[3],
+                                       double v[3]) {
+  double s = t / dt;
+  const int k = (int)fmin(fmax(floor(s), 0.0), (double)(K - 2));
+  s -= (double)k;
+  const double s2 = s * s, s3 = s2 * s;
+  const double h00 = 2.0 * s3 - 3.0 * s2 + 1.0, h10 = s3 - 2.0 * s2 + s, h01 = 3.0 * s2 - 2.0 * s3, h11 = s3 - s2;
+  const double g00 = 6.0 * s2 - 6.0 * s, g10 = 3.0 * s2 - 4.0 * s + 1.0, g11 = 3.0 * s2 - 2.0 * s;
+  const double* a = L + 3 * k;   // node k; node k + 1 at a + 3
+  for (int i = 0; i < 3; ++i) {
+    const double p0 = a[i], p1 = a[3 + i];
+    // dt * tangent at nodes k and k + 1
+    const double m0 = k == 0 ? 0.5 * (4.0 * p1 - 3.0 * p0 - a[6 + i]) : 0.5 * (p1 - a[i - 3]);
+    const double m1 = k + 1 == K - 1 ? 0.5 * (3.0 * p1 - 4.0 * p0 + a[i - 3]) : 0.5 * (a[6 + i] - p0);
+    r[i] = h00 * p0 + h10 * m0 + h01 * p1 + h11 * m1;
+    v[i] = (g00 * (p0 - p1) + g10 * m0 + g11 * m1) / dt;
+  }
+}
+
 // fp64 prologue for one channel (row a2): reference geometry at the tile centre ct (and, for
 // gated kernels, the tile's cone classes).
 template <bool GATE, bool MOTION = false, bool REFRACT = false>
@@ -376,17 +404,36 @@ __device__ __forceinline__ ChanConst chan_prologue(const TdbpParams& prm, int ch
   double urx_m = urx, ury_m = ury, urz_m = urz;   // centre minus the receiver at its reception time
   double r_r = sqrt(urx * urx + ury * ury + urz * urz);
   double kap0 = 1.0, kg[3] = {0.0, 0.0, 0.0};
-  if (MOTION && prm.vel) {
+  if (MOTION && (prm.vel || prm.nav)) {
     // reference delay with the receiver moving at v during reception: c tau = r_t + |c_T - rx - v tau|
     // (fixed point from stop-and-hop, contraction |v|/c); the rx leg below is then taken w.r.t.
     // rx' = rx + v tau_ref, and per pixel tau - tau_ref = (dR_t + dR_r') / (c + w.v), w = unit(x - rx'),
     // i.e. U = dU / (1 + g), g = w.v / c = g0 + g1.d to first order in the pixel offset d.
-    const double* V = prm.vel + 3 * p;
-    double tau = (r_t + r_r) / prm.c;
-    for (int it = 0; it < 6; ++it) {
-      urx_m = urx - V[0] * tau; ury_m = ury - V[1] * tau; urz_m = urz - V[2] * tau;
+    // Tabled trajectories (R23): c tau = r_t + |c_T - r(tau)| from r(0), then rx' = r(tau_ref) and
+    // v = r'(tau_ref): over one tile's delay spread the trajectory is its tangent line (the neglected
+    // |r''| dtau^2 / 2 is ~1e-7 m for 1 m/s^2 over 0.5 ms).
+    double V[3];
+    if (prm.nav) {
+      const double* L = prm.nav + (size_t)ch * (size_t)prm.nav_k * 3;
+      double rp[3];
+      nav_pv(L, prm.nav_k, prm.nav_dt, 0.0, rp, V);
+      urx_m = ct[0] - rp[0]; ury_m = ct[1] - rp[1]; urz_m = ct[2] - rp[2];
       r_r = sqrt(urx_m * urx_m + ury_m * ury_m + urz_m * urz_m);
-      tau = (r_t + r_r) / prm.c;
+      double tau = (r_t + r_r) / prm.c;
+      for (int it = 0; it < 8; ++it) {
+        nav_pv(L, prm.nav_k, prm.nav_dt, tau, rp, V);
+        urx_m = ct[0] - rp[0]; ury_m = ct[1] - rp[1]; urz_m = ct[2] - rp[2];
+        r_r = sqrt(urx_m * urx_m + ury_m * ury_m + urz_m * urz_m);
+        tau = (r_t + r_r) / prm.c;
+      }
+    } else {
+      V[0] = prm.vel[3 * p]; V[1] = prm.vel[3 * p + 1]; V[2] = prm.vel[3 * p + 2];
+      double tau = (r_t + r_r) / prm.c;
+      for (int it = 0; it < 6; ++it) {
+        urx_m = urx - V[0] * tau; ury_m = ury - V[1] * tau; urz_m = urz - V[2] * tau;
+        r_r = sqrt(urx_m * urx_m + ury_m * ury_m + urz_m * urz_m);
+        tau = (r_t + r_r) / prm.c;
+      }
     }
     if (prm.mode == kExact) {
       // near-field plans: the kernel evaluates kappa = |x - rx'| / (|x - rx'| + (u + d).v / c) exactly
@@ -1223,7 +1270,7 @@ __global__ void __launch_bounds__(32 * WY * WZ) count_kernel(const TdbpParams pr
         const float qr = fmaf(kc.ux2, dx[k], fmaf(kc.uy2, dy[k], fmaf(kc.uz2, dz[k], dd[k])));
         const float rt = sqrtf(fmaxf(kc.r2_t + qt, 0.f)), rr = sqrtf(fmaxf(kc.r2_r + qr, 0.f));
         const float tk = kc.kap0 + kc.kgx * dx[k] + kc.kgy * dy[k] + kc.kgz * dz[k];
-        const float kap = (prm.vel && prm.mode == kExact) ? rr / (rr + tk) : tk;
+        const float kap = ((prm.vel || prm.nav) && prm.mode == kExact) ? rr / (rr + tk) : tk;
         const float du = (qt / fmaxf(rt + kc.r_t, 1e-30f) + qr / fmaxf(rr + kc.r_r, 1e-30f)) * (float)prm.k_s * kap;
         // absolute u = k_lo + 0.5 + Wh + (du + urr)
         const float ua = (float)kc.klo + 0.5f + (float)(prm.W >> 1) + (du + kc.urr);

@@ -22,7 +22,7 @@ _NAMES = {0: "SAS_OK", -1: "SAS_E_INVALID", -2: "SAS_E_STATE", -3: "SAS_E_NOMEM"
 
 EXPORTS = ("sas_bp_create", "sas_bp_destroy", "sas_bp_set_pings", "sas_bp_set_pings_device", "sas_bp_form",
            "sas_bp_form_device", "sas_bp_count_terms", "sas_bp_workspace_bytes", "sas_rangecompress",
-           "sas_rangecompress_device", "sas_last_error", "sas_version", "sas_bp_get_plan", "sas_bp_form_streamed", "sas_bp_set_beam", "sas_bp_set_motion", "sas_bp_set_medium",
+           "sas_rangecompress_device", "sas_last_error", "sas_version", "sas_bp_get_plan", "sas_bp_form_streamed", "sas_bp_set_beam", "sas_bp_set_motion", "sas_bp_set_nav", "sas_bp_set_medium",
            "sas_bp_set_weighting", "sas_upsample", "sas_upsample_device", "sas_baseband", "sas_baseband_device",
            "sas_whitening_gain", "sas_whitening_gain_device", "sas_rangecompress_whitened",
            "sas_rangecompress_whitened_device")
@@ -83,6 +83,7 @@ def load_library(path: Optional[str] = None):
         "sas_bp_form_streamed": ([vp, f32p, i32, i32, i32, f64p, f64p, f64p, f32p, i32], ctypes.c_int),
         "sas_bp_set_beam": ([vp, ctypes.POINTER(sas_beam), f64p, i32], ctypes.c_int),
         "sas_bp_set_motion": ([vp, f64p, i32], ctypes.c_int),
+        "sas_bp_set_nav": ([vp, f64p, i32, i32, i32, ctypes.c_double], ctypes.c_int),
         "sas_bp_set_medium": ([vp, ctypes.c_double, ctypes.c_double], ctypes.c_int),
         "sas_bp_set_weighting": ([vp, i32], ctypes.c_int),
         "sas_upsample": ([f32p, i32, i32, i32, f32p], ctypes.c_int),
@@ -313,6 +314,17 @@ class Backprojector:
             return
         v = np.ascontiguousarray(vel, dtype=np.float64).reshape(-1, 3)
         _check(_lib.sas_bp_set_motion(self._h, _ptr(v, ctypes.c_double), v.shape[0]))
+
+    def set_nav(self, lut=None, dt: float = 0.0):
+        """Receivers follow tabled trajectories lut [P][E][K][3] (nodes dt seconds apart from the
+        transmit; NEXT-2, reading R23); None = no table."""
+        if lut is None:
+            _check(_lib.sas_bp_set_nav(self._h, None, 0, 0, 0, 0.0))
+            return
+        a = np.ascontiguousarray(lut, dtype=np.float64)
+        if a.ndim != 4 or a.shape[-1] != 3:
+            raise ValueError("lut must be float64 [P][E][K][3]")
+        _check(_lib.sas_bp_set_nav(self._h, _ptr(a, ctypes.c_double), a.shape[0], a.shape[1], a.shape[2], float(dt)))
 
     def set_medium(self, zb: float = 0.0, c2: float = 0.0):
         """Flat sediment-water interface z = zb with sediment sound speed c2 (NEXT-3); c2 <= 0 =

@@ -365,3 +365,32 @@ def random_case(seed: int, P=3, E=2, Ns=256, n=(9, 7, 3), fc=40e3, fs=50e3, c=C_
     t0 = np.full(P, 2.0 * 1.5 / c) + rng.uniform(0, 1e-4, P)
     ech = ((rng.normal(size=(P, E, Ns)) + 1j * rng.normal(size=(P, E, Ns))) / np.sqrt(2)).astype(np.complex64)
     return dict(echoes=ech, tx=tx, rx=rx, t0=t0, fc=fc, fs=fs, c=c, grid=grid)
+
+
+def nav_table(s: "Scenario", K: int = 8, accel: float = 0.5, yaw_rate_deg: float = 2.0, vel=None, seed: int = 0):
+    """Seeded tabled receiver trajectories for the scenario's pings (input for NEXT-2 reading R23,
+    the paper's position look-up table): K nodes dt apart from each transmit covering the
+    record (dt = (max t0 + Ns/fs) / (K - 1)); receiver (p, e) starts at rx[p, e] and moves as
+        r(t) = rx + v_p t + a_p t^2 / 2 + (Rz(w_p t) - I)(rx - tx_p)
+    (platform velocity v_p -- the scenario's vel, else the given / a seeded one --, a seeded
+    acceleration a_p, and the lever arm turning at a seeded yaw rate w_p).  Returns (lut [P][E][K][3], dt)."""
+    rng = np.random.default_rng(seed)
+    P, E = s.P, s.E
+    T = float(np.max(s.t0)) + s.Ns / s.fs
+    dt = T / (K - 1)
+    if vel is None:
+        vel = s.vel if s.vel is not None else rng.normal(size=(P, 3)) * np.array([1.0, 0.3, 0.1])
+    vel = np.asarray(vel, dtype=np.float64).reshape(P, 3)
+    acc = rng.normal(size=(P, 3)) * accel
+    w = np.deg2rad(yaw_rate_deg) * rng.normal(size=P)
+    t = np.arange(K) * dt
+    lever = s.rx - s.tx[:, None, :]                                  # [P][E][3]
+    ang = w[:, None] * t[None, :]                                     # [P][K]
+    cs, sn = np.cos(ang) - 1.0, np.sin(ang)
+    dlx = cs[:, None, :] * lever[:, :, None, 0] - sn[:, None, :] * lever[:, :, None, 1]
+    dly = sn[:, None, :] * lever[:, :, None, 0] + cs[:, None, :] * lever[:, :, None, 1]
+    lut = (s.rx[:, :, None, :] + vel[:, None, None, :] * t[None, None, :, None]
+           + 0.5 * acc[:, None, None, :] * (t * t)[None, None, :, None])
+    lut[..., 0] += dlx
+    lut[..., 1] += dly
+    return np.ascontiguousarray(lut), dt

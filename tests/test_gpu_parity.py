@@ -842,3 +842,97 @@ def test_rangecompress_pipelined_and_legacy(bpmod, Ns, Nr, nch, M, impl, monkeyp
         got = bpmod.rangecompress_whitened(x, rep, G)
         ref = oracle.rangecompress_whitened(x, rep, G.astype(np.float64))
     assert np.max(np.abs(got - ref)) <= 2e-5 * np.max(np.abs(ref))
+
+
+# ------------------------------------------------------------------ NEXT-2: tabled receiver trajectories (R23)
+
+def _nav_form(pkg, s, echoes, lut, dt, beam=None):
+    with pkg.Backprojector(s.fc, s.bandwidth, s.fs, s.c, s.grid) as bp:
+        bp.set_pings(echoes, s.tx, s.rx, s.t0)
+        bp.set_nav(lut, dt)
+        if beam:
+            bp.set_beam(*beam)
+        img = bp.form()
+        return img, bp.count_terms(), bp.plan()
+
+
+@pytest.mark.parametrize("cid,K", [(1, 6), (3, 9), (4, 5)])
+def test_nav_table_vs_oracle(bpmod, cid, K):
+    """Receivers on tabled trajectories (velocity + acceleration + lever arms turning at a yaw
+    rate; the paper's position LUT): full reduced images vs the oracle's per-term fixed
+    point on the interpolated trajectory (config 4 runs the near-field exact receive leg), exact
+    in-window term counts within 1e-4."""
+    s = synth.scenario(cid, reduced=True)
+    e = s.echoes()
+    lut, dt = synth.nav_table(s, K=K, accel=0.8, yaw_rate_deg=3.0, seed=cid)
+    got, (dense, inwin), plan = _nav_form(bpmod, s, e, lut, dt)
+    ref, cnt = oracle.tdbp_points_nav(e, s.tx, lut, dt, s.t0, s.fc, s.fs, s.c, oracle.grid_points(s.grid),
+                                      with_count=True)
+    ref = ref.reshape(got.shape)
+    pk = s.target_pixels
+    pk = pk[np.abs(_at(ref, pk)) > 0.1 * np.abs(ref).max()]
+    _check(got, ref, _at(got, pk), _at(ref, pk), label=f"nav cfg{cid}r")
+    assert abs(inwin - int(cnt.sum())) <= max(1, 1e-4 * cnt.sum())
+
+
+def test_nav_linear_table_matches_set_motion(bpmod):
+    """A table of the constant-velocity trajectory rx + v t images like sas_bp_set_motion (the
+    same reference solution up to fp64 rounding of the spline)."""
+    s = synth.scenario(3, reduced=True)
+    e = s.echoes()
+    rng = np.random.default_rng(9)
+    vel = np.stack([1.5 + 0.2 * rng.normal(size=s.P), 0.3 * rng.normal(size=s.P), 0.1 * rng.normal(size=s.P)], 1)
+    lut, dt = synth.nav_table(s, K=4, accel=0.0, yaw_rate_deg=0.0, vel=vel)
+    a, _, _ = _nav_form(bpmod, s, e, lut, dt)
+    b = _motion_form(bpmod, s, e, vel)
+    assert np.max(np.abs(a - b)) <= 1e-5 * np.max(np.abs(b))
+
+
+@pytest.mark.parametrize("bistatic", [False, True])
+def test_nav_with_gating(bpmod, bistatic):
+    """Tabled trajectories with FOV gating (R22 + R23: gate on the recorded positions): parity with
+    the oracle's gated tabled sum and its in-cone count."""
+    s = synth.scenario(2, reduced=True)
+    e = s.echoes()
+    lut, dt = synth.nav_table(s, K=7, accel=0.5, yaw_rate_deg=2.0, seed=21)
+    az = 2 * np.arcsin(s.sin_half_beam)
+    got, (dense, inwin), _ = _nav_form(bpmod, s, e, lut, dt, beam=(az, 0.0, bistatic))
+    ref, cnt = oracle.tdbp_points_gated_nav(e, s.tx, s.rx, lut, dt, s.t0, s.fc, s.fs, s.c,
+                                            oracle.grid_points(s.grid), az=az, bistatic=bistatic, with_count=True)
+    ref = ref.reshape(got.shape)
+    pk = s.target_pixels
+    pk = pk[np.abs(_at(ref, pk)) > 0.1 * np.abs(ref).max()]
+    _check(got, ref, _at(got, pk), _at(ref, pk), label=f"nav + gate bistatic={bistatic}")
+    assert 0 < inwin < dense
+    assert abs(inwin - int(cnt.sum())) <= max(1, 1e-4 * cnt.sum())
+
+
+def test_set_nav_errors(bpmod):
+    s = synth.scenario(1, reduced=True)
+    e = s.echoes()
+    lut, dt = synth.nav_table(s, K=5)
+    with bpmod.Backprojector(s.fc, s.bandwidth, s.fs, s.c, s.grid) as bp:
+        bp.set_pings(e, s.tx, s.rx, s.t0)
+        for bad_lut, bad_dt in ((lut[:, :, :2], dt), (lut, 0.0), (lut, -1.0), (lut, np.nan)):
+            with pytest.raises(bpmod.SasError):
+                bp.set_nav(bad_lut, bad_dt)
+        nan = lut.copy(); nan[0, 0, 1, 0] = np.nan
+        with pytest.raises(bpmod.SasError):
+            bp.set_nav(nan, dt)
+        fast = lut.copy(); fast[0, 0, 2, 0] += 0.02 * s.c * dt
+        with pytest.raises(bpmod.SasError):
+            bp.set_nav(fast, dt)
+        bp.set_nav(lut[:-1], dt)            # tables for another ping count: form refuses (SAS_E_STATE)
+        with pytest.raises(bpmod.SasError):
+            bp.form()
+        bp.set_nav(lut, dt)
+        bp.set_medium(100.0, 1600.0)        # refraction + motion: unsupported
+        with pytest.raises(bpmod.SasError):
+            bp.form()
+        bp.set_medium(0.0, 0.0)
+        a = bp.form()
+        bp.set_nav(None)                     # back to stop-and-hop
+        b = bp.form()
+    ref = _form(bpmod, s, e)
+    assert np.array_equal(b.view(np.uint32), ref.view(np.uint32))
+    assert not np.array_equal(a, b)

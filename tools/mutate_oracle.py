@@ -55,7 +55,32 @@ MUTATIONS = [
      "      im -= sqrt(G[k]) * sin(a);"),
 ]
 
-TESTS = ["tests/test_oracle_pins.py", "tests/test_oracle_next4.py", "tests/test_oracle_gate_pins.py"]
+MUTATIONS += [
+    ("nav: first-order start tangent",
+     "      m[i] = 0.5 * (-3.0 * lut[i] + 4.0 * lut[3 + i] - lut[6 + i]);",
+     "      m[i] = lut[3 + i] - lut[i];"),
+    ("nav: end tangent sign slip",
+     "      m[i] = 0.5 * (3.0 * lut[3 * (K - 1) + i] - 4.0 * lut[3 * (K - 2) + i] + lut[3 * (K - 3) + i]);",
+     "      m[i] = 0.5 * (3.0 * lut[3 * (K - 1) + i] - 4.0 * lut[3 * (K - 2) + i] - lut[3 * (K - 3) + i]);"),
+    ("nav: Hermite basis h10 with (1 - s) once",
+     "  const double h10 = s * (1.0 - s) * (1.0 - s);",
+     "  const double h10 = s * (1.0 - s);"),
+    ("nav: segment index not clamped below (no continued first cubic)",
+     "  if (k < 0) k = 0;\n  if (k > K - 2) k = K - 2;\n  s -= (double)k;",
+     "  if (k > K - 2) k = K - 2;\n  if (k < 0) { k = 0; s = 0.0; }\n  s -= (double)k;"),
+    ("nav: delay evaluated at the transmit-time receiver position (no fixed point)",
+     "    nav_eval(lut, K, dt, tau, r);\n    const double nt = (rt + dist3(x, r)) / c;",
+     "    const double nt = (rt + dist3(x, r)) / c;"),
+    ("gated_nav: drop the receive-cone gate",
+     "        if (bistatic && !in_fov(x, rx + 3 * ch, a, b, az, el)) continue;\n"
+     "        const float* d = echoes + 2 * ch * (int64_t)Ns;\n"
+     "        const double tau = delay_nav(",
+     "        const float* d = echoes + 2 * ch * (int64_t)Ns;\n"
+     "        const double tau = delay_nav("),
+]
+
+TESTS = ["tests/test_oracle_pins.py", "tests/test_oracle_next4.py", "tests/test_oracle_gate_pins.py",
+         "tests/test_oracle_nav_pins.py"]
 
 
 def main():
