@@ -46,6 +46,9 @@ namespace sasbp {
 #ifndef SASBP_MINB_AXIS
 #define SASBP_MINB_AXIS 4   // the same for axis-aligned grids (A/B on config 4: 5 CTAs/SM -0.7 %)
 #endif
+#ifndef SASBP_MINB_GATE
+#define SASBP_MINB_GATE SASBP_MINB   // the same for the gated (NEXT-1) kernels
+#endif
 #ifndef SASBP_CUNROLL2
 #define SASBP_CUNROLL2 0
 #endif
@@ -60,6 +63,11 @@ namespace sasbp {
 #endif
 #ifndef SASBP_GATE_PREF
 #define SASBP_GATE_PREF 0   // A/B knob: gated series kernels load the next channel's hot constants one channel ahead
+#endif
+#ifndef SASBP_GATE_PRED
+// gated kernels: a gated-out pixel skips its two accumulate FFMA2s under a per-pixel predicate
+// (0: it reads a zero cell instead, an address select of ~3 ALU instructions per pixel)
+#define SASBP_GATE_PRED 0   // A/B on config 2: 135.3 ms (1) vs 123.0 ms (0): the predicated MUFUs cost more than the selects
 #endif
 #ifndef SASBP_GATE_NOINLINE
 #define SASBP_GATE_NOINLINE 0   // A/B knob: the fp64 per-pixel cone tests of edge tiles as out-of-line calls
@@ -92,6 +100,9 @@ namespace sasbp {
 #endif
 #ifndef SASBP_XFORM_CURSOR
 #define SASBP_XFORM_CURSOR 1   // window transform with per-lane cursors (0: indexed form, A/B)
+#endif
+#ifndef SASBP_XFORM_CURSOR_GATE
+#define SASBP_XFORM_CURSOR_GATE 0   // A/B knob: the cursor form in the gated kernels too
 #endif
 #ifndef SASBP_DIV_MULHI
 #define SASBP_DIV_MULHI 1
@@ -648,7 +659,7 @@ SASBP_MASK_FN uint32_t gate_mask(const TdbpParams* prm, const TM tm, int ping, c
 // WEIGHT = true multiplies every term by the spreading weight R_tx R_rx (NEXT-4, reading R18).
 template <int KX, int KY, int KZ, int WY, int WZ, bool HAS_DZ, int MODE, bool USE_TMA, bool GATE = false,
           bool MOTION = false, bool AXIS = false, bool WEIGHT = false>
-__global__ void __launch_bounds__(32 * WY * WZ, (AXIS ? SASBP_MINB_AXIS : SASBP_MINB) * 4 / (WY * WZ))
+__global__ void __launch_bounds__(32 * WY * WZ, (GATE ? SASBP_MINB_GATE : AXIS ? SASBP_MINB_AXIS : SASBP_MINB) * 4 / (WY * WZ))
     tdbp_kernel(SASBP_PRM_QUAL TdbpParams prm,
                                                                           const __grid_constant__ TmaDesc tmap) {
   using TM = TileMap<KX, KY, KZ, WY, WZ>;
@@ -886,7 +897,7 @@ __global__ void __launch_bounds__(32 * WY * WZ, (AXIS ? SASBP_MINB_AXIS : SASBP_
       }
     }
 #else
-    if constexpr (SASBP_XFORM_CURSOR && !SASBP_BININDEX && !GATE) {
+    if constexpr (SASBP_XFORM_CURSOR && !SASBP_BININDEX && (!GATE || SASBP_XFORM_CURSOR_GATE)) {
        // warp w rewrites channels w, w+kWarps, ...: two cells per lane-step, flattened over
        // (channel, cell pair) so the lanes stay busy across channel boundaries.  Each lane keeps
        // cursors (raw source, cell destination, cell coordinate) and advances them by 32 pairs,
@@ -1059,6 +1070,7 @@ __global__ void __launch_bounds__(32 * WY * WZ, (AXIS ? SASBP_MINB_AXIS : SASBP_
           msk = gate_mask<TM, 2 * NP>(&prm, tm, kc.ping, prm.rx + 3 * (size_t)chg, msk);
         }
         masked = (kc.gate & 3) == kGEdge || ((kc.gate >> 2) & 3) == kGEdge;   // warp-uniform
+        if (SASBP_GATE_PRED && !masked) msk = 0xFFFFFFFFu;   // IN channel: every pixel accumulates
       }
 #if SASBP_BININDEX
       const float urrv = kc.urr + voff;                            // V = U' + urrv
@@ -1145,7 +1157,7 @@ __global__ void __launch_bounds__(32 * WY * WZ, (AXIS ? SASBP_MINB_AXIS : SASBP_
   #else
             uint32_t addr = (uint32_t)__float_as_int(Ts) * 16u + (uint32_t)kc.woff;
   #endif
-            if (MSK && masked) {   // gated-out pixel: read the zero cell
+            if (MSK && masked && !SASBP_GATE_PRED) {   // gated-out pixel: read the zero cell
               const uint32_t mk = 0u - ((msk >> (2 * p + s)) & 1u);
               addr = (addr & mk) | (zcell & ~mk);
             }
@@ -1155,6 +1167,7 @@ __global__ void __launch_bounds__(32 * WY * WZ, (AXIS ? SASBP_MINB_AXIS : SASBP_
             float sn, cs;
             __sincosf(phs, &sn, &cs);
             const float2 rot = make_float2(cs, sn);
+            if (MSK && SASBP_GATE_PRED && !((msk >> (2 * p + s)) & 1u)) continue;   // gated out: no accumulate
             A[2 * p + s] = __ffma2_rn(f2(eh.x), rot, A[2 * p + s]);
             B[2 * p + s] = __ffma2_rn(f2(eh.y), rot, B[2 * p + s]);
           }
