@@ -381,6 +381,146 @@ __global__ void __launch_bounds__(256) baseband_blocked_kernel(const float* __re
   }
 }
 
+// ---------------------------------------------------------------- K0, complex-tap form (round 2, the default for D = 4)
+//
+// The mixer commutes with the FIR.  With w(n) = exp(-j 2 pi fc t_n), whose phase is linear in n,
+// w(n_m - k) = w(n_m) exp(+j 2 pi kr k) (kr = fc / fs_in mod 1), so R20's
+//   y[m] = sum_k h[k] x[n_m - k] w(n_m - k)  =  w(n_m) sum_k g[k] x[n_m - k],
+//   g[k] = h[k] exp(+j 2 pi kr k),  n_m = m D + (Nh - 1) / 2 :
+// the FIR runs on the REAL passband samples with complex taps (computed once per CTA, fp64 phase
+// reduction), and one phasor per OUTPUT (exact at the thread's first output, fp32 rotation by
+// exp(-j 2 pi kr D) for the next 7) replaces one per input sample.  No mixing pass, half the
+// staged bytes (4-byte real samples), the same FFMA2 count per tap as the mixed form.  Staging:
+// aligned float4 loads (D = 4, 16-byte aligned rows) de-interleaved into the D polyphase rows;
+// each row keeps 8 samples per 12-word group so a thread's 8-sample window is two conflict-free
+// LDS.128 (lane stride 12 words).
+constexpr int kCtLead = 8;   // words of slack before row 0 (slot -1 of the first float4 lands at -5)
+__host__ __device__ __forceinline__ int ct_pos(int i) { return (i >> 3) * 12 + (i & 7); }
+
+__device__ __forceinline__ void ct_block(float2 (&acc)[kBbR], const float (&wa)[kBbR], const float (&wb)[kBbR],
+                                         const float2* __restrict__ gq) {
+#pragma unroll
+  for (int aa = 0; aa < 8; ++aa) {
+    const float2 g = gq[aa];   // complex tap, same address for the whole warp
+#pragma unroll
+    for (int r = 0; r < kBbR; ++r) {
+      const float v = (r + aa < 8) ? wa[r + aa] : wb[r + aa - 8];
+      acc[r] = __ffma2_rn(make_float2(v, v), g, acc[r]);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(128) baseband_ctap_kernel(const float* __restrict__ x, int E, int Nin, double kr,
+                                                            double fc, const double* __restrict__ t0p,
+                                                            const float* __restrict__ h, int Nh, int Apad, int Nout,
+                                                            int MO, long long runs, int RowW, float2 rotD,
+                                                            float2* __restrict__ out) {
+  constexpr int D = 4;
+  extern __shared__ __align__(16) unsigned char bb_smem[];
+  float2* gs = reinterpret_cast<float2*>(bb_smem);                 // [D][Apad] g_q[a] = g[Nh - 1 - (a D + q)]
+  float* xs = reinterpret_cast<float*>(gs + (size_t)D * Apad) + kCtLead;   // [D][RowW] real polyphase rows
+  const long long b = blockIdx.x;
+  const long long ch = b / runs;
+  const int m0 = (int)(b - ch * runs) * MO;
+  const int half = (Nh - 1) >> 1;
+  const int nlo = m0 * D + half - (Nh - 1);    // local input i = n - nlo = t D + j
+  const int Lq = MO + Apad;
+  const float* xc = x + ch * (long long)Nin;
+  const double bp = bb_base(t0p, ch / E, fc);
+  const int Bd = blockDim.x, tid = threadIdx.x;
+  for (int k = tid; k < D * Apad; k += Bd) {
+    const int q = k / Apad, a = k - q * Apad, j = a * D + q;
+    float2 g = make_float2(0.f, 0.f);
+    if (j < Nh) {
+      const int kk = Nh - 1 - j;                 // tap index
+      double ph = kr * (double)kk;               // cycles, fp64
+      ph -= rint(ph);
+      float sn, cs;
+      __sincosf(6.283185307179586f * (float)ph, &sn, &cs);
+      const float hv = h[kk];
+      g = make_float2(hv * cs, hv * sn);
+    }
+    gs[k] = g;
+  }
+  // staging: float4 k covers local inputs 4 k - o .. 4 k - o + 3; component j -> row (j - o) & 3, slot k + sj
+  const int o = nlo & 3;
+  const int a0 = nlo - o;
+  const int nk = Lq + (o ? 1 : 0);
+  constexpr int kV = 9;
+  for (int k0 = tid; k0 < nk; k0 += kV * Bd) {
+    float4 v[kV];
+#pragma unroll
+    for (int u = 0; u < kV; ++u) {
+      const int k = k0 + u * Bd;
+      const int a = a0 + 4 * k;
+      v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (k < nk) {
+        if (a >= 0 && a + 3 < Nin) {
+          v[u] = __ldcs(reinterpret_cast<const float4*>(xc + a));
+        } else {
+          if (a >= 0 && a < Nin) v[u].x = __ldcs(xc + a);
+          if (a + 1 >= 0 && a + 1 < Nin) v[u].y = __ldcs(xc + a + 1);
+          if (a + 2 >= 0 && a + 2 < Nin) v[u].z = __ldcs(xc + a + 2);
+          if (a + 3 >= 0 && a + 3 < Nin) v[u].w = __ldcs(xc + a + 3);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kV; ++u) {
+      const int k = k0 + u * Bd;
+      if (k >= nk) break;
+      const float vv[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) xs[((j - o) & 3) * RowW + ct_pos(k + ((j - o) >> 2))] = vv[j];
+    }
+  }
+  __syncthreads();
+  const int tt = tid * kBbR;
+  if (tt >= MO || m0 + tt >= Nout) return;
+  float2 acc[kBbR];
+#pragma unroll
+  for (int r = 0; r < kBbR; ++r) acc[r] = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int q = 0; q < D; ++q) {
+    const float* row = xs + q * RowW + ct_pos(tt);   // tt is a multiple of 8: group tt / 8
+    const float2* gq = gs + q * Apad;
+    float wa[kBbR], wb[kBbR];
+    auto ld8 = [&](float (&w)[kBbR], const float* p) {
+      const float4 lo = *reinterpret_cast<const float4*>(p), hi = *reinterpret_cast<const float4*>(p + 4);
+      w[0] = lo.x; w[1] = lo.y; w[2] = lo.z; w[3] = lo.w; w[4] = hi.x; w[5] = hi.y; w[6] = hi.z; w[7] = hi.w;
+    };
+    ld8(wa, row);
+    for (int ab = 0; ab < Apad; ab += 16, row += 24) {
+      ld8(wb, row + 12);
+      ct_block(acc, wa, wb, gq + ab);
+      if (ab + 8 >= Apad) break;
+      ld8(wa, row + 24);
+      ct_block(acc, wb, wa, gq + ab + 8);
+    }
+  }
+  // y[m] = w(n_m) acc, n_m = m D + half: exact phasor at the first output, rotated for the next 7
+  double ph = fma((double)(m0 + tt) * D + half, kr, bp);
+  ph -= rint(ph);
+  float2 w;
+  __sincosf(-6.283185307179586f * (float)ph, &w.y, &w.x);
+  const float2 rotDp = make_float2(-rotD.y, rotD.x);
+  float2* yo = out + ch * (long long)Nout + m0 + tt;
+  float2 y[kBbR];
+#pragma unroll
+  for (int r = 0; r < kBbR; ++r) {
+    if (r) w = __ffma2_rn(make_float2(w.y, w.y), rotDp, __fmul2_rn(make_float2(w.x, w.x), rotD));
+    y[r] = __ffma2_rn(make_float2(acc[r].y, acc[r].y), make_float2(-w.y, w.x), __fmul2_rn(make_float2(acc[r].x, acc[r].x), w));
+  }
+  if (m0 + tt + kBbR <= Nout && ((((uintptr_t)yo) & 15) == 0)) {
+#pragma unroll
+    for (int r = 0; r < kBbR; r += 2) st_cs_v4(yo + r, y[r], y[r + 1]);
+  } else {
+#pragma unroll
+    for (int r = 0; r < kBbR; ++r)
+      if (m0 + tt + r < Nout) __stcs(yo + r, y[r]);
+  }
+}
+
 cudaError_t set_bb_smem(int D, size_t smem) {
   auto kern = D == 2 ? baseband_blocked_kernel<2> : D == 4 ? baseband_blocked_kernel<4>
             : D == 8 ? baseband_blocked_kernel<8> : baseband_blocked_kernel<0>;
@@ -473,6 +613,32 @@ static sas_status bb_launch(const float* x, int32_t P, int32_t E, int32_t Nin, d
   }
   const char* force = getenv("SASBP_BB_SIMPLE");
   cudaError_t e = cudaSuccess;
+  const char* legacy = getenv("SASBP_BB_LEGACY");
+  if (D == 4 && (Nin % 4) == 0 && (((uintptr_t)x) & 15) == 0 && !(force && force[0] == '1') &&
+      !(legacy && legacy[0] == '1')) {
+    // complex-tap kernel (128 threads, 1024 outputs per CTA)
+    const int thr = 128;
+    const int MOb = thr * kBbR;
+    const int Lq = MOb + Apad;
+    const int RowW = ((ct_pos(Lq) + 1 + 8) + 3) & ~3;   // >= 8 words of slack after the last slot
+    const size_t csmem = (size_t)D * Apad * sizeof(float2) + ((size_t)kCtLead + (size_t)D * RowW + 4) * sizeof(float);
+    const long long runs = (Nout + MOb - 1) / MOb;
+    const long long blocks = runs * (long long)P * E;
+    if (blocks > 2147483647LL) return cond_fail(SAS_E_INVALID, "too many channels for one launch");
+    if (csmem <= 200 * 1024) {
+      if (csmem > 48 * 1024)
+        e = cudaFuncSetAttribute(baseband_ctap_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem);
+      if (e == cudaSuccess) {
+        const double aD = 2.0 * 3.141592653589793 * kr * D;
+        baseband_ctap_kernel<<<(unsigned)blocks, thr, csmem, st>>>(
+            x, E, Nin, kr, fc, t0, h, Nh, Apad, Nout, MOb, runs, RowW,
+            make_float2((float)std::cos(aD), (float)-std::sin(aD)), out);
+        e = cudaGetLastError();
+      }
+      if (e != cudaSuccess) return cond_fail(SAS_E_CUDA, "baseband_ctap_kernel", e);
+      return SAS_OK;
+    }
+  }
   if (threads >= 32 && !(force && force[0] == '1')) {
     const int MOb = threads * kBbR;
     const long long runs = (Nout + MOb - 1) / MOb;

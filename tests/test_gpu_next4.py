@@ -392,7 +392,8 @@ def test_weighted_streamed_matches_form(bpmod):
 @pytest.mark.parametrize("Nin,Nh,Nout", [(4096, 63, 1024), (4096, 3, 1024), (4096, 5, 1000), (4096, 7, 1030),
                                          (8192, 1, 2048), (12, 9, 5), (4100, 201, 1025)])
 def test_baseband_vec4_staging(bpmod, Nin, Nh, Nout, monkeypatch):
-    """D = 4 with 16-byte aligned rows stages the passband input with aligned float4 loads; the
+    """D = 4 with 16-byte aligned rows: the complex-tap kernel (default) and the mixed blocked
+    kernel (SASBP_BB_LEGACY=1) stage the passband input with aligned float4 loads; the
     window start nlo = m0 D - (Nh - 1)/2 takes every residue mod 4 over these Nh (o = 0, 3, 2, 1),
     record edges (nlo < 0, the end past Nin) and Nout not a multiple of the CTA's run.  Against the
     fp64 oracle (R20) and the scalar staging path (SASBP_BB_VEC4=0)."""
@@ -406,6 +407,9 @@ def test_baseband_vec4_staging(bpmod, Nin, Nh, Nout, monkeypatch):
     ref = oracle.baseband(x, fs, fc, t0, h, 4, Nout)
     scale = max(np.max(np.abs(ref)), 1e-30)
     assert np.max(np.abs(got - ref)) <= TOL_FILT * scale
-    monkeypatch.setenv("SASBP_BB_VEC4", "0")
+    monkeypatch.setenv("SASBP_BB_LEGACY", "1")        # the mixed blocked kernel, float4 staging
+    mx = bpmod.baseband(x, fs, fc, t0, h, 4, Nout)
+    assert np.max(np.abs(mx - ref)) <= TOL_FILT * scale
+    monkeypatch.setenv("SASBP_BB_VEC4", "0")          # ... and its scalar staging
     sc = bpmod.baseband(x, fs, fc, t0, h, 4, Nout)
     assert np.max(np.abs(sc - ref)) <= TOL_FILT * scale
