@@ -176,7 +176,7 @@ def host_cpu_model():
 
 # ------------------------------------------------------------------ arms
 
-def time_short_kernel(fn, stream, warm_s: float = 0.3, min_ms: float = 100.0, groups: int = 5) -> float:
+def time_short_kernel(fn, stream, warm_s: float = 1.0, min_ms: float = 250.0, groups: int = 5) -> float:
     """ms per call of a short (few-ms) launch sequence: warm up for warm_s of wall time (clocks
     and memory state settle after the host-side gaps between bench phases), then time `groups`
     back-to-back groups of >= min_ms/groups each with CUDA events on `stream` and return the
@@ -492,8 +492,9 @@ def run_sasbp(args):
         k1_ms = time_short_kernel(lambda: pkg.rangecompress_device(echoes_d, rep_d, out_d, stream=stream), stream)
         k1_bytes = 16 * P * E * Ns
         hbm = _measured_hbm()
-        k1 = {"kernel": ("rc_fft_kernel<PACK> (overlap-save, L=4096, %d records per transform)" % (4096 // (Ns + nr - 1))
-                         if Ns + nr - 1 <= 2048 else "rc_fft_kernel (overlap-save, L=4096)"), "Nr": nr, "ms": k1_ms,
+        k1 = {"kernel": ("rc_pipe_kernel<PACK> (bulk-staged persistent overlap-save, L=4096, %d records per transform)"
+                         % (4096 // (Ns + nr - 1)) if Ns + nr - 1 <= 2048 else
+                         "rc_pipe_kernel (bulk-staged persistent overlap-save, L=4096)"), "Nr": nr, "ms": k1_ms,
               "achieved": k1_bytes / (k1_ms * 1e-3) / 1e9, "unit": "GB/s", "bound": "hbm", "peak": hbm[0],
               "peak_source": hbm[1], "frac": k1_bytes / (k1_ms * 1e-3) / 1e9 / hbm[0],
               "algorithmic_bytes": k1_bytes, "note": "16 B per sample: read raw + write compressed once",
@@ -567,7 +568,7 @@ def run_sasbp(args):
                           "whitened_k1_ms": wc_ms,
                           "whitened_k1_GB_per_s": 16 * nch * Ns / (wc_ms * 1e-3) / 1e9,
                           "note": "gain: 8 B read per sample; whitened K1: 16 B per sample, Nr + M - 1 = 663 taps"},
-            "k0_baseband": {"kernel": "baseband_kernel (polyphase, fp64 phase reduction)",
+            "k0_baseband": {"kernel": "baseband_ctap_kernel (complex taps on the real samples, polyphase, fp64 phase reduction)",
                             "shape": f"{nch} channels x {nin} real @ {4 * s.fs / 1e3:.0f} kHz -> {Ns} complex, D=4, "
                                      f"Nh={hbb.size}", "ms": bb_ms, "algorithmic_bytes": bb_bytes,
                             "achieved": bb_bytes / (bb_ms * 1e-3) / 1e9, "unit": "GB/s", "bound": "hbm",

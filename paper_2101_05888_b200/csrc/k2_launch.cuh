@@ -25,6 +25,7 @@ struct K2Launch {
   cudaStream_t st;
   int* occ;          // out: resident CTAs per SM of the launched kernel
   int* split = nullptr;   // out: wave-tail split factor of the launch (1 = none)
+  bool gsplit = false;    // gated: two launches -- IN pairs through a mask-free kernel, then the rest (A/B knob)
 };
 
 template <typename Kern>
@@ -112,6 +113,32 @@ cudaError_t launch_family(const TdbpParams& prm, const TmaDesc& tmap, const K2La
     if (prm.refract) {
       if (M) return cudaErrorNotSupported;   // rejected on the host before launch
       return launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kRefract, T, GATE, false, AX>, nt, prm, tmap, smem, L);
+    }
+    if constexpr (GATE && !M && !WEIGHT) {
+      if (L.gsplit) {
+        // Two-launch gated form: the (tile, channel) pairs wholly inside the cone(s) run a kernel
+        // without per-pixel masks (the dense loop), then the edge pairs accumulate with masks.  The
+        // per-pixel terms and their order within each launch are those of the one-launch form.
+        TdbpParams p1 = prm, p2 = prm;
+        p1.gpart = 1;
+        p2.gpart = 2;
+        p2.accumulate = 1;
+        K2Launch L2 = L;
+        L2.occ = nullptr;
+        L2.split = nullptr;
+        cudaError_t e;
+        switch (L.mode) {
+          case kSeries3: e = launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kSeries3, T, true, false, AX, false, true>, nt, p1, tmap, smem, L); break;
+          case kSeries4: e = launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kSeries4, T, true, false, AX, false, true>, nt, p1, tmap, smem, L); break;
+          default: e = launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kExact, T, true, false, AX, false, true>, nt, p1, tmap, smem, L); break;
+        }
+        if (e != cudaSuccess) return e;
+        switch (L.mode) {
+          case kSeries3: return launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kSeries3, T, true, false, AX>, nt, p2, tmap, smem, L2);
+          case kSeries4: return launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kSeries4, T, true, false, AX>, nt, p2, tmap, smem, L2);
+          default: return launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kExact, T, true, false, AX>, nt, p2, tmap, smem, L2);
+        }
+      }
     }
     switch (L.mode) {
       case kSeries3: return launch_k(tdbp_kernel<KX, KY, KZ, WY, WZ, DZ, kSeries3, T, GATE, M, AX>, nt, prm, tmap, smem, L);

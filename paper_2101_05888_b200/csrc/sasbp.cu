@@ -268,6 +268,10 @@ cudaError_t launch_tdbp(sas_bp_t h, float2* image, unsigned long long* counter, 
   const char* na = getenv("SASBP_NO_AXIS");   // A/B and test switch: force the general-geometry kernel
   const bool no_axis = na && na[0] == '1';
   sasbp::K2Launch L{tma, h->axis && !no_axis, rx_mode(h), count, st, &g_last_occ, &g_last_split};
+  // A/B knob: the two-launch gated form (IN pairs mask-free, then the edge pairs); config 2 with the
+  // generator's beam: 125.4-126.1 ms against 122.9 ms for one launch (profiles/ab_r02.txt), so off
+  const char* g2 = getenv("SASBP_GATE_TWO");
+  L.gsplit = g2 && g2[0] == '1';
   g_last_occ = 0;
   g_last_split = 0;
   const bool g = prm.gate && !count;

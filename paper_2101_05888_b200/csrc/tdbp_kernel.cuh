@@ -104,6 +104,9 @@ namespace sasbp {
 #ifndef SASBP_XFORM_CURSOR_GATE
 #define SASBP_XFORM_CURSOR_GATE 0   // A/B knob: the cursor form in the gated kernels too
 #endif
+#ifndef SASBP_XFORM_CURSOR_GIN
+#define SASBP_XFORM_CURSOR_GIN 0   // A/B knob: the cursor form in the mask-free gated (GIN) kernels
+#endif
 #ifndef SASBP_DIV_MULHI
 #define SASBP_DIV_MULHI 1
 #endif
@@ -163,6 +166,8 @@ struct TdbpParams {
   // field-of-view gating (NEXT-1, reading R15); gate = 0 -> dense sum
   int gate;               // 1 = gate at tx; 2 = gate at tx and at each rx (bistatic)
   int cull;               // skip (tile, channel) pairs whose tile sphere misses a cone
+  int gpart;              // two-launch gated form: 0 = every class, 1 = only (tile, channel) pairs
+                          // wholly inside the cone(s), 2 = only the others (edge / unculled out)
   int az_on, el_on;
   const double* axes;     // [P][2][3] per-ping along-track axis a, boresight b; NULL = (+x, +y)
   double sin_half_az, half_az, tan_half_el, half_el;
@@ -403,6 +408,13 @@ __device__ __forceinline__ ChanConst chan_prologue(const TdbpParams& prm, int ch
       cr_cls = cone_class(prm, vr, a, b);
     }
     if (prm.cull && (ct_cls == kGOut || cr_cls == kGOut)) {
+      ChanConst k{};
+      k.ping = p;
+      k.gate = 16;
+      return k;
+    }
+    const bool in_all = ct_cls == kGIn && cr_cls == kGIn;
+    if ((prm.gpart == 1 && !in_all) || (prm.gpart == 2 && in_all)) {   // the other launch's share
       ChanConst k{};
       k.ping = p;
       k.gate = 16;
@@ -657,8 +669,10 @@ SASBP_MASK_FN uint32_t gate_mask(const TdbpParams* prm, const TM tm, int ping, c
 // true for grids with diagonal steps (each step along its own axis): the pixel offsets are kept
 // per column / row / plane instead of per pixel pair (fewer registers, same arithmetic).
 // WEIGHT = true multiplies every term by the spreading weight R_tx R_rx (NEXT-4, reading R18).
+// GIN = true (gated kernels, prm.gpart = 1): only (tile, channel) pairs wholly inside the cone(s)
+// reach the pixel loop, so it carries no per-pixel gate masks (the dense kernel's loop).
 template <int KX, int KY, int KZ, int WY, int WZ, bool HAS_DZ, int MODE, bool USE_TMA, bool GATE = false,
-          bool MOTION = false, bool AXIS = false, bool WEIGHT = false>
+          bool MOTION = false, bool AXIS = false, bool WEIGHT = false, bool GIN = false>
 __global__ void __launch_bounds__(32 * WY * WZ, (GATE ? SASBP_MINB_GATE : AXIS ? SASBP_MINB_AXIS : SASBP_MINB) * 4 / (WY * WZ))
     tdbp_kernel(SASBP_PRM_QUAL TdbpParams prm,
                                                                           const __grid_constant__ TmaDesc tmap) {
@@ -897,7 +911,7 @@ __global__ void __launch_bounds__(32 * WY * WZ, (GATE ? SASBP_MINB_GATE : AXIS ?
       }
     }
 #else
-    if constexpr (SASBP_XFORM_CURSOR && !SASBP_BININDEX && (!GATE || SASBP_XFORM_CURSOR_GATE)) {
+    if constexpr (SASBP_XFORM_CURSOR && !SASBP_BININDEX && (!GATE || SASBP_XFORM_CURSOR_GATE || (GIN && SASBP_XFORM_CURSOR_GIN))) {
        // warp w rewrites channels w, w+kWarps, ...: two cells per lane-step, flattened over
        // (channel, cell pair) so the lanes stay busy across channel boundaries.  Each lane keeps
        // cursors (raw source, cell destination, cell coordinate) and advances them by 32 pairs,
@@ -1020,7 +1034,7 @@ __global__ void __launch_bounds__(32 * WY * WZ, (GATE ? SASBP_MINB_GATE : AXIS ?
         if constexpr (kPref) {   // the transmit-leg constants, once per ping
           kc.tx2x = cb[c].tx2x; kc.tx2y = cb[c].tx2y; kc.tx2z = cb[c].tx2z; kc.r2_t = cb[c].r2_t; kc.r_t = cb[c].r_t;
         }
-        if (GATE) {   // transmit-cone mask of this thread's pixels for the new ping
+        if (GATE && !GIN) {   // transmit-cone mask of this thread's pixels for the new ping
           mtx = 0xFFu;
           if ((kc.gate & 3) == kGEdge)
             mtx = gate_mask<TM, 2 * NP>(&prm, tm, cur_ping, prm.tx + 3 * cur_ping, (1u << (2 * NP)) - 1u);
@@ -1063,7 +1077,7 @@ __global__ void __launch_bounds__(32 * WY * WZ, (GATE ? SASBP_MINB_GATE : AXIS ?
       }
       uint32_t msk = 0xFFu;
       bool masked = false;
-      if (GATE) {
+      if (GATE && !GIN) {
         msk = mtx;
         if (((kc.gate >> 2) & 3) == kGEdge) {   // receive-cone mask (bistatic), per channel
           const int chg = ch_lo + bat(b) * kNB + c;
@@ -1173,7 +1187,7 @@ __global__ void __launch_bounds__(32 * WY * WZ, (GATE ? SASBP_MINB_GATE : AXIS ?
           }
         }
       };
-      if constexpr (GATE) {
+      if constexpr (GATE && !GIN) {
 #if SASBP_GATE_SPLIT
         if (masked) pixels(std::true_type{}); else pixels(std::false_type{});
 #else

@@ -421,8 +421,13 @@ def _gated_form(bpmod, s, e, az, el=0.0, bistatic=False, cull=True, axes=None):
 
 
 @pytest.mark.parametrize("bistatic", [False, True])
-def test_gated_stripmap_vs_oracle(bpmod, bistatic):
-    """Gated sum with the generator's azimuth beam (P:160 FOV query; R15) on reduced config 2."""
+@pytest.mark.parametrize("launches", ["one", "two"])
+def test_gated_stripmap_vs_oracle(bpmod, bistatic, launches, monkeypatch):
+    """Gated sum with the generator's azimuth beam (P:160 FOV query; R15) on reduced config 2, in
+    the one-launch form and the two-launch A/B form (SASBP_GATE_TWO: mask-free IN pairs, then the
+    edge pairs)."""
+    if launches == "two":
+        monkeypatch.setenv("SASBP_GATE_TWO", "1")
     s = synth.scenario(2, reduced=True)
     e = s.echoes()
     az = 2 * np.arcsin(s.sin_half_beam)
