@@ -27,6 +27,8 @@ def tdbp(s, e, **opt):
             bp.set_beam(*opt["beam"])
         if "vel" in opt:
             bp.set_motion(opt["vel"])
+        if "nav" in opt:
+            bp.set_nav(*opt["nav"])
         if "medium" in opt:
             bp.set_medium(*opt["medium"])
         bp.set_pings(e, s.tx, s.rx, s.t0)
@@ -72,6 +74,36 @@ for M in (2, 48, 64, 256):
     run(f"whitening gain M={M}", lambda: pkg.whitening_gain(x, M, 0.1))
 G = pkg.whitening_gain(x, 64, 0.1)
 run("whitened compression", lambda: pkg.rangecompress_whitened(x, rep, G))
+# round 2: K1 bulk-staged persistent kernel (packed ragged / long records / whitened odd start lag), the legacy K1
+# kernel on even Ns, K0 complex-tap kernel and its legacy mixed form, tabled receiver trajectories, two-launch gating
+xe = (rng.normal(size=(7, 1, 1024)) + 1j * rng.normal(size=(7, 1, 1024))).astype(np.complex64)
+rep160 = (rng.normal(size=160) + 1j * rng.normal(size=160)).astype(np.complex64)
+run("rangecompress pipe packed", lambda: pkg.rangecompress(xe, rep160))
+xl = (rng.normal(size=(2, 2, 3000)) + 1j * rng.normal(size=(2, 2, 3000))).astype(np.complex64)
+run("rangecompress pipe long", lambda: pkg.rangecompress(xl, rep))
+Gl = pkg.whitening_gain(xl, 64, 0.1)
+run("whitened compression pipe (odd lag)", lambda: pkg.rangecompress_whitened(xl.reshape(4, 3000), rep, Gl))
+run("whitened compression pipe packed", lambda: pkg.rangecompress_whitened(xe.reshape(7, 1024), rep160, G))
+os.environ["SASBP_RC_LEGACY"] = "1"
+run("rangecompress legacy even Ns", lambda: pkg.rangecompress(xl, rep))
+del os.environ["SASBP_RC_LEGACY"]
+xb = rng.normal(size=(2, 3, 4096)).astype(np.float32)
+run("baseband ctap", lambda: pkg.baseband(xb, 480e3, 120e3, np.array([0.01, 0.02]), h, 4, 1024))
+os.environ["SASBP_BB_LEGACY"] = "1"
+run("baseband mixed (legacy)", lambda: pkg.baseband(xb, 480e3, 120e3, np.array([0.01, 0.02]), h, 4, 1024))
+del os.environ["SASBP_BB_LEGACY"]
+for cid in (1, 4):
+    sn = synth.scenario(cid, reduced=(cid != 1))
+    sn = sn.subset_pings(np.arange(min(sn.P, 8)))
+    en = sn.echoes()
+    lut, dtn = synth.nav_table(sn, K=5, accel=0.8, yaw_rate_deg=3.0, seed=cid)
+    run(f"nav table cfg{cid}", lambda: tdbp(sn, en, nav=(lut, dtn)))
+s2g = synth.scenario(2, reduced=True).subset_pings(np.arange(12))
+e2g = s2g.echoes()
+azg = 2 * float(np.arcsin(s2g.sin_half_beam))
+os.environ["SASBP_GATE_TWO"] = "1"
+run("gated two-launch cfg2", lambda: tdbp(s2g, e2g, beam=(azg, 0.0, True, True)))
+del os.environ["SASBP_GATE_TWO"]
 print("all cases ran")
 # degenerate geometry: sensors on a pixel centre and on a tile centre (with receiver motion)
 import oracle  # noqa: E402  (positions only: grid_points)
