@@ -410,7 +410,10 @@ __device__ __forceinline__ void ct_block(float2 (&acc)[kBbR], const float (&wa)[
   }
 }
 
-__global__ void __launch_bounds__(128) baseband_ctap_kernel(const float* __restrict__ x, int E, int Nin, double kr,
+#ifndef BB_CTAP_MINB
+#define BB_CTAP_MINB 8   // resident CTAs per SM the register allocation targets (64 registers; A/B config 4: 1.82 vs 1.94 ms at 7 CTAs/SM, 70 registers)
+#endif
+__global__ void __launch_bounds__(128, BB_CTAP_MINB) baseband_ctap_kernel(const float* __restrict__ x, int E, int Nin, double kr,
                                                             double fc, const double* __restrict__ t0p,
                                                             const float* __restrict__ h, int Nh, int Apad, int Nout,
                                                             int MO, long long runs, int RowW, float2 rotD,

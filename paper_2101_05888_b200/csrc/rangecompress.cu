@@ -331,12 +331,15 @@ __global__ void __launch_bounds__(kFT, PACK ? RC_MINB_PACK : RC_MINB) rc_fft_ker
 // The same transform as rc_fft_kernel (same blocks, same spectrum product, same outputs), with the
 // block input staged through shared memory instead of loaded by each thread:
 //  * persistent CTAs (RC_PIPE_MINB per SM) walk the blocks with a grid stride;
-//  * each block's input lands in one of two staging buffers by 1D bulk copies (cp.async.bulk
-//    global -> shared, completion counted on the buffer's mbarrier): a long record's block window
-//    is one copy, a packed block's records one copy each, at their positions c S - lag0;
-//  * the copy of block t + 2 is issued as soon as every thread has read block t's input, so it
-//    streams in while blocks t and t + 1 are transformed (rc_fft_kernel issued its 16 loads per
-//    thread and waited: 3.2 long-scoreboard stall cycles per issued instruction, 58 % issue);
+//  * each block's input lands in a staging buffer (RC_PIPE_NBUF of them, default 1) by 1D bulk
+//    copies (cp.async.bulk global -> shared, completion counted on the buffer's mbarrier): a long
+//    record's block window is one copy, a packed block's records one copy each, at their positions
+//    c S - lag0;
+//  * the copy of block t + NBUF is issued as soon as every thread has read block t's input, so it
+//    streams in while block t is transformed (rc_fft_kernel issued its 16 loads per thread and
+//    waited: 3.2 long-scoreboard stall cycles per issued instruction, 58 % issue);
+//  * two exchange buffers in alternation (RC_PIPE_PP): a buffer is rewritten only after the barrier
+//    that follows its last reads, so each exchange needs one barrier (4 per block instead of 8);
 //  * the packed layout's zero gaps are written once per CTA (copies never touch them); a ragged
 //    last block and long-record blocks at a channel edge zero their uncovered span after the wait;
 //  * shared-memory indices are compile-time offsets from one base per pass (pad() distributes over
@@ -395,6 +398,27 @@ __device__ __forceinline__ void pass_store_c(float2 v[16], float2* sm, const flo
 #pragma unroll
   for (int r = 0; r < 16; ++r) p[r * kStep] = v[sig(r)];
 }
+#ifndef RC_TW16
+#define RC_TW16 0   // A/B knob: the NS = 16 passes take their twiddles from a per-CTA shared table
+#endif
+// NS = 16 pass with table twiddles: t16[r - 1][k] = (w, j w) for the forward sign and (conj w, j conj w)
+// for the inverse, w = W_256^{r k}: v w = v.x (w) + v.y (j w) is one FMUL2 + one FFMA2, and no
+// recurrence (the recurrence form spends 14 complex products per pass building w_r = w_1^r)
+template <bool INV>
+__device__ __forceinline__ void pass_store_t16(float2 v[16], float2* sm, const float4* __restrict__ t16, int j) {
+  const int k = j & 15;
+#pragma unroll
+  for (int r = 1; r < 16; ++r) {
+    const float4 t = t16[(r - 1) * 16 + k];
+    v[r] = __ffma2_rn(make_float2(v[r].y, v[r].y), make_float2(t.z, t.w),
+                      __fmul2_rn(make_float2(v[r].x, v[r].x), make_float2(t.x, t.y)));
+  }
+  dft16<INV, false>(v);
+  float2* p = sm + pad((j - k) * 16 + k);
+#pragma unroll
+  for (int r = 0; r < 16; ++r) p[r * 17] = v[sig(r)];
+}
+
 // load_smem with constant offsets: pad(j + 256 r) = pad(j) + 272 r
 __device__ __forceinline__ void load_smem_c(float2 v[16], const float2* sm, int j) {
   const float2* p = sm + pad(j);
@@ -423,6 +447,8 @@ __global__ void __launch_bounds__(kFT, RC_PIPE_MINB) rc_pipe_kernel(const __grid
   float2* sm2 = sm + (kNX - 1) * kPad;
   (void)sm2;
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + kNX * kPad);   // [2]
+  float4* t16 = reinterpret_cast<float4*>(bar + 2);                 // [2][15][16] (RC_TW16)
+  (void)t16;
   const int j = threadIdx.x;
   const int s = a.lag0 & 1;
   const uint32_t bar0 = rc_smaddr(bar), bar1 = rc_smaddr(bar + 1);
@@ -453,6 +479,14 @@ __global__ void __launch_bounds__(kFT, RC_PIPE_MINB) rc_pipe_kernel(const __grid
 
   // one-time: zero both staging buffers (the packed gaps stay zero), init the mbarriers
   for (int i = j; i < kNBuf * kBufE; i += kFT) buf[i] = make_float2(0.f, 0.f);
+  if (RC_TW16) {
+    for (int i = j; i < 2 * 15 * 16; i += kFT) {
+      const int dir = i / 240, r = (i % 240) / 16 + 1, k = i % 16;
+      float2 w = __ldg(a.tw + ((r * k * 16) & (kL - 1)));   // W_4096^{16 r k}, forward sign
+      if (dir) w.y = -w.y;
+      t16[i] = make_float4(w.x, w.y, -w.y, w.x);
+    }
+  }
   if (j == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0));
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar1));
@@ -504,7 +538,7 @@ __global__ void __launch_bounds__(kFT, RC_PIPE_MINB) rc_pipe_kernel(const __grid
     __syncthreads();   // every thread has read this input; X complete
     if (j == 0 && b + kNBuf * G < a.nblk) issue(b + kNBuf * G, kb);
     load_smem_c(v, sm, j);
-    pass_store_c<false, 16>(v, sm2, a.tw, j);
+    if (RC_TW16) pass_store_t16<false>(v, sm2, t16, j); else pass_store_c<false, 16>(v, sm2, a.tw, j);
     __syncthreads();
     load_smem_c(v, sm2, j);
     pass_regs<false, 256>(v, a.tw, j);
@@ -518,7 +552,7 @@ __global__ void __launch_bounds__(kFT, RC_PIPE_MINB) rc_pipe_kernel(const __grid
     }
     __syncthreads();
     load_smem_c(v, sm, j);
-    pass_store_c<true, 16>(v, sm2, a.tw, j);
+    if (RC_TW16) pass_store_t16<true>(v, sm2, t16 + 240, j); else pass_store_c<true, 16>(v, sm2, a.tw, j);
     __syncthreads();
     load_smem_c(v, sm2, j);
     pass_regs<true, 256>(v, a.tw, j);
@@ -530,7 +564,7 @@ __global__ void __launch_bounds__(kFT, RC_PIPE_MINB) rc_pipe_kernel(const __grid
     __syncthreads();
     load_smem_c(v, sm, j);
     __syncthreads();
-    pass_store_c<false, 16>(v, sm, a.tw, j);
+    if (RC_TW16) pass_store_t16<false>(v, sm, t16, j); else pass_store_c<false, 16>(v, sm, a.tw, j);
     __syncthreads();
     load_smem_c(v, sm, j);
     pass_regs<false, 256>(v, a.tw, j);
@@ -546,7 +580,7 @@ __global__ void __launch_bounds__(kFT, RC_PIPE_MINB) rc_pipe_kernel(const __grid
     __syncthreads();
     load_smem_c(v, sm, j);
     __syncthreads();
-    pass_store_c<true, 16>(v, sm, a.tw, j);
+    if (RC_TW16) pass_store_t16<true>(v, sm, t16 + 240, j); else pass_store_c<true, 16>(v, sm, a.tw, j);
     __syncthreads();
     load_smem_c(v, sm, j);
     pass_regs<true, 256>(v, a.tw, j);
@@ -644,7 +678,7 @@ static sas_status rc_launch_fft(const float2* raw, long nch, int32_t Ns, const f
     a.kpb = kL / a.S;
     a.mS = 0xFFFFFFFFu / (uint32_t)a.S + 1u;
     a.nblk = pack ? (nch + a.kpb - 1) / a.kpb : nch * (long long)a.bpc;
-    const size_t smem = ((size_t)kNBuf * kBufE + (size_t)kNX * kPad) * sizeof(float2) + 16;
+    const size_t smem = ((size_t)kNBuf * kBufE + (size_t)kNX * kPad) * sizeof(float2) + 16 + (RC_TW16 ? 480 * 16 : 0);
     int dev = 0, nsm = 0, occ = 0;
     auto kern = pack ? rc_pipe_kernel<true> : rc_pipe_kernel<false>;
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
