@@ -104,6 +104,9 @@ namespace sasbp {
 #ifndef SASBP_XFORM_CURSOR_GATE
 #define SASBP_XFORM_CURSOR_GATE 0   // A/B knob: the cursor form in the gated kernels too
 #endif
+#ifndef SASBP_LAZY_RANGE
+#define SASBP_LAZY_RANGE 0   // A/B knob: the CTA tile / channel range re-derived at each use (raised the 3D kernel 123 -> 128 registers)
+#endif
 #ifndef SASBP_XFORM_CURSOR_GIN
 #define SASBP_XFORM_CURSOR_GIN 0   // A/B knob: the cursor form in the mask-free gated (GIN) kernels
 #endif
@@ -694,16 +697,31 @@ __global__ void __launch_bounds__(32 * WY * WZ, (GATE ? SASBP_MINB_GATE : AXIS ?
   const uint32_t raw_base = (uint32_t)__cvta_generic_to_shared(rawp);
 
   // tile of this CTA and its channel range (a wave-tail tile is shared by tsplit CTAs)
-  int tile = (int)blockIdx.x, ch_lo = prm.ch_lo, ch_hi = prm.ch_hi;
-  bool red = false;
+#if SASBP_LAZY_RANGE
+  // recomputed at each (per-batch) use from blockIdx and the launch constants, so no register stays
+  // live across the pixel loop for them (kept in registers they cost the 2D kernel 2 registers at the
+  // 128 cap and 4 % of its throughput)
+  auto red_cta = [&]() -> bool { return SASBP_TAILSPLIT && prm.tsplit > 1 && (int)blockIdx.x >= prm.tail0; };
+  auto ch_edge = [&](int k) -> int {   // k = 0: first channel, k = 1: one past the last
+    if (!red_cta()) return k ? prm.ch_hi : prm.ch_lo;
+    const int sp = ((int)blockIdx.x - prm.tail0) % prm.tsplit + k;
+    return prm.ch_lo + (int)(((long long)prm.ch_hi - prm.ch_lo) * sp / prm.tsplit);
+  };
+  const int tile = red_cta() ? prm.tail0 + ((int)blockIdx.x - prm.tail0) / prm.tsplit : (int)blockIdx.x;
+#else
+  int tile = (int)blockIdx.x, ch_lo_v = prm.ch_lo, ch_hi_v = prm.ch_hi;
+  bool red_v = false;
   if (SASBP_TAILSPLIT && prm.tsplit > 1 && tile >= prm.tail0) {
     const int r = tile - prm.tail0, sp = r % prm.tsplit;
     const long long n = (long long)prm.ch_hi - prm.ch_lo;
     tile = prm.tail0 + r / prm.tsplit;
-    ch_lo = prm.ch_lo + (int)(n * sp / prm.tsplit);
-    ch_hi = prm.ch_lo + (int)(n * (sp + 1) / prm.tsplit);
-    red = true;
+    ch_lo_v = prm.ch_lo + (int)(n * sp / prm.tsplit);
+    ch_hi_v = prm.ch_lo + (int)(n * (sp + 1) / prm.tsplit);
+    red_v = true;
   }
+  auto red_cta = [&]() -> bool { return red_v; };
+  auto ch_edge = [&](int k) -> int { return k ? ch_hi_v : ch_lo_v; };
+#endif
   const TM tm(prm, tile);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double ct[3];
@@ -785,7 +803,7 @@ __global__ void __launch_bounds__(32 * WY * WZ, (GATE ? SASBP_MINB_GATE : AXIS ?
   // refraction: interface height relative to the tile centre, slownesses in samples per metre
   const float zbr = MODE == kRefract ? (float)(prm.zb - ct[2]) : 0.f;
   const float k1r = (float)(prm.fs / prm.c), k2r = MODE == kRefract ? (float)(prm.fs / prm.c2) : 0.f;
-  const int nch = ch_hi - ch_lo;
+  const int nch = ch_edge(1) - ch_edge(0);
   const int nbatch = (nch + kNB - 1) / kNB;
   // Channel order: every tile visits all batches, starting at a batch offset proportional to
   // its launch rank among the resident CTAs (blockIdx / resident).  CTAs that are resident at
@@ -827,7 +845,7 @@ __global__ void __launch_bounds__(32 * WY * WZ, (GATE ? SASBP_MINB_GATE : AXIS ?
     if (sub < kBPW && bb < nbatch) {
       const int nbb = min(kNB, nch - bat(bb) * kNB);
       if (cl < nbb) {
-        const ChanConst k = chan_prologue<GATE, MOTION, MODE == kRefract>(prm, ch_lo + bat(bb) * kNB + cl, ct, cl,
+        const ChanConst k = chan_prologue<GATE, MOTION, MODE == kRefract>(prm, ch_edge(0) + bat(bb) * kNB + cl, ct, cl,
                                                                          win_base);
         cc[(bb % kRing) * kNB + cl] = k;
         live = !(k.gate & 16);
@@ -844,7 +862,7 @@ __global__ void __launch_bounds__(32 * WY * WZ, (GATE ? SASBP_MINB_GATE : AXIS ?
   auto issue = [&](int b) {
     if (GATE && !blive[b % kRing]) return;   // dead batch: no loads, no mbarrier phase
     const int nb = min(kNB, nch - bat(b) * kNB);
-    const int ch0 = ch_lo + bat(b) * kNB;
+    const int ch0 = ch_edge(0) + bat(b) * kNB;
     const ChanConst* cb = cc + (b % kRing) * kNB;
     const int c0 = warp * kCW;
     const int mine = max(0, min(kCW, nb - c0));
@@ -1080,7 +1098,7 @@ __global__ void __launch_bounds__(32 * WY * WZ, (GATE ? SASBP_MINB_GATE : AXIS ?
       if (GATE && !GIN) {
         msk = mtx;
         if (((kc.gate >> 2) & 3) == kGEdge) {   // receive-cone mask (bistatic), per channel
-          const int chg = ch_lo + bat(b) * kNB + c;
+          const int chg = ch_edge(0) + bat(b) * kNB + c;
           msk = gate_mask<TM, 2 * NP>(&prm, tm, kc.ping, prm.rx + 3 * (size_t)chg, msk);
         }
         masked = (kc.gate & 3) == kGEdge || ((kc.gate >> 2) & 3) == kGEdge;   // warp-uniform
@@ -1204,7 +1222,7 @@ __global__ void __launch_bounds__(32 * WY * WZ, (GATE ? SASBP_MINB_GATE : AXIS ?
     if (tm.valid(prm, k)) {
       float2* o = prm.image + ((size_t)tm.iz(k) * prm.ny + tm.iy(k)) * prm.nx + tm.ix(k);
       float2 v = make_float2(A[k].x - B[k].y, A[k].y + B[k].x);
-      if (red) { atomicAdd(o, v); continue; }   // wave-tail partial (image zeroed by the launch)
+      if (red_cta()) { atomicAdd(o, v); continue; }   // wave-tail partial (image zeroed by the launch)
       if (prm.accumulate) { const float2 a = *o; v.x += a.x; v.y += a.y; }
       *o = v;
     }
