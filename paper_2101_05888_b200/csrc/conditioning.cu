@@ -449,16 +449,19 @@ __global__ void __launch_bounds__(128, BB_CTAP_MINB) baseband_ctap_kernel(const 
   const int o = nlo & 3;
   const int a0 = nlo - o;
   const int nk = Lq + (o ? 1 : 0);
-  constexpr int kV = 9;
-  for (int k0 = tid; k0 < nk; k0 += kV * Bd) {
+  // the kernel runs 128 threads (host launch): slot k + 128 u sits 128 / 8 * 12 = 192 words after slot
+  // k in a row, so each component's store address is one base per thread plus a constant offset
+  constexpr int kV = 9, kThr = 128, kInc = kThr / 8 * 12;
+  const bool interior = a0 >= 0 && a0 + 4 * nk <= Nin;   // CTA-uniform: no per-load bounds tests
+  for (int k0 = tid; k0 < nk; k0 += kV * kThr) {
     float4 v[kV];
 #pragma unroll
     for (int u = 0; u < kV; ++u) {
-      const int k = k0 + u * Bd;
+      const int k = k0 + u * kThr;
       const int a = a0 + 4 * k;
       v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
       if (k < nk) {
-        if (a >= 0 && a + 3 < Nin) {
+        if (interior || (a >= 0 && a + 3 < Nin)) {
           v[u] = __ldcs(reinterpret_cast<const float4*>(xc + a));
         } else {
           if (a >= 0 && a < Nin) v[u].x = __ldcs(xc + a);
@@ -468,13 +471,16 @@ __global__ void __launch_bounds__(128, BB_CTAP_MINB) baseband_ctap_kernel(const 
         }
       }
     }
+    float* base[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) base[j] = xs + ((j - o) & 3) * RowW + ct_pos(k0 + ((j - o) >> 2));
 #pragma unroll
     for (int u = 0; u < kV; ++u) {
-      const int k = k0 + u * Bd;
-      if (k >= nk) break;
-      const float vv[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
-#pragma unroll
-      for (int j = 0; j < 4; ++j) xs[((j - o) & 3) * RowW + ct_pos(k + ((j - o) >> 2))] = vv[j];
+      if (k0 + u * kThr >= nk) break;
+      base[0][u * kInc] = v[u].x;
+      base[1][u * kInc] = v[u].y;
+      base[2][u * kInc] = v[u].z;
+      base[3][u * kInc] = v[u].w;
     }
   }
   __syncthreads();
