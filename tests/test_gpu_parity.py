@@ -941,3 +941,21 @@ def test_set_nav_errors(bpmod):
     ref = _form(bpmod, s, e)
     assert np.array_equal(b.view(np.uint32), ref.view(np.uint32))
     assert not np.array_equal(a, b)
+
+
+def test_nav_table_streamed_and_cpasync(bpmod, monkeypatch):
+    """Tabled trajectories through the chunked host path (form_streamed: per-chunk launches index the
+    table by global channel) and through the cp.async staging fallback equal the plain form."""
+    s = synth.scenario(3, reduced=True)
+    e = s.echoes()
+    lut, dt = synth.nav_table(s, K=6, accel=0.6, yaw_rate_deg=2.5, seed=33)
+    with bpmod.Backprojector(s.fc, s.bandwidth, s.fs, s.c, s.grid) as bp:
+        bp.set_pings(e, s.tx, s.rx, s.t0)
+        bp.set_nav(lut, dt)
+        ref = bp.form()
+        got = bp.form_streamed(e, s.tx, s.rx, s.t0, chunks=3)
+    assert np.max(np.abs(got - ref)) <= 1e-5 * np.max(np.abs(ref))
+    monkeypatch.setenv("SASBP_NO_TMA", "1")
+    got2, _, plan = _nav_form(bpmod, s, e, lut, dt)
+    assert plan["tma"] is False
+    assert np.max(np.abs(got2 - ref)) <= 1e-5 * np.max(np.abs(ref))
