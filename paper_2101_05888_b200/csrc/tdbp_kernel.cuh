@@ -586,6 +586,7 @@ __host__ __device__ inline size_t raw_slot_bytes(int W) { return ((size_t)box_sa
 #define SASBP_BPW 2   // batches per warp in one prologue group (lanes = BPW * kNB <= 32)
 #endif
 constexpr int kBPW = SASBP_BPW;
+static_assert(kBPW * kNB <= 32, "one prologue group runs kBPW batches of kNB channels on the 32 lanes of a warp");
 constexpr int kRing = 8 * kBPW;   // ChanConst batches kept in shared memory (prologues run ahead)
 // after the ring: mbarrier (8 B, +8 pad), zero cell (16 B), per-slot batch-live flags (kRing ints)
 __host__ __device__ inline size_t k2_raw_off() {
@@ -857,6 +858,7 @@ __global__ void __launch_bounds__(32 * WY * WZ, (GATE ? SASBP_MINB_GATE : AXIS ?
   };
   // window loads of batch b: warp w issues the rows of channels [w*kCW, (w+1)*kCW); every warp
   // arrives once on the batch's mbarrier with the byte count of its rows.
+  static_assert(kNB % kWarps == 0, "each warp issues the window rows of kNB / kWarps channels");
   constexpr int kCW = kNB / kWarps;
   auto issue = [&](int b) {
     if (GATE && !blive[b % kRing]) return;   // dead batch: no loads, no mbarrier phase
