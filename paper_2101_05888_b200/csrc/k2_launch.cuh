@@ -186,7 +186,7 @@ cudaError_t k2_launch_3d_w(const TdbpParams& prm, const TmaDesc& tmap, const K2L
 #define SASBP_KY3D 2   // voxels per thread along y (3D)
 #endif
 #ifndef SASBP_KZ3D
-#define SASBP_KZ3D 2   // voxels per thread along z (3D); KY3D * KZ3D = 4 (8 voxels per thread)
+#define SASBP_KZ3D 4   // voxels per thread along z (3D): 2 x KY3D x KZ3D = 16 voxels per thread, tile 16 x 8 x 16
 #endif
 #ifndef SASBP_WZ3D
 #define SASBP_WZ3D 4   // warps per 3D CTA, stacked along z

@@ -46,6 +46,11 @@ namespace sasbp {
 #ifndef SASBP_MINB_AXIS
 #define SASBP_MINB_AXIS 4   // the same for axis-aligned grids (A/B on config 4: 5 CTAs/SM -0.7 %)
 #endif
+#ifndef SASBP_MINB_3D
+#define SASBP_MINB_3D 2   // 3D volume kernels (16 voxels per thread): 2 CTAs/SM, up to 255 registers
+                          // (config 4 A/B: 16x8x16 tiles at 2 CTAs/SM 1431 Gterm/s, 16x8x12 at 3 1399,
+                          // 16x8x8 at 4 1367; profiles/ab_r02.txt)
+#endif
 #ifndef SASBP_MINB_GATE
 #define SASBP_MINB_GATE SASBP_MINB   // the same for the gated (NEXT-1) kernels
 #endif
@@ -677,7 +682,7 @@ SASBP_MASK_FN uint32_t gate_mask(const TdbpParams* prm, const TM tm, int ping, c
 // reach the pixel loop, so it carries no per-pixel gate masks (the dense kernel's loop).
 template <int KX, int KY, int KZ, int WY, int WZ, bool HAS_DZ, int MODE, bool USE_TMA, bool GATE = false,
           bool MOTION = false, bool AXIS = false, bool WEIGHT = false, bool GIN = false>
-__global__ void __launch_bounds__(32 * WY * WZ, (GATE ? SASBP_MINB_GATE : AXIS ? SASBP_MINB_AXIS : SASBP_MINB) * 4 / (WY * WZ))
+__global__ void __launch_bounds__(32 * WY * WZ, (KZ > 1 ? SASBP_MINB_3D : GATE ? SASBP_MINB_GATE : AXIS ? SASBP_MINB_AXIS : SASBP_MINB) * 4 / (WY * WZ))
     tdbp_kernel(SASBP_PRM_QUAL TdbpParams prm,
                                                                           const __grid_constant__ TmaDesc tmap) {
   using TM = TileMap<KX, KY, KZ, WY, WZ>;
@@ -896,7 +901,9 @@ __global__ void __launch_bounds__(32 * WY * WZ, (GATE ? SASBP_MINB_GATE : AXIS ?
   __syncthreads();
   issue(0);
   int cur_ping = -1;
-  uint32_t mtx = 0xFFu;   // transmit-cone pixel mask of the current ping (GATE)
+  static_assert(2 * NP <= 32, "per-pixel gate masks are 32-bit");
+  constexpr uint32_t kAllPx = 2 * NP == 32 ? 0xFFFFFFFFu : (1u << (2 * NP)) - 1u;   // every pixel of a thread
+  uint32_t mtx = kAllPx;   // transmit-cone pixel mask of the current ping (GATE)
 
   uint32_t phase = 0;   // mbarrier parity of the next live batch
   for (int b = 0; b < nbatch; ++b) {
@@ -1054,9 +1061,9 @@ __global__ void __launch_bounds__(32 * WY * WZ, (GATE ? SASBP_MINB_GATE : AXIS ?
           kc.tx2x = cb[c].tx2x; kc.tx2y = cb[c].tx2y; kc.tx2z = cb[c].tx2z; kc.r2_t = cb[c].r2_t; kc.r_t = cb[c].r_t;
         }
         if (GATE && !GIN) {   // transmit-cone mask of this thread's pixels for the new ping
-          mtx = 0xFFu;
+          mtx = kAllPx;
           if ((kc.gate & 3) == kGEdge)
-            mtx = gate_mask<TM, 2 * NP>(&prm, tm, cur_ping, prm.tx + 3 * cur_ping, (1u << (2 * NP)) - 1u);
+            mtx = gate_mask<TM, 2 * NP>(&prm, tm, cur_ping, prm.tx + 3 * cur_ping, kAllPx);
         }
         // transmit leg, exact range-relative form: dR = q / (sqrt(r^2 + q) + r), in samples
 #if SASBP_TX_SERIES
@@ -1094,7 +1101,7 @@ __global__ void __launch_bounds__(32 * WY * WZ, (GATE ? SASBP_MINB_GATE : AXIS ?
           BT[p] = __fmul2_rn(__fmul2_rn(q, make_float2(rcp_approx(den0), rcp_approx(den1))), f2(kfs));
         }
       }
-      uint32_t msk = 0xFFu;
+      uint32_t msk = kAllPx;
       bool masked = false;
       if (GATE && !GIN) {
         msk = mtx;
